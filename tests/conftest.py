@@ -1,0 +1,29 @@
+import os
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "oracle"))
+
+
+def pytest_configure(config):
+    config.addinivalue_line("markers", "gpu: needs a B200 (sm_100a) GPU")
+
+
+def _ensure_oracle_built():
+    so = os.path.join(ROOT, "oracle", "_build", "liboracle.so")
+    if not os.path.exists(so):
+        import subprocess
+        subprocess.check_call(["make", "-C", os.path.join(ROOT, "oracle"),
+                               os.path.join(ROOT, "oracle", "_build", "liboracle.so")])
+
+
+_ensure_oracle_built()
+
+
+@pytest.fixture(scope="session")
+def golden_files():
+    d = os.path.join(ROOT, "tests", "golden")
+    return sorted(os.path.join(d, f) for f in os.listdir(d) if f.endswith(".npz"))
