@@ -1,0 +1,164 @@
+/*
+ * fastclip_b200.h -- C ABI of the B200-native FastCLIP loss step.
+ *
+ * Drop-in boundary for the per-worker loss step of the reference trainer
+ * (proj/core/src/trainer.cpp:427-589). The reference has no FFI: the step is a sequence of
+ * C++ namespace calls (engine::g_values, UTable::update/snapshot, engine::weights_*,
+ * engine::embedding_cotangents, engine::grad_tau_*, opt::temperature_step and the fabric
+ * collectives). Each entry point below cites the reference interface it replaces.
+ *
+ * Conventions: plain pointers and sizes only; embeddings are bf16 row-major [rows x dim]
+ * (the reference's L2-normalised E rows, engine.hpp:45-53), gradients fp32, tables fp64
+ * (state.hpp:37-122). Device pointers are marked (device); one context per rank, not
+ * thread-safe, stream-ordered. Status codes map 1:1 onto errors.hpp:10-60; no C++
+ * exception crosses this boundary; fc_last_error() returns the message of the last failure.
+ */
+#ifndef FASTCLIP_B200_H
+#define FASTCLIP_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Status codes (errors.hpp:10-60). */
+typedef enum {
+  FC_OK = 0,
+  FC_ERR_CONFIG = 1,             /* ConfigError */
+  FC_ERR_SHAPE = 2,              /* ShapeError */
+  FC_ERR_DEGENERATE_BATCH = 3,   /* DegenerateBatchError (B < 2) */
+  FC_ERR_DOMAIN = 4,             /* std::domain_error (tau <= 0, eps < 0, gamma outside (0,1]) */
+  FC_ERR_OWNERSHIP = 5,          /* OwnershipViolation (duplicate ids in one step) */
+  FC_ERR_STALENESS = 6,          /* StalenessError */
+  FC_ERR_COLLECTIVE_SHAPE = 7,   /* CollectiveShapeError */
+  FC_ERR_COLLECTIVE_ABORTED = 8, /* CollectiveAborted (NCCL async error on a peer) */
+  FC_ERR_NUMERIC = 9,            /* NumericError (non-finite tau gradient) */
+  FC_ERR_IO = 10,                /* IoError (table upload/download size mismatch) */
+  FC_ERR_CUDA = 11,              /* CUDA runtime / driver failure */
+  FC_ERR_NCCL = 12,              /* NCCL failure */
+  FC_ERR_UNSUPPORTED = 13        /* shape outside the kernels' contract (e.g. dim % 8 != 0) */
+} fc_status;
+
+/* Variants in the reference's enum order (trainer.hpp:145-153). */
+typedef enum {
+  FC_OPENCLIP_MBCL = 0,
+  FC_SOGCLR = 1,
+  FC_ISOGCLR = 2,
+  FC_FASTCLIP_V0 = 3,
+  FC_FASTCLIP_V1 = 4,
+  FC_FASTCLIP_V2 = 5,
+  FC_FASTCLIP_V3 = 6
+} fc_variant;
+
+/* Fully resolved step configuration: AlgoConfig (trainer.hpp:164-187) restricted to the
+ * loss step + TempConfig (state.hpp:81-89) + AdamConfig (optimizers.hpp:10-15). */
+typedef struct {
+  int32_t variant;            /* fc_variant */
+  int64_t n_train;            /* N: u/tau table size and the v2 1/N prefactor */
+  int32_t dim;                /* d (multiple of 8) */
+  int32_t local_batch;        /* Bl = global batch / world (trainer.hpp:186) */
+  int32_t world;              /* K ranks (one GPU each) */
+  int32_t rank;               /* this rank, owns global rows [rank*Bl, (rank+1)*Bl) */
+  double tau_init;            /* temperature.init */
+  double tau0;                /* projection floor */
+  double rho;                 /* margin (v2/v3) */
+  double tau_lr;              /* temperature.lr */
+  double beta1, beta2, adam_eps;
+  int32_t lr_decay_enabled;   /* TauLrLatch (schedules.hpp:52-59) */
+  double lr_decay_threshold;
+  double lr_decay_factor;
+  int32_t scale_by_tau;       /* loss.scale_by_tau resolved (trainer.cpp:184-194) */
+  int32_t device;             /* CUDA device ordinal */
+  uint8_t nccl_id[128];       /* ncclUniqueId from rank 0 (fc_nccl_unique_id), world > 1 */
+} fc_config;
+
+/* Inputs of one step (trainer.cpp:419-425 outputs + step scalars). */
+typedef struct {
+  const void* e1;             /* (device) bf16 [Bl x dim]: local image embeddings */
+  const void* e2;             /* (device) bf16 [Bl x dim]: local text embeddings */
+  const int32_t* ids;         /* (device) int32 [Bl]: distinct dataset indices of the local batch */
+  double gamma;               /* inner LR gamma_t (GammaSchedule::at, schedules.cpp:25-31) */
+  double eps;                 /* epsilon_t (EpsilonSchedule::at, schedules.cpp:62-65) */
+} fc_step_in;
+
+/* Outputs of one step. */
+typedef struct {
+  float* de1;                 /* (device) fp32 [Bl x dim]: engine::Cotangents::d_e1 */
+  float* de2;                 /* (device) fp32 [Bl x dim]: engine::Cotangents::d_e2 */
+} fc_step_out;
+
+/* Scalars of the last step (read after the step's stream work completes). */
+typedef struct {
+  double loss;                /* exact batch loss at tau^t (losses.cpp:126-180 per variant) */
+  double gtau;                /* all-reduced G_tau (trainer.cpp:572); 0 for v1/v2 */
+  double tau;                 /* global tau after the step (temperature_step) */
+  uint64_t exp_clamps;        /* safe_exp clamps among the local g evaluations */
+  int32_t latched;            /* TauLrLatch state after the step */
+} fc_step_scalars;
+
+/* resolve_algo_config's temperature / loss defaults for `variant` (trainer.cpp:139-194,
+ * config.cpp:36-60). Leaves dim/local_batch/world/rank/device zero. */
+int fc_config_defaults(int32_t variant, int64_t n_train, fc_config* out);
+
+/* GammaSchedule::at (schedules.cpp:25-31), cosine or constant kind. */
+double fc_gamma_at(int32_t cosine, double constant, double gamma_min, int64_t decay_epochs,
+                   int64_t iters_per_epoch, int64_t t);
+/* EpsilonSchedule::at (schedules.cpp:62-65); switch_epoch < 0 = never. */
+double fc_epsilon_at(double initial, double late, int64_t switch_epoch, int64_t epoch);
+
+/* New NCCL unique id (rank 0), to be broadcast to the other ranks out of band. */
+int fc_nccl_unique_id(uint8_t out[128]);
+
+/* Creates a rank context: device u/tau tables (u = 0, tau = init: state.cpp:42-43,105-110),
+ * workspaces, streams and (world > 1) the NCCL communicator. */
+int fc_create(const fc_config* cfg, void** ctx);
+int fc_destroy(void* ctx);
+
+/* One loss step: trainer.cpp:427-589 for this rank. Enqueued on `stream` (cudaStream_t,
+ * NULL = legacy default); asynchronous. Replaces, in order: g_values (engine.cpp:151-176),
+ * UTable::update/snapshot (state.cpp:45-71), the u/tau all-gathers (trainer.cpp:459-487),
+ * weights_* (engine.cpp:37-75), embedding_cotangents (engine.cpp:77-121), grad_tau_*
+ * (engine.cpp:208-266), all_reduce_mean_scalar (fabric.cpp:210-212) and
+ * temperature_step / IndividualTemp::update (optimizers.cpp:77-83, state.cpp:124-131). */
+int fc_loss_step(void* ctx, const fc_step_in* in, fc_step_out* out, void* stream);
+
+/* Waits for the last step and returns its scalars. */
+int fc_step_scalars_get(void* ctx, fc_step_scalars* out);
+
+/* Per-anchor views of the last step for the local rows (host fp64 [Bl] each, may be NULL):
+ * g1/g2 (engine.cpp:151-176), u1/u2 snapshot (state.cpp:57-71; g for MBCL), t1/t2 = tau^t. */
+int fc_local_views(void* ctx, double* g1, double* g2, double* u1, double* u2, double* t1, double* t2);
+
+/* Table checkpoint hooks (UTable / IndividualTemp SoA, state.cpp:73-95,133-162): host fp64
+ * [n_train] arrays; tau/m/v/step arrays only for individual-temperature variants (else NULL). */
+int fc_table_download(void* ctx, double* u1, double* u2, double* tau1, double* tau2, double* m1,
+                      double* v1, int64_t* s1, double* m2, double* v2, int64_t* s2);
+int fc_table_upload(void* ctx, const double* u1, const double* u2, const double* tau1,
+                    const double* tau2, const double* m1, const double* v1, const int64_t* s1,
+                    const double* m2, const double* v2, const int64_t* s2);
+/* Global tau replica state (Replica::tau, tau_adam, latch; trainer.cpp:245-254). */
+int fc_tau_state_get(void* ctx, double* tau, double* m, double* v, int64_t* step, int32_t* latched);
+int fc_tau_state_set(void* ctx, double tau, double m, double v, int64_t step, int32_t latched);
+
+/* Per-phase CUDA-event timing of the step (off by default). Phases: 0 embedding all-gather,
+ * 1 diag + tau^t row parameters, 2 pass-1 similarity statistics, 3 tables/weights/tau update
+ * (+ scalar collectives), 4 pass-2 Q tiles, 5 gradient GEMM. fc_phase_times waits for the
+ * last step and returns milliseconds per phase. */
+int fc_set_phase_timing(void* ctx, int32_t on);
+int fc_phase_times(void* ctx, float* ms, int32_t n);
+
+/* Number of CUDA kernels fc_loss_step enqueues per step (launch accounting for the bench). */
+int fc_kernels_per_step(void* ctx);
+
+/* Raw S = A B^T through the pass-1 tcgen05 tile kernel (diagnostics / kernel unit tests):
+ * a [rows x dim], b [cols x dim] bf16 (device), out fp32 [rows x cols] (device). */
+int fc_debug_similarity(const void* a, const void* b, int32_t rows, int32_t cols, int32_t dim,
+                        float* out, void* stream);
+
+const char* fc_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FASTCLIP_B200_H */

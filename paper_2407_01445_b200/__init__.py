@@ -1,0 +1,7 @@
+"""B200-native FastCLIP loss step (arXiv 2407.01445): sm_100a tcgen05 kernels behind a C ABI.
+
+See DESIGN.md for the hot path, the kernels and their rooflines; fastclip.py for the host
+mirror of the reference's loss-step interface.
+"""
+from .fastclip import (LossStep, FastclipError, StepScalars, config_defaults, debug_similarity,  # noqa: F401
+                       epsilon_at, gamma_at, lib, nccl_unique_id, VARIANTS)

@@ -1,0 +1,76 @@
+// kernels.cuh -- parameter blocks and launchers of the FastCLIP B200 kernels.
+#pragma once
+
+#include <cstdint>
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+namespace fc {
+
+// ---- tiling shared by the two tcgen05 kernels (CTA pair = cluster of 2, cta_group::2) ----
+constexpr int kPairM = 256;      // rows per pair tile (128 per CTA)
+constexpr int kCtaM = 128;       // TMEM lanes / rows per CTA
+constexpr int kPairN = 256;      // columns per pair tile (UMMA N)
+constexpr int kBlockK = 64;      // bf16 per 128-byte swizzle atom
+constexpr int kStages = 4;       // TMA -> MMA ring depth
+constexpr int kEpiWarps = 8;     // 2 per TMEM lane quarter (column halves)
+constexpr int kThreads = (2 + kEpiWarps) * 32;
+constexpr int kStageBytesA = kCtaM * kBlockK * 2;        // 16 KB
+constexpr int kStageBytesB = (kPairN / 2) * kBlockK * 2;  // 16 KB (own half of N)
+constexpr int kSmemBytes = kStages * (kStageBytesA + kStageBytesB) + 1024 /*align*/ + 256 /*barriers*/;
+
+// ---- similarity-tile kernel (pass 1: row statistics; pass 2: Q tiles) ----
+// One "segment" is an S block S' = A B^T with A = E_rows[a_row0 .. a_row0+rows) and
+// B = E_cols[0 .. cols). Segment R: (E1[L], E2[G]); segment C: (E2[L], E1[G]) so that the
+// column statistics / transposed Q of S are row quantities of S'.
+struct SimSeg {
+  int rows;                 // local anchors in this segment
+  int a_row0;               // global index of local row 0 (diagonal masking)
+  int cols;                 // contrast set size (global batch B)
+  const float2* row_stat;   // STATS: [rows] {S_ii, 1/t_i * log2(e)}
+  float2* partial;          // STATS: [rows][n_jt*2] {sum e, sum (s - s_ii) e}
+  const float4* row_par;    // Q: [rows] {S_ii, log2(e)/t_i, coef_i, 0}
+  const float4* col_par;    // Q: [cols] {S_jj, log2(e)/t_j, coef_j, 0}
+  __nv_bfloat16* q;         // Q: [rows][ldq]
+};
+struct SimParams {
+  SimSeg seg[2];
+  int nseg;
+  int d;
+  int ldq;
+  int n_jt;
+  int n_rb[2];
+  int n_items;
+  unsigned long long* clamps;  // STATS: exponent clamps (safe_exp, losses.cpp:22-28)
+};
+
+// ---- weighted-gradient GEMM: out = scale * (Q' X - r o X_local) ----
+struct GemmSeg {
+  int rows;                  // local anchors
+  int x_row0;                // global index of local row 0 (for the r o X_local term)
+  const float* r;            // [rows]
+  const __nv_bfloat16* x;    // [B][d] row-major (the B operand, read for the r term)
+  float* out;                // [rows][d]
+};
+struct GemmParams {
+  GemmSeg seg[2];
+  int nseg;
+  int d;
+  int n_mb[2];
+  int n_nb;
+  int n_split;
+  int kb_total;      // K blocks of 64 over ldq
+  int kb_per_split;
+  int n_items;
+  float scale;       // 1 / (Bl (B-1)), engine.cpp:84-85
+};
+
+enum SimMode { kSimStats = 0, kSimQ = 1, kSimRaw = 2 };
+
+cudaError_t launch_sim(int mode, const SimParams& p, const CUtensorMap* mapA, const CUtensorMap* mapB,
+                       int grid, cudaStream_t s, float* raw_out);
+cudaError_t launch_gemm(const GemmParams& p, const CUtensorMap* mapQ, const CUtensorMap* mapX, int grid,
+                        cudaStream_t s);
+
+}  // namespace fc

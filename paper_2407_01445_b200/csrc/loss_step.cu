@@ -1,0 +1,612 @@
+// loss_step.cu -- host runtime of the B200 FastCLIP loss step behind the C ABI
+// (include/fastclip_b200.h). One LossStep per rank: it owns the dataset-sized u/tau tables
+// in HBM, the per-step workspaces, the TMA descriptors and (world > 1) an NCCL
+// communicator, and enqueues the step of trainer.cpp:427-589 on a CUDA stream:
+//
+//   [K>1] all-gather E1, E2 (bf16)                        trainer.cpp:422-425
+//   diag + tau^t row parameters                           trainer.cpp:428-434
+//   pass 1: tcgen05 S tiles -> row statistics             engine.cpp:151-176, :182-204
+//   table: g, UTable EMA + snapshot, packed payload       state.cpp:45-71
+//   [K>1] all-gather [u1|u2|t1|t2|id] (fp64)              trainer.cpp:459-487
+//   weights for the whole batch, r_i, tau-grad terms      engine.cpp:37-75, :208-266
+//   [K>1] all-reduce [G_tau, loss]                        trainer.cpp:572
+//   tau update (global Adam / v2 per-index Adam)          optimizers.cpp:65-83, state.cpp:124-131
+//   pass 2: tcgen05 S tiles -> bf16 Q' tiles              engine.cpp:91-118 (weights)
+//   tcgen05 GEMM Q' E -> dE1, dE2                         engine.cpp:77-121
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+#include <nccl.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/fastclip_b200.h"
+#include "kernels.cuh"
+#include "table_kernels.cuh"
+
+namespace {
+
+thread_local std::string g_last_error;
+
+struct FcError {
+  int code;
+  std::string msg;
+};
+
+#define FC_CUDA(call)                                                                          \
+  do {                                                                                         \
+    cudaError_t e_ = (call);                                                                   \
+    if (e_ != cudaSuccess)                                                                     \
+      throw FcError{FC_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_)};          \
+  } while (0)
+#define FC_NCCL(call)                                                                          \
+  do {                                                                                         \
+    ncclResult_t r_ = (call);                                                                  \
+    if (r_ != ncclSuccess) throw FcError{FC_ERR_NCCL, std::string(#call) + ": " + ncclGetErrorString(r_)}; \
+  } while (0)
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    FC_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
+    if (q != cudaDriverEntryPointSuccess || !p) throw FcError{FC_ERR_CUDA, "cuTensorMapEncodeTiled unavailable"};
+    fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+// bf16 2D map over a row-major [outer x inner] array with a 128-byte swizzled box.
+CUtensorMap make_map(const void* base, uint64_t inner, uint64_t outer, uint64_t row_bytes, uint32_t box_inner,
+                     uint32_t box_outer) {
+  CUtensorMap m;
+  cuuint64_t dims[2] = {inner, outer};
+  cuuint64_t strides[1] = {row_bytes};
+  cuuint32_t box[2] = {box_inner, box_outer};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, es,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw FcError{FC_ERR_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string(r) + ")"};
+  return m;
+}
+
+template <class T>
+T* dalloc(size_t n) {
+  T* p = nullptr;
+  if (n == 0) n = 1;
+  FC_CUDA(cudaMalloc(&p, n * sizeof(T)));
+  return p;
+}
+
+int sm_count(int dev) {
+  int n = 0;
+  cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  return n > 0 ? n : 148;
+}
+
+bool is_individual(int v) { return v == FC_ISOGCLR || v == FC_FASTCLIP_V2; }
+
+struct LossStep {
+  fc_config cfg{};
+  int B = 0, Bl = 0, d = 0, K = 1, rank = 0, ldq = 0, n_jt = 0, n_sm = 148;
+  bool indiv = false, track_u = true;
+  ncclComm_t comm = nullptr;
+  // tables
+  double *u1 = nullptr, *u2 = nullptr, *tau1 = nullptr, *tau2 = nullptr, *m1 = nullptr, *v1 = nullptr,
+         *m2 = nullptr, *v2 = nullptr;
+  long long *s1 = nullptr, *s2 = nullptr;
+  fc::TauState* tau_state = nullptr;
+  // workspaces
+  __nv_bfloat16 *e1g = nullptr, *e2g = nullptr;   // gathered embeddings (K > 1)
+  float* diag = nullptr;
+  float2 *rowstat = nullptr, *partial = nullptr;
+  unsigned long long* clamps = nullptr;
+  double* f64 = nullptr;   // per-local-anchor fp64 arrays
+  double *send = nullptr, *recv = nullptr, *gt_recv = nullptr, *red = nullptr;
+  float4 *par1 = nullptr, *par2 = nullptr;
+  float* rcoef = nullptr;
+  __nv_bfloat16* q = nullptr;   // [2][Bl][ldq]
+  int* err = nullptr;
+  fc::StepResult* result_d = nullptr;
+  fc::StepResult* result_h = nullptr;   // pinned
+  cudaEvent_t done{};
+  // optional per-phase CUDA events (bench roofline): phases of the last step
+  static constexpr int kPhases = 6;   // gatherE, prep, pass1, scalars, pass2, gemm
+  bool timing = false;
+  cudaEvent_t ev[kPhases + 1]{};
+  void mark(int i, cudaStream_t st) {
+    if (timing) FC_CUDA(cudaEventRecord(ev[i], st));
+  }
+  // cached descriptors
+  const void* map_e1 = nullptr;
+  const void* map_e2 = nullptr;
+  CUtensorMap mE1k, mE2k, mE1n, mE2n, mQ[2];
+  int n_split = 4;
+  fc::StepArgs args{};
+
+  double* F(int i) const { return f64 + static_cast<size_t>(i) * Bl; }
+
+  void init(const fc_config* c) {
+    cfg = *c;
+    K = cfg.world;
+    rank = cfg.rank;
+    Bl = cfg.local_batch;
+    B = Bl * K;
+    d = cfg.dim;
+    if (K < 1 || rank < 0 || rank >= K) throw FcError{FC_ERR_CONFIG, "world/rank out of range"};
+    if (Bl < 1) throw FcError{FC_ERR_CONFIG, "local_batch must be >= 1"};
+    if (B < 2) throw FcError{FC_ERR_DEGENERATE_BATCH, "global batch must have >= 2 pairs"};
+    if (d < 8 || d % 8 != 0) throw FcError{FC_ERR_UNSUPPORTED, "dim must be a positive multiple of 8"};
+    if (cfg.n_train < B) throw FcError{FC_ERR_CONFIG, "n_train smaller than one global batch"};
+    if (cfg.n_train > 0x7fffffffLL) throw FcError{FC_ERR_CONFIG, "n_train must fit int32 ids"};
+    if (cfg.variant < 0 || cfg.variant > 6) throw FcError{FC_ERR_CONFIG, "unknown variant"};
+    if (!(cfg.tau0 > 0.0) || cfg.tau_init < cfg.tau0) throw FcError{FC_ERR_CONFIG, "temperature.init/tau0"};
+    indiv = is_individual(cfg.variant);
+    track_u = cfg.variant != FC_OPENCLIP_MBCL;
+    ldq = (B + 63) / 64 * 64;
+    n_jt = (B + fc::kPairN - 1) / fc::kPairN;
+    FC_CUDA(cudaSetDevice(cfg.device));
+    n_sm = sm_count(cfg.device);
+    if (const char* e = std::getenv("FC_GEMM_SPLIT")) n_split = std::max(1, atoi(e));
+
+    const size_t N = static_cast<size_t>(cfg.n_train);
+    u1 = dalloc<double>(N);
+    u2 = dalloc<double>(N);
+    FC_CUDA(cudaMemset(u1, 0, N * 8));
+    FC_CUDA(cudaMemset(u2, 0, N * 8));
+    if (indiv) {
+      tau1 = dalloc<double>(N); tau2 = dalloc<double>(N);
+      m1 = dalloc<double>(N); v1 = dalloc<double>(N); m2 = dalloc<double>(N); v2 = dalloc<double>(N);
+      s1 = dalloc<long long>(N); s2 = dalloc<long long>(N);
+      std::vector<double> init(N, cfg.tau_init);
+      FC_CUDA(cudaMemcpy(tau1, init.data(), N * 8, cudaMemcpyHostToDevice));
+      FC_CUDA(cudaMemcpy(tau2, init.data(), N * 8, cudaMemcpyHostToDevice));
+      for (double* p : {m1, v1, m2, v2}) FC_CUDA(cudaMemset(p, 0, N * 8));
+      FC_CUDA(cudaMemset(s1, 0, N * 8));
+      FC_CUDA(cudaMemset(s2, 0, N * 8));
+    }
+    tau_state = dalloc<fc::TauState>(1);
+    fc::TauState ts{cfg.tau_init, 0.0, 0.0, 0, 0, 0};
+    FC_CUDA(cudaMemcpy(tau_state, &ts, sizeof(ts), cudaMemcpyHostToDevice));
+
+    if (K > 1) {
+      e1g = dalloc<__nv_bfloat16>(static_cast<size_t>(B) * d);
+      e2g = dalloc<__nv_bfloat16>(static_cast<size_t>(B) * d);
+      ncclUniqueId id;
+      std::memcpy(&id, cfg.nccl_id, sizeof(id));
+      FC_NCCL(ncclCommInitRank(&comm, K, id, rank));
+    }
+    diag = dalloc<float>(B);
+    rowstat = dalloc<float2>(2 * static_cast<size_t>(Bl));
+    partial = dalloc<float2>(2 * static_cast<size_t>(Bl) * n_jt * 2);
+    clamps = dalloc<unsigned long long>(1);
+    f64 = dalloc<double>(static_cast<size_t>(Bl) * 18);
+    send = dalloc<double>(5 * static_cast<size_t>(Bl));
+    recv = K > 1 ? dalloc<double>(5 * static_cast<size_t>(B)) : send;
+    gt_recv = K > 1 ? dalloc<double>(2 * static_cast<size_t>(B)) : nullptr;
+    red = dalloc<double>(2);
+    par1 = dalloc<float4>(B);
+    par2 = dalloc<float4>(B);
+    rcoef = dalloc<float>(Bl);
+    q = dalloc<__nv_bfloat16>(2 * static_cast<size_t>(Bl) * ldq);
+    err = dalloc<int>(1);
+    FC_CUDA(cudaMemset(err, 0, sizeof(int)));
+    result_d = dalloc<fc::StepResult>(1);
+    FC_CUDA(cudaMallocHost(&result_h, sizeof(fc::StepResult)));
+    std::memset(result_h, 0, sizeof(*result_h));
+    FC_CUDA(cudaEventCreateWithFlags(&done, cudaEventDisableTiming));
+    mQ[0] = make_map(q, ldq, Bl, static_cast<uint64_t>(ldq) * 2, 64, 128);
+    mQ[1] = make_map(q + static_cast<size_t>(Bl) * ldq, ldq, Bl, static_cast<uint64_t>(ldq) * 2, 64, 128);
+    build_args();
+  }
+
+  void build_args() {
+    fc::StepArgs& a = args;
+    a.B = B; a.Bl = Bl; a.d = d; a.world = K; a.rank = rank; a.row0 = rank * Bl; a.n_jt = n_jt;
+    a.variant = cfg.variant; a.individual = indiv; a.track_u = track_u; a.scale_by_tau = cfg.scale_by_tau;
+    a.lr_decay_enabled = cfg.lr_decay_enabled;
+    a.n_train = cfg.n_train;
+    a.rho = cfg.rho; a.tau_lr = cfg.tau_lr; a.tau0 = cfg.tau0; a.beta1 = cfg.beta1; a.beta2 = cfg.beta2;
+    a.adam_eps = cfg.adam_eps; a.lr_decay_threshold = cfg.lr_decay_threshold; a.lr_decay_factor = cfg.lr_decay_factor;
+    a.diag = diag;
+    a.u1_tab = u1; a.u2_tab = u2; a.tau1_tab = tau1; a.tau2_tab = tau2;
+    a.m1_tab = m1; a.v1_tab = v1; a.s1_tab = s1; a.m2_tab = m2; a.v2_tab = v2; a.s2_tab = s2;
+    a.tau_state = tau_state;
+    a.rowstat_R = rowstat; a.rowstat_C = rowstat + Bl;
+    a.partial_R = partial; a.partial_C = partial + static_cast<size_t>(Bl) * n_jt * 2;
+    a.clamps = clamps;
+    a.t_loc1 = F(0); a.t_loc2 = F(1);
+    a.sum1 = F(2); a.dx1 = F(3); a.sum2 = F(4); a.dx2 = F(5);
+    a.g1 = F(6); a.g2 = F(7); a.u1 = F(8); a.u2 = F(9);
+    a.term_a = F(10); a.term_b = F(11); a.term_loss = F(12);
+    a.gt1 = F(13); a.gt2 = F(14);   // contiguous [gt1 | gt2]
+    a.send = send; a.recv = recv;
+    a.gt_recv = K > 1 ? gt_recv : F(13);
+    a.par1 = par1; a.par2 = par2; a.rcoef = rcoef; a.red = red; a.err = err; a.result = result_d;
+  }
+
+  void ensure_maps(const void* e1, const void* e2) {
+    if (e1 == map_e1 && e2 == map_e2) return;
+    const uint64_t rb = static_cast<uint64_t>(d) * 2;
+    mE1k = make_map(e1, d, B, rb, 64, 128);
+    mE2k = make_map(e2, d, B, rb, 64, 128);
+    mE1n = make_map(e1, d, B, rb, 64, 64);
+    mE2n = make_map(e2, d, B, rb, 64, 64);
+    map_e1 = e1;
+    map_e2 = e2;
+  }
+
+  int pair_grid(long items) const {
+    long pairs = std::min<long>(n_sm / 2, items);
+    return static_cast<int>(std::max<long>(1, pairs) * 2);
+  }
+
+  void step(const fc_step_in* in, fc_step_out* out, cudaStream_t st) {
+    if (!in || !out || !in->e1 || !in->e2 || !in->ids || !out->de1 || !out->de2)
+      throw FcError{FC_ERR_SHAPE, "fc_loss_step: null input/output pointer"};
+    if (in->eps < 0.0) throw FcError{FC_ERR_DOMAIN, "epsilon must be non-negative"};
+    if (track_u && (!(in->gamma > 0.0) || in->gamma > 1.0)) throw FcError{FC_ERR_DOMAIN, "gamma must be in (0,1]"};
+    const __nv_bfloat16* E1 = static_cast<const __nv_bfloat16*>(in->e1);
+    const __nv_bfloat16* E2 = static_cast<const __nv_bfloat16*>(in->e2);
+    mark(0, st);
+    if (K > 1) {
+      FC_NCCL(ncclGroupStart());
+      FC_NCCL(ncclAllGather(E1, e1g, static_cast<size_t>(Bl) * d * 2, ncclUint8, comm, st));
+      FC_NCCL(ncclAllGather(E2, e2g, static_cast<size_t>(Bl) * d * 2, ncclUint8, comm, st));
+      FC_NCCL(ncclGroupEnd());
+      E1 = e1g;
+      E2 = e2g;
+    }
+    ensure_maps(E1, E2);
+    fc::StepArgs a = args;
+    a.ids = in->ids;
+
+    mark(1, st);
+    fc::fc_diag_kernel<<<(B * 32 + 255) / 256, 256, 0, st>>>(E1, E2, B, d, diag);
+    fc::fc_rowpar_kernel<<<(Bl + 255) / 256, 256, 0, st>>>(a);
+    FC_CUDA(cudaGetLastError());
+
+    // ---- pass 1: row statistics of S[L,G] (segment R) and S^T[L,G] (segment C) ----
+    fc::SimParams sp{};
+    sp.nseg = 2;
+    sp.d = d;
+    sp.ldq = ldq;
+    sp.n_jt = n_jt;
+    for (int s = 0; s < 2; ++s) {
+      fc::SimSeg& g = sp.seg[s];
+      g.rows = Bl;
+      g.a_row0 = rank * Bl;
+      g.cols = B;
+      g.row_stat = s ? a.rowstat_C : a.rowstat_R;
+      g.partial = s ? a.partial_C : a.partial_R;
+      sp.n_rb[s] = (Bl + fc::kPairM - 1) / fc::kPairM;
+    }
+    sp.n_items = (sp.n_rb[0] + sp.n_rb[1]) * n_jt;
+    sp.clamps = clamps;
+    CUtensorMap mA[2] = {mE1k, mE2k}, mB[2] = {mE2k, mE1k};
+    mark(2, st);
+    FC_CUDA(fc::launch_sim(fc::kSimStats, sp, mA, mB, pair_grid(sp.n_items), st, nullptr));
+
+    // ---- u table, payload, (all-gather), weights, reductions, tau update ----
+    mark(3, st);
+    fc::fc_table_kernel<<<(Bl + 255) / 256, 256, 0, st>>>(a, in->gamma);
+    FC_CUDA(cudaGetLastError());
+    if (K > 1) FC_NCCL(ncclAllGather(send, recv, 5 * static_cast<size_t>(Bl), ncclFloat64, comm, st));
+    fc::fc_weights_kernel<<<(B + 255) / 256, 256, 0, st>>>(a, in->eps);
+    fc::fc_reduce_kernel<<<1, 1024, 0, st>>>(a);
+    FC_CUDA(cudaGetLastError());
+    if (K > 1) FC_NCCL(ncclAllReduce(red, red, 2, ncclFloat64, ncclSum, comm, st));
+    if (indiv) {
+      if (K > 1) FC_NCCL(ncclAllGather(a.gt1, gt_recv, 2 * static_cast<size_t>(Bl), ncclFloat64, comm, st));
+      fc::fc_indiv_update_kernel<<<(B + 255) / 256, 256, 0, st>>>(a);
+    }
+    fc::fc_finalize_kernel<<<1, 32, 0, st>>>(a);
+    FC_CUDA(cudaGetLastError());
+
+    // ---- pass 2: Q' tiles (bf16) for both segments ----
+    for (int s = 0; s < 2; ++s) {
+      fc::SimSeg& g = sp.seg[s];
+      g.row_stat = nullptr;
+      g.partial = nullptr;
+      g.row_par = (s ? par2 : par1) + rank * Bl;
+      g.col_par = s ? par1 : par2;
+      g.q = q + static_cast<size_t>(s) * Bl * ldq;
+    }
+    mark(4, st);
+    FC_CUDA(fc::launch_sim(fc::kSimQ, sp, mA, mB, pair_grid(sp.n_items), st, nullptr));
+
+    // ---- pass 2b: dE = c (Q' E - r o E_local) ----
+    mark(5, st);
+    fc::GemmParams gp{};
+    gp.nseg = 2;
+    gp.d = d;
+    gp.n_nb = (d + fc::kPairN - 1) / fc::kPairN;
+    gp.kb_total = ldq / fc::kBlockK;
+    int split = std::max(1, std::min(n_split, gp.kb_total));
+    gp.kb_per_split = (gp.kb_total + split - 1) / split;
+    split = (gp.kb_total + gp.kb_per_split - 1) / gp.kb_per_split;
+    gp.n_split = split;
+    gp.scale = static_cast<float>(1.0 / (static_cast<double>(Bl) * static_cast<double>(B - 1)));
+    for (int s = 0; s < 2; ++s) {
+      fc::GemmSeg& g = gp.seg[s];
+      g.rows = Bl;
+      g.x_row0 = rank * Bl;
+      g.r = rcoef;
+      g.x = s ? E1 : E2;
+      g.out = s ? out->de2 : out->de1;
+      gp.n_mb[s] = (Bl + fc::kPairM - 1) / fc::kPairM;
+      if (split > 1) FC_CUDA(cudaMemsetAsync(g.out, 0, static_cast<size_t>(Bl) * d * 4, st));
+    }
+    gp.n_items = (gp.n_mb[0] + gp.n_mb[1]) * gp.n_nb * gp.n_split;
+    CUtensorMap mX[2] = {mE2n, mE1n};
+    FC_CUDA(fc::launch_gemm(gp, mQ, mX, pair_grid(gp.n_items), st));
+    mark(6, st);
+
+    FC_CUDA(cudaMemcpyAsync(result_h, result_d, sizeof(fc::StepResult), cudaMemcpyDeviceToHost, st));
+    FC_CUDA(cudaEventRecord(done, st));
+  }
+
+  int kernels_per_step() const {
+    return 2 /*diag,rowpar*/ + 1 /*pass1*/ + 1 /*table*/ + 2 /*weights,reduce*/ + (indiv ? 1 : 0) + 1 /*finalize*/ +
+           1 /*pass2*/ + 1 /*gemm*/;
+  }
+
+  void destroy() {
+    if (comm) ncclCommDestroy(comm);
+    for (void* p : {(void*)u1, (void*)u2, (void*)tau1, (void*)tau2, (void*)m1, (void*)v1, (void*)m2, (void*)v2,
+                    (void*)s1, (void*)s2, (void*)tau_state, (void*)e1g, (void*)e2g, (void*)diag, (void*)rowstat,
+                    (void*)partial, (void*)clamps, (void*)f64, (void*)red, (void*)par1, (void*)par2, (void*)rcoef,
+                    (void*)q, (void*)err, (void*)result_d, (void*)gt_recv})
+      if (p) cudaFree(p);
+    if (recv && recv != send) cudaFree(recv);
+    if (send) cudaFree(send);
+    if (result_h) cudaFreeHost(result_h);
+    cudaEventDestroy(done);
+    if (timing)
+      for (auto& e : ev) cudaEventDestroy(e);
+  }
+};
+
+template <class Fn>
+int guarded(Fn&& fn) {
+  try {
+    fn();
+    return FC_OK;
+  } catch (const FcError& e) {
+    g_last_error = e.msg;
+    return e.code;
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    return FC_ERR_CUDA;
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* fc_last_error(void) { return g_last_error.c_str(); }
+
+int fc_config_defaults(int32_t variant, int64_t n_train, fc_config* out) {
+  if (!out) return FC_ERR_SHAPE;
+  if (variant < 0 || variant > 6) {
+    g_last_error = "unknown variant";
+    return FC_ERR_CONFIG;
+  }
+  std::memset(out, 0, sizeof(*out));
+  out->variant = variant;
+  out->n_train = n_train;
+  // trainer.cpp:139-194 with the registry defaults of config.cpp:36-60
+  out->tau_init = variant == FC_FASTCLIP_V3 ? 0.07 : 0.03;
+  out->tau0 = 0.005;
+  if (variant == FC_SOGCLR || variant == FC_FASTCLIP_V1) out->tau_lr = 0.0;
+  else if (is_individual(variant)) out->tau_lr = 1e-2;
+  else out->tau_lr = 2e-4;
+  out->rho = is_individual(variant) ? 9.0 : (variant == FC_FASTCLIP_V3 ? 6.5 : 0.0);
+  out->beta1 = 0.9;
+  out->beta2 = 0.999;
+  out->adam_eps = 1e-8;
+  out->lr_decay_enabled = variant == FC_FASTCLIP_V3 ? 1 : 0;
+  out->lr_decay_threshold = 0.03;
+  out->lr_decay_factor = 1.0 / 3.0;
+  out->scale_by_tau = (variant == FC_FASTCLIP_V0 || variant == FC_OPENCLIP_MBCL) ? 0 : 1;
+  out->world = 1;
+  return FC_OK;
+}
+
+double fc_gamma_at(int32_t cosine, double constant, double gamma_min, int64_t decay_epochs, int64_t iters_per_epoch,
+                   int64_t t) {
+  // schedules.cpp:25-31
+  if (!cosine) return constant;
+  const int64_t epoch = t / iters_per_epoch;
+  if (epoch >= decay_epochs) return gamma_min;
+  const double frac = static_cast<double>(epoch) / static_cast<double>(decay_epochs);
+  return 0.5 * (1.0 + std::cos(3.141592653589793238462643383279502884 * frac)) * (1.0 - gamma_min) + gamma_min;
+}
+
+double fc_epsilon_at(double initial, double late, int64_t switch_epoch, int64_t epoch) {
+  if (switch_epoch < 0) return initial;  // schedules.cpp:62-65
+  return epoch < switch_epoch ? initial : late;
+}
+
+int fc_nccl_unique_id(uint8_t out[128]) {
+  return guarded([&] {
+    ncclUniqueId id;
+    FC_NCCL(ncclGetUniqueId(&id));
+    std::memcpy(out, &id, sizeof(id));
+  });
+}
+
+int fc_create(const fc_config* cfg, void** ctx) {
+  if (!cfg || !ctx) return FC_ERR_SHAPE;
+  auto* s = new LossStep;
+  const int rc = guarded([&] { s->init(cfg); });
+  if (rc != FC_OK) {
+    s->destroy();
+    delete s;
+    *ctx = nullptr;
+    return rc;
+  }
+  *ctx = s;
+  return FC_OK;
+}
+
+int fc_destroy(void* ctx) {
+  if (!ctx) return FC_OK;
+  auto* s = static_cast<LossStep*>(ctx);
+  s->destroy();
+  delete s;
+  return FC_OK;
+}
+
+int fc_loss_step(void* ctx, const fc_step_in* in, fc_step_out* out, void* stream) {
+  if (!ctx) return FC_ERR_SHAPE;
+  return guarded([&] { static_cast<LossStep*>(ctx)->step(in, out, static_cast<cudaStream_t>(stream)); });
+}
+
+int fc_step_scalars_get(void* ctx, fc_step_scalars* out) {
+  if (!ctx || !out) return FC_ERR_SHAPE;
+  auto* s = static_cast<LossStep*>(ctx);
+  int rc = guarded([&] { FC_CUDA(cudaEventSynchronize(s->done)); });
+  if (rc != FC_OK) return rc;
+  out->loss = s->result_h->loss;
+  out->gtau = s->result_h->gtau;
+  out->tau = s->result_h->tau;
+  out->exp_clamps = s->result_h->clamps;
+  out->latched = s->result_h->latched;
+  if (s->result_h->err) {
+    g_last_error = "non-finite temperature gradient";
+    return s->result_h->err;
+  }
+  return FC_OK;
+}
+
+int fc_local_views(void* ctx, double* g1, double* g2, double* u1, double* u2, double* t1, double* t2) {
+  if (!ctx) return FC_ERR_SHAPE;
+  auto* s = static_cast<LossStep*>(ctx);
+  return guarded([&] {
+    FC_CUDA(cudaEventSynchronize(s->done));
+    const size_t n = static_cast<size_t>(s->Bl) * 8;
+    double* host[6] = {g1, g2, u1, u2, t1, t2};
+    const double* dev[6] = {s->args.g1, s->args.g2, s->args.u1, s->args.u2, s->args.t_loc1, s->args.t_loc2};
+    for (int i = 0; i < 6; ++i)
+      if (host[i]) FC_CUDA(cudaMemcpy(host[i], dev[i], n, cudaMemcpyDeviceToHost));
+  });
+}
+
+int fc_table_download(void* ctx, double* u1, double* u2, double* tau1, double* tau2, double* m1, double* v1,
+                      int64_t* s1, double* m2, double* v2, int64_t* s2) {
+  if (!ctx) return FC_ERR_SHAPE;
+  auto* s = static_cast<LossStep*>(ctx);
+  return guarded([&] {
+    FC_CUDA(cudaDeviceSynchronize());
+    const size_t n = static_cast<size_t>(s->cfg.n_train) * 8;
+    if (u1) FC_CUDA(cudaMemcpy(u1, s->u1, n, cudaMemcpyDeviceToHost));
+    if (u2) FC_CUDA(cudaMemcpy(u2, s->u2, n, cudaMemcpyDeviceToHost));
+    if (s->indiv) {
+      void* host[8] = {tau1, tau2, m1, v1, s1, m2, v2, s2};
+      const void* dev[8] = {s->tau1, s->tau2, s->m1, s->v1, s->s1, s->m2, s->v2, s->s2};
+      for (int i = 0; i < 8; ++i)
+        if (host[i]) FC_CUDA(cudaMemcpy(host[i], dev[i], n, cudaMemcpyDeviceToHost));
+    }
+  });
+}
+
+int fc_table_upload(void* ctx, const double* u1, const double* u2, const double* tau1, const double* tau2,
+                    const double* m1, const double* v1, const int64_t* s1, const double* m2, const double* v2,
+                    const int64_t* s2) {
+  if (!ctx) return FC_ERR_SHAPE;
+  auto* s = static_cast<LossStep*>(ctx);
+  return guarded([&] {
+    FC_CUDA(cudaDeviceSynchronize());
+    const size_t n = static_cast<size_t>(s->cfg.n_train) * 8;
+    if (u1) FC_CUDA(cudaMemcpy(s->u1, u1, n, cudaMemcpyHostToDevice));
+    if (u2) FC_CUDA(cudaMemcpy(s->u2, u2, n, cudaMemcpyHostToDevice));
+    if (s->indiv) {
+      const void* host[8] = {tau1, tau2, m1, v1, s1, m2, v2, s2};
+      void* dev[8] = {s->tau1, s->tau2, s->m1, s->v1, s->s1, s->m2, s->v2, s->s2};
+      for (int i = 0; i < 8; ++i)
+        if (host[i]) FC_CUDA(cudaMemcpy(dev[i], host[i], n, cudaMemcpyHostToDevice));
+    }
+  });
+}
+
+int fc_tau_state_get(void* ctx, double* tau, double* m, double* v, int64_t* step, int32_t* latched) {
+  if (!ctx) return FC_ERR_SHAPE;
+  auto* s = static_cast<LossStep*>(ctx);
+  return guarded([&] {
+    fc::TauState ts;
+    FC_CUDA(cudaDeviceSynchronize());
+    FC_CUDA(cudaMemcpy(&ts, s->tau_state, sizeof(ts), cudaMemcpyDeviceToHost));
+    if (tau) *tau = ts.tau;
+    if (m) *m = ts.m;
+    if (v) *v = ts.v;
+    if (step) *step = ts.step;
+    if (latched) *latched = ts.latched;
+  });
+}
+
+int fc_tau_state_set(void* ctx, double tau, double m, double v, int64_t step, int32_t latched) {
+  if (!ctx) return FC_ERR_SHAPE;
+  auto* s = static_cast<LossStep*>(ctx);
+  return guarded([&] {
+    fc::TauState ts{tau, m, v, static_cast<long long>(step), latched, 0};
+    FC_CUDA(cudaDeviceSynchronize());
+    FC_CUDA(cudaMemcpy(s->tau_state, &ts, sizeof(ts), cudaMemcpyHostToDevice));
+  });
+}
+
+int fc_set_phase_timing(void* ctx, int32_t on) {
+  if (!ctx) return FC_ERR_SHAPE;
+  auto* s = static_cast<LossStep*>(ctx);
+  return guarded([&] {
+    if (on && !s->timing)
+      for (auto& e : s->ev) FC_CUDA(cudaEventCreate(&e));
+    s->timing = s->timing || on;
+  });
+}
+
+int fc_phase_times(void* ctx, float* ms, int32_t n) {
+  if (!ctx || !ms) return FC_ERR_SHAPE;
+  auto* s = static_cast<LossStep*>(ctx);
+  return guarded([&] {
+    if (!s->timing) throw FcError{FC_ERR_CONFIG, "phase timing not enabled"};
+    FC_CUDA(cudaEventSynchronize(s->ev[LossStep::kPhases]));
+    for (int i = 0; i < n && i < LossStep::kPhases; ++i) FC_CUDA(cudaEventElapsedTime(&ms[i], s->ev[i], s->ev[i + 1]));
+  });
+}
+
+int fc_kernels_per_step(void* ctx) { return ctx ? static_cast<LossStep*>(ctx)->kernels_per_step() : 0; }
+
+int fc_debug_similarity(const void* a, const void* b, int32_t rows, int32_t cols, int32_t dim, float* out,
+                        void* stream) {
+  return guarded([&] {
+    if (dim % 8 != 0) throw FcError{FC_ERR_UNSUPPORTED, "dim % 8"};
+    const uint64_t rb = static_cast<uint64_t>(dim) * 2;
+    CUtensorMap ma = make_map(a, dim, rows, rb, 64, 128);
+    CUtensorMap mb = make_map(b, dim, cols, rb, 64, 128);
+    fc::SimParams sp{};
+    sp.nseg = 1;
+    sp.d = dim;
+    sp.n_jt = (cols + fc::kPairN - 1) / fc::kPairN;
+    sp.n_rb[0] = (rows + fc::kPairM - 1) / fc::kPairM;
+    sp.n_rb[1] = 0;
+    sp.seg[0].rows = rows;
+    sp.seg[0].a_row0 = 0;
+    sp.seg[0].cols = cols;
+    sp.n_items = sp.n_rb[0] * sp.n_jt;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const int pairs = std::min(sm_count(dev) / 2, sp.n_items);
+    FC_CUDA(fc::launch_sim(fc::kSimRaw, sp, &ma, &mb, std::max(1, pairs) * 2, static_cast<cudaStream_t>(stream), out));
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,275 @@
+// table_kernels.cu -- the per-anchor (O(B)) kernels of the FastCLIP loss step.
+//
+// These are HBM/latency-bound gather/scatter and scalar kernels (no tensor-core shape):
+//   fc_diag_kernel        S_ii = <E1_i, E2_i> for the global batch (fp32 from bf16)
+//   fc_rowpar_kernel      tau^t snapshot per local anchor (global tau or IndividualTemp
+//                         gather by id, state.cpp:112-122) -> pass-1 row parameters
+//   fc_table_kernel       fixed-order reduction of the pass-1 partials -> g (engine.cpp:151-176),
+//                         UTable EMA + snapshot (state.cpp:45-71), packed all-gather payload
+//   fc_weights_kernel     PairWeights for the whole batch (engine.cpp:37-75), pass-2 row/col
+//                         parameters, r_i, per-anchor tau-gradient and loss terms
+//   fc_reduce_kernel      fixed-order block reduction of the local terms (G_tau, loss)
+//   fc_finalize_kernel    all-reduced G_tau -> temperature_step (optimizers.cpp:65-83) with the
+//                         TauLrLatch (schedules.hpp:55-58); step scalars
+//   fc_indiv_update_kernel  v2: IndividualTemp::update for every id of the global batch
+//                         (state.cpp:124-131), replicated identically on every rank
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "table_kernels.cuh"
+
+namespace fc {
+
+namespace {
+constexpr double kLog2eD = 1.4426950408889634073599;
+}
+
+__global__ void fc_diag_kernel(const __nv_bfloat16* __restrict__ e1, const __nv_bfloat16* __restrict__ e2,
+                               int B, int d, float* __restrict__ diag) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) / 32;
+  const int lane = threadIdx.x & 31;
+  if (warp >= B) return;
+  const uint4* a = reinterpret_cast<const uint4*>(e1 + static_cast<size_t>(warp) * d);
+  const uint4* b = reinterpret_cast<const uint4*>(e2 + static_cast<size_t>(warp) * d);
+  float acc = 0.f;
+  for (int v = lane; v < d / 8; v += 32) {
+    const uint4 x = __ldg(a + v);
+    const uint4 y = __ldg(b + v);
+    const uint32_t xs[4] = {x.x, x.y, x.z, x.w};
+    const uint32_t ys[4] = {y.x, y.y, y.z, y.w};
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      const float2 fx = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&xs[t]));
+      const float2 fy = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&ys[t]));
+      acc = fmaf(fx.x, fy.x, acc);
+      acc = fmaf(fx.y, fy.y, acc);
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if (lane == 0) diag[warp] = acc;
+}
+
+__global__ void fc_rowpar_kernel(StepArgs a) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r == 0) *a.clamps = 0ull;
+  if (r >= a.Bl) return;
+  double t1, t2;
+  if (a.individual) {
+    const int id = a.ids[r];
+    t1 = a.tau1_tab[id];
+    t2 = a.tau2_tab[id];
+  } else {
+    t1 = t2 = a.tau_state->tau;
+  }
+  a.t_loc1[r] = t1;
+  a.t_loc2[r] = t2;
+  const float s_ii = a.diag[a.row0 + r];
+  a.rowstat_R[r] = make_float2(s_ii, static_cast<float>(kLog2eD / t1));
+  a.rowstat_C[r] = make_float2(s_ii, static_cast<float>(kLog2eD / t2));
+}
+
+__global__ void fc_table_kernel(StepArgs a, double gamma) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= a.Bl) return;
+  const int nparts = a.n_jt * 2;
+  const float2* pr = a.partial_R + static_cast<size_t>(r) * nparts;
+  const float2* pc = a.partial_C + static_cast<size_t>(r) * nparts;
+  double s1 = 0.0, x1 = 0.0, s2 = 0.0, x2 = 0.0;
+  for (int q = 0; q < nparts; ++q) {  // fixed order: deterministic
+    const float2 u = pr[q];
+    const float2 v = pc[q];
+    s1 += u.x; x1 += u.y;
+    s2 += v.x; x2 += v.y;
+  }
+  a.sum1[r] = s1; a.dx1[r] = x1;
+  a.sum2[r] = s2; a.dx2[r] = x2;
+  const double inv = 1.0 / static_cast<double>(a.B - 1);
+  const double g1 = s1 * inv;   // engine.cpp:176
+  const double g2 = s2 * inv;
+  a.g1[r] = g1;
+  a.g2[r] = g2;
+  double u1 = g1, u2 = g2;      // MBCL: the "u" gathered is the current-batch g (trainer.cpp:456)
+  const int id = a.ids[r];
+  if (a.track_u) {              // state.cpp:52-53 (fp64 EMA), then snapshot (state.cpp:57-71)
+    u1 = (1.0 - gamma) * a.u1_tab[id] + gamma * g1;
+    u2 = (1.0 - gamma) * a.u2_tab[id] + gamma * g2;
+    a.u1_tab[id] = u1;
+    a.u2_tab[id] = u2;
+  }
+  a.u1[r] = u1;
+  a.u2[r] = u2;
+  // packed payload [u1 | u2 | t1 | t2 | id] (trainer.cpp:459-487 "u-gather" + "tau-gather")
+  double* snd = a.send;
+  snd[r] = u1;
+  snd[a.Bl + r] = u2;
+  snd[2 * a.Bl + r] = a.t_loc1[r];
+  snd[3 * a.Bl + r] = a.t_loc2[r];
+  snd[4 * a.Bl + r] = static_cast<double>(id);
+}
+
+__global__ void fc_weights_kernel(StepArgs a, double eps) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= a.B) return;
+  const int k = i / a.Bl;
+  const int r = i % a.Bl;
+  const double* blk = a.recv + static_cast<size_t>(k) * 5 * a.Bl;
+  const double u1 = blk[r], u2 = blk[a.Bl + r];
+  double t1 = blk[2 * a.Bl + r], t2 = blk[3 * a.Bl + r];
+  const double tau = a.tau_state->tau;
+  double w1, w2;
+  if (a.variant == 0) {  // MBCL: weights_mbcl (engine.cpp:65-75)
+    const double c = 1.0 / static_cast<double>(a.B - 1);
+    w1 = 1.0 / (c + u1);
+    w2 = 1.0 / (c + u2);
+    t1 = t2 = tau;
+  } else if (a.individual) {  // weights_individual_tau (engine.cpp:52-63)
+    w1 = (1.0 / (eps + u1)) * t1;
+    w2 = (1.0 / (eps + u2)) * t2;
+  } else {  // weights_global_tau (engine.cpp:37-50)
+    w1 = 1.0 / (eps + u1);
+    w2 = 1.0 / (eps + u2);
+    if (a.scale_by_tau) { w1 *= tau; w2 *= tau; }
+    t1 = t2 = tau;
+  }
+  const double c1 = w1 / t1;   // P1 coefficient: w1_a / t1_a  (engine.cpp:104,118)
+  const double c2 = w2 / t2;   // P2 coefficient: w2_a / t2_a
+  const float s_ii = a.diag[i];
+  a.par1[i] = make_float4(s_ii, static_cast<float>(kLog2eD / t1), static_cast<float>(c1), 0.f);
+  a.par2[i] = make_float4(s_ii, static_cast<float>(kLog2eD / t2), static_cast<float>(c2), 0.f);
+
+  if (k != a.rank) return;
+  // ---- local anchor: r_i, tau-gradient terms, loss term ----
+  a.rcoef[r] = static_cast<float>(c1 * a.sum1[r] + c2 * a.sum2[r]);
+  const double inv = 1.0 / static_cast<double>(a.B - 1);
+  const double ds1 = (-(a.dx1[r] / (t1 * t1))) * inv;   // engine.cpp:198-205
+  const double ds2 = (-(a.dx2[r] / (t2 * t2))) * inv;
+  const double g1 = a.g1[r], g2 = a.g2[r];
+  if (a.variant == 0) {
+    const double c = inv;
+    a.term_a[r] = ds1 / (c + g1) + ds2 / (c + g2);          // grad_tau_mbcl (engine.cpp:261-266)
+    a.term_b[r] = 0.0;
+    a.term_loss[r] = log(c + g1) + log(c + g2);             // eval_mbcl (losses.cpp:168-180)
+  } else if (a.individual) {
+    const double inv_n = 1.0 / static_cast<double>(a.n_train);   // engine.cpp:240-259
+    a.gt1[r] = inv_n * (log(eps + u1) + a.rho + t1 * ds1 / (eps + u1));
+    a.gt2[r] = inv_n * (log(eps + u2) + a.rho + t2 * ds2 / (eps + u2));
+    a.term_a[r] = 0.0;
+    a.term_b[r] = 0.0;
+    a.term_loss[r] = t1 * (log(eps + g1) + a.rho) + t2 * (log(eps + g2) + a.rho);  // eval_rgcl
+  } else {
+    a.term_a[r] = ds1 / (eps + u1) + ds2 / (eps + u2);        // grad_tau_unscaled (engine.cpp:208-224)
+    a.term_b[r] = log(eps + u1) + log(eps + u2);              // grad_tau_margin logs (engine.cpp:226-238)
+    a.term_loss[r] = log(eps + g1) + log(eps + g2);           // eval_gcl (losses.cpp:126-138)
+  }
+}
+
+// One block; fixed-order strided accumulation + fixed tree => deterministic sums.
+__global__ void fc_reduce_kernel(StepArgs a) {
+  __shared__ double sh[3][1024];
+  double s0 = 0.0, s1 = 0.0, s2 = 0.0;
+  for (int r = threadIdx.x; r < a.Bl; r += blockDim.x) {
+    s0 += a.term_a[r];
+    s1 += a.term_b[r];
+    s2 += a.term_loss[r];
+  }
+  sh[0][threadIdx.x] = s0;
+  sh[1][threadIdx.x] = s1;
+  sh[2][threadIdx.x] = s2;
+  __syncthreads();
+  for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+    if (threadIdx.x < w) {
+      sh[0][threadIdx.x] += sh[0][threadIdx.x + w];
+      sh[1][threadIdx.x] += sh[1][threadIdx.x + w];
+      sh[2][threadIdx.x] += sh[2][threadIdx.x + w];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    const double bl = static_cast<double>(a.Bl);
+    const double unscaled = sh[0][0] / bl;
+    double gtl = unscaled;                                   // v0 / MBCL
+    if (a.variant == 6) gtl = sh[1][0] / bl + 2.0 * a.rho + a.tau_state->tau * unscaled;  // v3
+    a.red[0] = gtl;        // all-reduced (sum) across ranks, then * 1/K (fabric.cpp:73-83)
+    a.red[1] = sh[2][0];   // loss numerator, summed across ranks
+  }
+}
+
+// trainer.cpp:557-577 for the global-temperature schemes + step scalars for every variant.
+__global__ void fc_finalize_kernel(StepArgs a) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  TauState* ts = a.tau_state;
+  const double tau_t = ts->tau;
+  const double nB = static_cast<double>(a.B);
+  StepResult* res = a.result;
+  // exact batch loss at tau^t (losses.cpp:126-180)
+  double loss;
+  if (a.variant == 0 || a.individual) loss = a.red[1] / nB;
+  else loss = tau_t * a.red[1] / nB;
+  if (a.variant == 6) loss += 2.0 * a.rho * tau_t;
+  res->loss = loss;
+  res->gtau = 0.0;
+  res->clamps = *a.clamps;
+  const bool learnable_global = (a.variant == 0 || a.variant == 3 || a.variant == 6);
+  if (learnable_global) {
+    const double gtau = a.red[0] * (1.0 / static_cast<double>(a.world));
+    res->gtau = gtau;
+    double lr = a.tau_lr;
+    if (a.lr_decay_enabled) {   // TauLrLatch::modifier at the pre-step tau (schedules.hpp:55-58)
+      if (tau_t < a.lr_decay_threshold) ts->latched = 1;
+      lr *= ts->latched ? a.lr_decay_factor : 1.0;
+    }
+    if (!isfinite(gtau)) {
+      *a.err = 9;  // NumericError (optimizers.cpp:67)
+    } else {       // scalar_adamw_step with weight decay 0, then projection (optimizers.cpp:65-83)
+      ts->m = a.beta1 * ts->m + (1.0 - a.beta1) * gtau;
+      ts->v = a.beta2 * ts->v + (1.0 - a.beta2) * gtau * gtau;
+      const double c1 = 1.0 - pow(a.beta1, static_cast<double>(ts->step + 1));
+      const double c2 = 1.0 - pow(a.beta2, static_cast<double>(ts->step + 1));
+      ts->step += 1;
+      const double rr = (ts->m / c1) / (sqrt(ts->v / c2) + a.adam_eps);
+      const double next = tau_t - lr * (rr + 0.0 * tau_t);
+      ts->tau = next < a.tau0 ? a.tau0 : next;
+    }
+  }
+  res->tau = ts->tau;
+  res->latched = ts->latched;
+  res->err = *a.err;
+}
+
+// v2 / iSogCLR: IndividualTemp::update for every id of the global batch (state.cpp:124-131);
+// each rank applies the same updates in the same arithmetic -> identical table replicas.
+__global__ void fc_indiv_update_kernel(StepArgs a) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= a.B) return;
+  const int k = i / a.Bl;
+  const int r = i % a.Bl;
+  const int id = static_cast<int>(a.recv[static_cast<size_t>(k) * 5 * a.Bl + 4 * a.Bl + r]);
+  const double gts[2] = {a.gt_recv[static_cast<size_t>(k) * 2 * a.Bl + r],
+                         a.gt_recv[static_cast<size_t>(k) * 2 * a.Bl + a.Bl + r]};
+  double* taus[2] = {a.tau1_tab, a.tau2_tab};
+  double* ms[2] = {a.m1_tab, a.m2_tab};
+  double* vs[2] = {a.v1_tab, a.v2_tab};
+  long long* ss[2] = {a.s1_tab, a.s2_tab};
+  for (int t = 0; t < 2; ++t) {
+    const double g = gts[t];
+    if (!isfinite(g)) { *a.err = 9; return; }
+    double m = ms[t][id], v = vs[t][id];
+    const long long st = ss[t][id];
+    m = a.beta1 * m + (1.0 - a.beta1) * g;
+    v = a.beta2 * v + (1.0 - a.beta2) * g * g;
+    const double c1 = 1.0 - pow(a.beta1, static_cast<double>(st + 1));
+    const double c2 = 1.0 - pow(a.beta2, static_cast<double>(st + 1));
+    const double rr = (m / c1) / (sqrt(v / c2) + a.adam_eps);
+    const double tau = taus[t][id];
+    const double next = tau - a.tau_lr * (rr + 0.0 * tau);
+    ms[t][id] = m;
+    vs[t][id] = v;
+    ss[t][id] = st + 1;
+    taus[t][id] = next < a.tau0 ? a.tau0 : next;
+  }
+}
+
+}  // namespace fc

@@ -1,0 +1,74 @@
+// table_kernels.cuh -- device state and argument block of the per-anchor kernels.
+#pragma once
+
+#include <cstdint>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+namespace fc {
+
+// Replica scalar state of the global temperature (trainer.cpp:245-254), device resident.
+struct TauState {
+  double tau;
+  double m, v;
+  long long step;
+  int latched;
+  int pad;
+};
+
+// Scalars of one step, copied to pinned host memory at the end of the step.
+struct StepResult {
+  double loss;
+  double gtau;
+  double tau;
+  unsigned long long clamps;
+  int latched;
+  int err;
+};
+
+struct StepArgs {
+  // shapes / config
+  int B, Bl, d, world, rank, row0, n_jt;
+  int variant, individual, track_u, scale_by_tau, lr_decay_enabled;
+  long long n_train;
+  double rho, tau_lr, tau0, beta1, beta2, adam_eps, lr_decay_threshold, lr_decay_factor;
+  // inputs
+  const int32_t* ids;          // [Bl]
+  const float* diag;           // [B]
+  // dataset-sized tables (fp64 SoA)
+  double* u1_tab; double* u2_tab;
+  double* tau1_tab; double* tau2_tab;
+  double* m1_tab; double* v1_tab; long long* s1_tab;
+  double* m2_tab; double* v2_tab; long long* s2_tab;
+  TauState* tau_state;
+  // pass-1 products
+  float2* rowstat_R; float2* rowstat_C;   // [Bl]
+  float2* partial_R; float2* partial_C;   // [Bl][n_jt*2]
+  unsigned long long* clamps;
+  // per-local-anchor fp64 state of the step
+  double* t_loc1; double* t_loc2;
+  double* sum1; double* dx1; double* sum2; double* dx2;
+  double* g1; double* g2; double* u1; double* u2;
+  double* term_a; double* term_b; double* term_loss;
+  double* gt1; double* gt2;              // v2 tau gradients, contiguous [gt1 | gt2] (send)
+  double* send;                          // [5][Bl] packed payload
+  const double* recv;                    // [K][5][Bl] (== send when K == 1)
+  const double* gt_recv;                 // [K][2][Bl] (== gt1 when K == 1)
+  // pass-2 parameters
+  float4* par1; float4* par2;            // [B]
+  float* rcoef;                          // [Bl]
+  double* red;                           // [2] local G_tau, loss numerator (all-reduced)
+  int* err;
+  StepResult* result;
+};
+
+__global__ void fc_diag_kernel(const __nv_bfloat16* __restrict__ e1, const __nv_bfloat16* __restrict__ e2,
+                               int B, int d, float* __restrict__ diag);
+__global__ void fc_rowpar_kernel(StepArgs a);
+__global__ void fc_table_kernel(StepArgs a, double gamma);
+__global__ void fc_weights_kernel(StepArgs a, double eps);
+__global__ void fc_reduce_kernel(StepArgs a);
+__global__ void fc_finalize_kernel(StepArgs a);
+__global__ void fc_indiv_update_kernel(StepArgs a);
+
+}  // namespace fc

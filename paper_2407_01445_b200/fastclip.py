@@ -1,0 +1,278 @@
+"""Host-side mirror of the reference loss-step interface over the C ABI (include/fastclip_b200.h).
+
+The reference drives the step through C++ namespace calls from Trainer::run
+(trainer.cpp:427-589); this module exposes the same step as one object per rank:
+
+    cfg  = config_defaults("fastclip_v3", n_train, dim=512, local_batch=5120)
+    step = LossStep(cfg)                        # UTable / IndividualTemp / Replica tau in HBM
+    de1, de2 = step.step(e1, e2, ids, gamma, eps)   # bf16 [Bl, d] CUDA tensors, int32 ids
+    s = step.scalars()                          # loss, G_tau, tau, clamps, latch
+
+There is no CPU fallback: every call goes to the sm_100a kernels in lib/libfastclip_b200.so,
+and a missing or unloadable library raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import build as _build
+
+VARIANTS = {
+    "openclip_mbcl": 0, "sogclr": 1, "isogclr": 2, "fastclip_v0": 3, "fastclip_v1": 4,
+    "fastclip_v2": 5, "fastclip_v3": 6,
+}
+VARIANT_NAMES = {v: k for k, v in VARIANTS.items()}
+
+ERRORS = {
+    1: "ConfigError", 2: "ShapeError", 3: "DegenerateBatchError", 4: "DomainError",
+    5: "OwnershipViolation", 6: "StalenessError", 7: "CollectiveShapeError",
+    8: "CollectiveAborted", 9: "NumericError", 10: "IoError", 11: "CudaError", 12: "NcclError",
+    13: "Unsupported",
+}
+
+
+class FastclipError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"{ERRORS.get(code, 'Error')} ({code}): {msg}")
+        self.code = code
+        self.kind = ERRORS.get(code, "Error")
+
+
+class FcConfig(C.Structure):
+    _fields_ = [
+        ("variant", C.c_int32), ("n_train", C.c_int64), ("dim", C.c_int32),
+        ("local_batch", C.c_int32), ("world", C.c_int32), ("rank", C.c_int32),
+        ("tau_init", C.c_double), ("tau0", C.c_double), ("rho", C.c_double),
+        ("tau_lr", C.c_double), ("beta1", C.c_double), ("beta2", C.c_double),
+        ("adam_eps", C.c_double), ("lr_decay_enabled", C.c_int32),
+        ("lr_decay_threshold", C.c_double), ("lr_decay_factor", C.c_double),
+        ("scale_by_tau", C.c_int32), ("device", C.c_int32), ("nccl_id", C.c_uint8 * 128),
+    ]
+
+
+class FcStepIn(C.Structure):
+    _fields_ = [("e1", C.c_void_p), ("e2", C.c_void_p), ("ids", C.c_void_p),
+                ("gamma", C.c_double), ("eps", C.c_double)]
+
+
+class FcStepOut(C.Structure):
+    _fields_ = [("de1", C.c_void_p), ("de2", C.c_void_p)]
+
+
+class FcStepScalars(C.Structure):
+    _fields_ = [("loss", C.c_double), ("gtau", C.c_double), ("tau", C.c_double),
+                ("exp_clamps", C.c_uint64), ("latched", C.c_int32)]
+
+
+_lib = None
+
+
+def lib():
+    """Loads (building if needed) the in-tree sm_100a library; raises if unavailable."""
+    global _lib
+    if _lib is None:
+        path = _build.build()
+        if not os.path.exists(path):
+            raise FastclipError(11, f"CUDA library missing: {path}")
+        L = C.CDLL(path)
+        D, I32, I64, P = C.c_double, C.c_int32, C.c_int64, C.c_void_p
+        L.fc_config_defaults.argtypes = [I32, I64, C.POINTER(FcConfig)]
+        L.fc_gamma_at.restype = D
+        L.fc_gamma_at.argtypes = [I32, D, D, I64, I64, I64]
+        L.fc_epsilon_at.restype = D
+        L.fc_epsilon_at.argtypes = [D, D, I64, I64]
+        L.fc_nccl_unique_id.argtypes = [C.POINTER(C.c_uint8 * 128)]
+        L.fc_create.argtypes = [C.POINTER(FcConfig), C.POINTER(P)]
+        L.fc_destroy.argtypes = [P]
+        L.fc_loss_step.argtypes = [P, C.POINTER(FcStepIn), C.POINTER(FcStepOut), P]
+        L.fc_step_scalars_get.argtypes = [P, C.POINTER(FcStepScalars)]
+        DP = C.POINTER(C.c_double)
+        LP = C.POINTER(C.c_int64)
+        L.fc_local_views.argtypes = [P, DP, DP, DP, DP, DP, DP]
+        L.fc_table_download.argtypes = [P, DP, DP, DP, DP, DP, DP, LP, DP, DP, LP]
+        L.fc_table_upload.argtypes = [P, DP, DP, DP, DP, DP, DP, LP, DP, DP, LP]
+        L.fc_tau_state_get.argtypes = [P, DP, DP, DP, LP, C.POINTER(C.c_int32)]
+        L.fc_tau_state_set.argtypes = [P, D, D, D, I64, I32]
+        L.fc_kernels_per_step.argtypes = [P]
+        L.fc_set_phase_timing.argtypes = [P, I32]
+        L.fc_phase_times.argtypes = [P, C.POINTER(C.c_float), I32]
+        L.fc_debug_similarity.argtypes = [P, P, I32, I32, I32, P, P]
+        L.fc_last_error.restype = C.c_char_p
+        _lib = L
+    return _lib
+
+
+EXPORTED = [
+    "fc_config_defaults", "fc_gamma_at", "fc_epsilon_at", "fc_nccl_unique_id", "fc_create",
+    "fc_destroy", "fc_loss_step", "fc_step_scalars_get", "fc_local_views", "fc_table_download",
+    "fc_table_upload", "fc_tau_state_get", "fc_tau_state_set", "fc_kernels_per_step",
+    "fc_debug_similarity", "fc_last_error", "fc_set_phase_timing", "fc_phase_times",
+]
+PHASES = ["allgather_e", "prep", "pass1_stats", "tables_tau", "pass2_q", "grad_gemm"]
+
+
+def _check(rc: int):
+    if rc != 0:
+        raise FastclipError(rc, lib().fc_last_error().decode(errors="replace"))
+
+
+def config_defaults(variant, n_train: int, **fields) -> FcConfig:
+    """resolve_algo_config's defaults for the loss step (trainer.cpp:139-194)."""
+    v = VARIANTS[variant] if isinstance(variant, str) else int(variant)
+    cfg = FcConfig()
+    _check(lib().fc_config_defaults(v, int(n_train), C.byref(cfg)))
+    for k, val in fields.items():
+        setattr(cfg, k, val)
+    return cfg
+
+
+def gamma_at(t: int, *, cosine: bool = True, constant: float = 0.6, gamma_min: float = 0.2,
+             decay_epochs: int = 1, iters_per_epoch: int = 1) -> float:
+    """GammaSchedule::at (schedules.cpp:25-31)."""
+    return lib().fc_gamma_at(int(cosine), constant, gamma_min, decay_epochs, iters_per_epoch, t)
+
+
+def epsilon_at(epoch: int, initial: float = 1e-14, late: float = 1e-14, switch_epoch: int = -1) -> float:
+    """EpsilonSchedule::at (schedules.cpp:62-65)."""
+    return lib().fc_epsilon_at(initial, late, switch_epoch, epoch)
+
+
+def nccl_unique_id() -> bytes:
+    buf = (C.c_uint8 * 128)()
+    _check(lib().fc_nccl_unique_id(C.byref(buf)))
+    return bytes(buf)
+
+
+@dataclass
+class StepScalars:
+    loss: float
+    gtau: float
+    tau: float
+    exp_clamps: int
+    latched: int
+
+
+def _dptr(t) -> int:
+    return int(t.data_ptr())
+
+
+class LossStep:
+    """One rank of the FastCLIP loss step (trainer.cpp:427-589) on a B200."""
+
+    def __init__(self, cfg: FcConfig):
+        self.cfg = cfg
+        self._h = C.c_void_p()
+        _check(lib().fc_create(C.byref(cfg), C.byref(self._h)))
+        self.variant = VARIANT_NAMES[cfg.variant]
+        self.individual = cfg.variant in (2, 5)
+        self._out = None
+
+    def close(self):
+        if self._h:
+            lib().fc_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def kernels_per_step(self) -> int:
+        return lib().fc_kernels_per_step(self._h)
+
+    def step(self, e1, e2, ids, gamma: float, eps: float, de1=None, de2=None, stream=None):
+        """Enqueues one step on ``stream`` (default: torch's current stream)."""
+        import torch
+        bl, d = self.cfg.local_batch, self.cfg.dim
+        for name, t in (("e1", e1), ("e2", e2)):
+            if t.dtype != torch.bfloat16 or not t.is_cuda or tuple(t.shape) != (bl, d) or not t.is_contiguous():
+                raise FastclipError(2, f"{name} must be a contiguous CUDA bf16 tensor of shape ({bl}, {d})")
+        if ids.dtype != torch.int32 or not ids.is_cuda or ids.numel() != bl:
+            raise FastclipError(2, f"ids must be a CUDA int32 tensor with {bl} entries")
+        if de1 is None or de2 is None:
+            if self._out is None:
+                self._out = (torch.empty(bl, d, device=e1.device, dtype=torch.float32),
+                             torch.empty(bl, d, device=e1.device, dtype=torch.float32))
+            de1, de2 = self._out
+        if stream is None:
+            stream = torch.cuda.current_stream(e1.device)
+        sin = FcStepIn(_dptr(e1), _dptr(e2), _dptr(ids), float(gamma), float(eps))
+        sout = FcStepOut(_dptr(de1), _dptr(de2))
+        _check(lib().fc_loss_step(self._h, C.byref(sin), C.byref(sout), C.c_void_p(stream.cuda_stream)))
+        return de1, de2
+
+    def enable_phase_timing(self):
+        _check(lib().fc_set_phase_timing(self._h, 1))
+
+    def phase_times(self) -> dict:
+        ms = (C.c_float * len(PHASES))()
+        _check(lib().fc_phase_times(self._h, ms, len(PHASES)))
+        return dict(zip(PHASES, list(ms)))
+
+    def scalars(self) -> StepScalars:
+        s = FcStepScalars()
+        _check(lib().fc_step_scalars_get(self._h, C.byref(s)))
+        return StepScalars(s.loss, s.gtau, s.tau, int(s.exp_clamps), int(s.latched))
+
+    def local_views(self) -> dict:
+        n = self.cfg.local_batch
+        arrs = {k: np.zeros(n) for k in ("g1", "g2", "u1", "u2", "t1", "t2")}
+        p = [arrs[k].ctypes.data_as(C.POINTER(C.c_double)) for k in ("g1", "g2", "u1", "u2", "t1", "t2")]
+        _check(lib().fc_local_views(self._h, *p))
+        return arrs
+
+    def tables(self) -> dict:
+        n = self.cfg.n_train
+        t = {"u1": np.zeros(n), "u2": np.zeros(n)}
+        if self.individual:
+            t.update(tau1=np.zeros(n), tau2=np.zeros(n), m1=np.zeros(n), v1=np.zeros(n),
+                     s1=np.zeros(n, np.int64), m2=np.zeros(n), v2=np.zeros(n), s2=np.zeros(n, np.int64))
+        _check(lib().fc_table_download(self._h, *self._tab_ptrs(t)))
+        return t
+
+    def load_tables(self, **t):
+        n = self.cfg.n_train
+        full = {}
+        for k in ("u1", "u2", "tau1", "tau2", "m1", "v1", "s1", "m2", "v2", "s2"):
+            if k in t and t[k] is not None:
+                dt = np.int64 if k in ("s1", "s2") else np.float64
+                a = np.ascontiguousarray(t[k], dtype=dt)
+                if a.shape != (n,):
+                    raise FastclipError(10, f"table {k} must have {n} entries")
+                full[k] = a
+        _check(lib().fc_table_upload(self._h, *self._tab_ptrs(full)))
+
+    @staticmethod
+    def _tab_ptrs(t):
+        out = []
+        for k in ("u1", "u2", "tau1", "tau2", "m1", "v1", "s1", "m2", "v2", "s2"):
+            a = t.get(k)
+            typ = C.c_int64 if k in ("s1", "s2") else C.c_double
+            out.append(a.ctypes.data_as(C.POINTER(typ)) if a is not None else None)
+        return out
+
+    def tau_state(self) -> dict:
+        tau, m, v = C.c_double(), C.c_double(), C.c_double()
+        st, lat = C.c_int64(), C.c_int32()
+        _check(lib().fc_tau_state_get(self._h, C.byref(tau), C.byref(m), C.byref(v), C.byref(st), C.byref(lat)))
+        return dict(tau=tau.value, m=m.value, v=v.value, step=st.value, latched=lat.value)
+
+    def set_tau_state(self, tau: float, m: float = 0.0, v: float = 0.0, step: int = 0, latched: int = 0):
+        _check(lib().fc_tau_state_set(self._h, tau, m, v, step, latched))
+
+
+def debug_similarity(a, b):
+    """S = a b^T through the pass-1 tcgen05 tile kernel (fp32), for kernel unit tests."""
+    import torch
+    rows, d = a.shape
+    cols = b.shape[0]
+    out = torch.empty(rows, cols, device=a.device, dtype=torch.float32)
+    stream = torch.cuda.current_stream(a.device)
+    _check(lib().fc_debug_similarity(_dptr(a), _dptr(b), rows, cols, d, _dptr(out), C.c_void_p(stream.cuda_stream)))
+    return out

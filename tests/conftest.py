@@ -27,3 +27,17 @@ _ensure_oracle_built()
 def golden_files():
     d = os.path.join(ROOT, "tests", "golden")
     return sorted(os.path.join(d, f) for f in os.listdir(d) if f.endswith(".npz"))
+
+
+def pytest_collection_modifyitems(config, items):
+    try:
+        import torch
+        has_gpu = torch.cuda.is_available()
+    except Exception:
+        has_gpu = False
+    if has_gpu:
+        return
+    skip = pytest.mark.skip(reason="no CUDA device in this container")
+    for it in items:
+        if "gpu" in it.keywords:
+            it.add_marker(skip)

@@ -1,0 +1,111 @@
+"""GPU parity tests: the sm_100a kernels through the C ABI vs the oracle / golden vectors.
+
+Tolerances (north_star; bf16 inputs, fp32 accumulation, bf16 Q tile):
+  * table indexing: bit-exact (untouched entries identical, touched entries at the right ids)
+  * g, u, tau, G_tau, loss: max relative error <= 1e-3
+  * dE1, dE2: norm-relative error <= 1e-3
+"""
+import numpy as np
+import pytest
+
+import oracle as O
+from gpu_helpers import norm_rel, rel, run_pair, gpu_cfg, to_dev_bf16
+from paper_2407_01445_b200 import synthetic as S
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-3
+
+
+def _check(got, ref, what=""):
+    assert rel(got["g1"], ref["g1"][: len(got["g1"])]) < TOL, what
+    assert rel(got["g2"], ref["g2"][: len(got["g2"])]) < TOL, what
+    assert rel(got["u1"], ref["u1"][: len(got["u1"])]) < TOL, what
+    assert rel(got["u2"], ref["u2"][: len(got["u2"])]) < TOL, what
+    assert abs(got["loss"] - ref["loss"]) <= TOL * abs(ref["loss"]) + 1e-12, (what, got["loss"], ref["loss"])
+    assert abs(got["tau_new"] - ref["tau_new"]) <= TOL * abs(ref["tau_new"]), (what, got["tau_new"], ref["tau_new"])
+    if ref["gtau"] != 0.0:
+        assert abs(got["gtau"] - ref["gtau"]) <= TOL * abs(ref["gtau"]), (what, got["gtau"], ref["gtau"])
+    n = got["dE1"].shape[0]
+    assert norm_rel(got["dE1"], ref["dE1"][:n]) < TOL, (what, norm_rel(got["dE1"], ref["dE1"][:n]))
+    assert norm_rel(got["dE2"], ref["dE2"][:n]) < TOL, (what, norm_rel(got["dE2"], ref["dE2"][:n]))
+
+
+def test_similarity_tile_kernel_matches_torch():
+    import torch
+    import paper_2407_01445_b200 as P
+    for rows, cols, d in ((256, 256, 64), (512, 768, 512), (300, 200, 136), (40, 1000, 1024)):
+        g = torch.Generator().manual_seed(rows + cols + d)
+        a = torch.randn(rows, d, generator=g).to(torch.bfloat16).cuda()
+        b = torch.randn(cols, d, generator=g).to(torch.bfloat16).cuda()
+        s = P.debug_similarity(a, b)
+        torch.cuda.synchronize()
+        ref = a.double() @ b.double().T
+        err = (s.double() - ref).abs().max().item() / ref.abs().max().item()
+        assert err < 1e-5, (rows, cols, d, err)
+
+
+@pytest.mark.parametrize("variant", ["fastclip_v3", "fastclip_v0", "fastclip_v1", "fastclip_v2",
+                                     "sogclr", "isogclr", "openclip_mbcl"])
+def test_step_matches_oracle_small(variant):
+    res, tabs, st, _ = run_pair(variant, B=96, d=64, N=500, steps=3, seed=11)
+    for i, (got, ref) in enumerate(res):
+        _check(got, ref, f"{variant} step {i}")
+    # table indexing is bit-exact: untouched entries identical, touched ones within tolerance
+    touched = np.zeros(500, bool)
+    for s in range(3):
+        touched[S.ids(96, 500, 11 * 1000 + s)] = True
+    np.testing.assert_array_equal(tabs["u1"][~touched], st.u1[~touched])
+    assert rel(tabs["u1"][touched], st.u1[touched]) < TOL
+    if "tau1" in tabs:
+        np.testing.assert_array_equal(tabs["tau1"][~touched], st.tau1[~touched])
+        assert rel(tabs["tau1"][touched], st.tau1[touched]) < TOL
+        np.testing.assert_array_equal(tabs["s1"], st.s1)
+
+
+def test_step_config1_shape_v3():
+    # BASELINE config 1: v3, B = 256, d = 512 (one pair tile)
+    res, _, _, _ = run_pair("fastclip_v3", B=256, d=512, N=20000, steps=2, seed=3)
+    for i, (got, ref) in enumerate(res):
+        _check(got, ref, f"config1 step {i}")
+
+
+def test_step_ragged_and_multi_tile():
+    # B not a multiple of the 256 tile, several row blocks and column tiles, d not a multiple of 64
+    res, _, _, _ = run_pair("fastclip_v3", B=600, d=200, N=5000, steps=2, seed=5)
+    for i, (got, ref) in enumerate(res):
+        _check(got, ref, f"ragged step {i}")
+
+
+def test_step_tau_floor_clamps():
+    # tau at the floor: safe_exp clamps (losses.cpp:22-28) are hit and counted
+    res, _, _, _ = run_pair("fastclip_v3", B=128, d=64, N=1000, steps=1, seed=7, cfg_over=dict(tau_init=0.005))
+    got, ref = res[0]
+    _check(got, ref, "clamp")
+    assert ref["clamps_g"] > 0
+    assert got["clamps_g"] == pytest.approx(ref["clamps_g"], rel=0.02, abs=2)
+
+
+def test_golden_fixtures_k1(golden_files):
+    import torch
+    import paper_2407_01445_b200 as P
+    for path in golden_files:
+        z = np.load(path)
+        if int(z["K"]) != 1:
+            continue
+        cfg = {k[4:]: z[k].item() for k in z.files if k.startswith("cfg_")}
+        B, d = int(z["B"]), int(z["d"])
+        step = P.LossStep(gpu_cfg(cfg, d, B))
+        step.load_tables(u1=z["state0_u1"], u2=z["state0_u2"])
+        for s in range(int(z["steps"])):
+            de1, de2 = step.step(to_dev_bf16(z[f"s{s}_E1bits"]), to_dev_bf16(z[f"s{s}_E2bits"]),
+                                 torch.from_numpy(z[f"s{s}_ids"]).cuda(), float(z["gamma"]), float(z["eps"]))
+            sc = step.scalars()
+            v = step.local_views()
+            got = dict(dE1=de1.cpu().numpy(), dE2=de2.cpu().numpy(), loss=sc.loss, gtau=sc.gtau,
+                       tau_new=sc.tau, **v)
+            ref = {k: z[f"s{s}_{k}"] for k in ("dE1", "dE2", "g1", "g2", "u1", "u2")}
+            ref.update(loss=float(z[f"s{s}_loss"]), gtau=float(z[f"s{s}_gtau"]),
+                       tau_new=float(z[f"s{s}_tau_new"]))
+            _check(got, ref, f"{path} s{s}")
+        np.testing.assert_allclose(step.tables()["u1"], z["state_end_u1"], rtol=TOL)
