@@ -221,7 +221,6 @@ def main():
             cfg.nccl_id[i] = b
     step = P.LossStep(cfg)
     step.load_tables(u1=S.warm_u(N, 1), u2=S.warm_u(N, 2))
-    step.enable_phase_timing()
 
     n_sets = 4
     host_sets = make_inputs(B, d, N, world, rank, n_sets)
@@ -245,10 +244,9 @@ def main():
     torch.cuda.synchronize()
     sc = step.scalars()
 
-    # ---------------- device-timed steps ----------------
+    # ---------------- device-timed steps (CUDA-graph replay, no host sync inside) ----------------
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    phase_sum = {k: 0.0 for k in P.fastclip.PHASES}
     clocks = ClockSampler(local)
     barrier()
     torch.cuda.synchronize()
@@ -259,8 +257,6 @@ def main():
         starts[i].record(stream)
         step.step(e1, e2, ids, gamma, eps, de1, de2, stream)
         ends[i].record(stream)
-        for k, v in step.phase_times().items():
-            phase_sum[k] += v
     torch.cuda.synchronize()
     barrier()
     clk = clocks.stop()
@@ -273,7 +269,22 @@ def main():
         total_ms = float(t.item())
     ms_per_step = total_ms / args.steps
     value = 1e3 / ms_per_step
+
+    # ---------------- per-kernel durations: CUDA events between the step's phases ----------------
+    # (event-record nodes inside the replayed graph, same stream, same inputs; K more steps)
+    step.enable_phase_timing()
+    for i in range(2):
+        e1, e2, ids = dev_sets[i % n_sets]
+        step.step(e1, e2, ids, gamma, eps, de1, de2, stream)
+    phase_sum = {k: 0.0 for k in P.fastclip.PHASES}
+    for i in range(args.steps):
+        flush.zero_()
+        e1, e2, ids = dev_sets[i % n_sets]
+        step.step(e1, e2, ids, gamma, eps, de1, de2, stream)
+        for k, v in step.phase_times().items():
+            phase_sum[k] += v
     phases = {k: v / args.steps for k, v in phase_sum.items()}
+    step.disable_phase_timing()
 
     # ---------------- end to end through the public API (host buffers) ----------------
     e2e = None
@@ -301,6 +312,7 @@ def main():
             step.step(db[0], db[1], db[2], gamma, eps, de1, de2, stream)
             s1.record(stream)
             _ = step.scalars()      # device -> host read of the step result (loss, G_tau, tau)
+            s1.synchronize()
             t_e2e.append(s0.elapsed_time(s1))
         tot = float(sum(t_e2e))
         if world > 1:

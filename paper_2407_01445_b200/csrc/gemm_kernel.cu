@@ -41,10 +41,12 @@ __device__ __forceinline__ void gdecode(const GemmParams& p, int item, int& s, i
   const int per_seg0 = p.n_mb[0] * p.n_nb * p.n_split;
   s = item < per_seg0 ? 0 : 1;
   int local = item - (s ? per_seg0 : 0);
-  ks = local % p.n_split;
-  local /= p.n_split;
+  // column block fastest: pairs running side by side read the same Q' rows and K range,
+  // so the second read of each Q' tile is an L2 hit (Q' is streamed from HBM once).
   nb = local % p.n_nb;
-  mb = local / p.n_nb;
+  local /= p.n_nb;
+  ks = local % p.n_split;
+  mb = local / p.n_split;
 }
 
 }  // namespace
@@ -106,7 +108,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           else
             mbar_arrive_cluster(&L.full[stage], 0);
           uint8_t* sb = L.b + stage * kStageBytesB;
-          tma_load_2d_pair(mq, &L.full[stage], L.a + stage * kStageBytesA, kb * kBlockK, a_row);
+          if (p.seg[s].a_mn_major) {
+            // A = Q^T: two 64(M) x 64(K) swizzle atoms of the row-major Q (K = rows of Q)
+            uint8_t* sa = L.a + stage * kStageBytesA;
+            tma_load_2d_pair(mq, &L.full[stage], sa, a_row, kb * kBlockK);
+            tma_load_2d_pair(mq, &L.full[stage], sa + kStageBytesA / 2, a_row + 64, kb * kBlockK);
+          } else {
+            tma_load_2d_pair(mq, &L.full[stage], L.a + stage * kStageBytesA, kb * kBlockK, a_row);
+          }
           // MN-major B: two 64(N) x 64(K) swizzle atoms for this CTA's 128 columns of N.
           tma_load_2d_pair(mx, &L.full[stage], sb, n0, kb * kBlockK);
           tma_load_2d_pair(mx, &L.full[stage], sb + kStageBytesB / 2, n0 + 64, kb * kBlockK);
@@ -117,7 +126,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   } else if (warp == 1) {
     // ===================== MMA issuer (leader) =====================
     if (rank == 0) {
-      constexpr uint32_t idesc = make_idesc_bf16(kPairM, kPairN, 0, 1);
+      constexpr uint32_t idesc_k = make_idesc_bf16(kPairM, kPairN, 0, 1);
+      constexpr uint32_t idesc_mn = make_idesc_bf16(kPairM, kPairN, 1, 1);
       uint32_t stage = 0, phase = 0;
       int it = 0;
       for (int item = pair; item < p.n_items; item += n_pairs, ++it) {
@@ -125,6 +135,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         gdecode(p, item, s, mb, nb, ks);
         const int kb0 = ks * p.kb_per_split;
         const int kb1 = min(p.kb_total, kb0 + p.kb_per_split);
+        const bool a_mn = p.seg[s].a_mn_major != 0;
+        const uint32_t idesc = a_mn ? idesc_mn : idesc_k;
         const uint32_t acc = it & 1;
         const uint32_t acc_phase = (it >> 1) & 1;
         mbar_wait(&L.tempty[acc], acc_phase ^ 1);
@@ -138,7 +150,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             const uint32_t b0 = smem_u32(L.b + stage * kStageBytesB);
 #pragma unroll
             for (int k = 0; k < kBlockK / 16; ++k) {
-              const uint64_t ad = make_sdesc_sw128(a0 + k * 32, 0, 1024);
+              const uint64_t ad = a_mn ? make_sdesc_sw128(a0 + k * 2048, kStageBytesA / 2, 1024)
+                                       : make_sdesc_sw128(a0 + k * 32, 0, 1024);
               // MN-major SW128: 16 K rows of 128 B per UMMA_K; LBO = next 64-wide N atom.
               const uint64_t bd = make_sdesc_sw128(b0 + k * 2048, kStageBytesB / 2, 1024);
               mma_bf16_pair(d_tmem, ad, bd, idesc, (kb != kb0) || (k != 0));
@@ -226,14 +239,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   if (warp == 2) tmem_dealloc<2>(tmem_base, 512);
 }
 
+cudaError_t gemm_set_smem() {
+  return cudaFuncSetAttribute(grad_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
+}
+
 cudaError_t launch_gemm(const GemmParams& p, const CUtensorMap* mapQ, const CUtensorMap* mapX, int grid,
                         cudaStream_t s) {
   const CUtensorMap& q1 = p.nseg > 1 ? mapQ[1] : mapQ[0];
   const CUtensorMap& x1 = p.nseg > 1 ? mapX[1] : mapX[0];
   if (grid < 2) grid = 2;
   grid &= ~1;
-  cudaError_t e = cudaFuncSetAttribute(grad_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
-  if (e != cudaSuccess) return e;
   grad_gemm_kernel<<<grid, kThreads, kSmemBytes, s>>>(p, mapQ[0], mapX[0], q1, x1);
   return cudaGetLastError();
 }

@@ -13,11 +13,22 @@ constexpr int kPairM = 256;      // rows per pair tile (128 per CTA)
 constexpr int kCtaM = 128;       // TMEM lanes / rows per CTA
 constexpr int kPairN = 256;      // columns per pair tile (UMMA N)
 constexpr int kBlockK = 64;      // bf16 per 128-byte swizzle atom
-constexpr int kStages = 4;       // TMA -> MMA ring depth
 constexpr int kEpiWarps = 8;     // 2 per TMEM lane quarter (column halves)
 constexpr int kThreads = (2 + kEpiWarps) * 32;
 constexpr int kStageBytesA = kCtaM * kBlockK * 2;        // 16 KB
 constexpr int kStageBytesB = (kPairN / 2) * kBlockK * 2;  // 16 KB (own half of N)
+// similarity kernel: A (the anchor rows) stays resident for up to 8 K blocks (d <= 512;
+// larger d streams A in 512-wide chunks through the same slots), B streams through a ring.
+constexpr int kSimASlots = 8;
+constexpr int kSimStages = 5;
+constexpr int kSimEpiWarps = 16;   // 4 per TMEM lane quarter, 64 columns each
+constexpr int kSimThreads = (2 + kSimEpiWarps) * 32;
+constexpr int kSimPSlots = 3;      // column-parameter slots (Q pass): kappa, beta, coef x 256
+constexpr int kSimPSlotBytes = 3 * kPairN * 4;
+constexpr int kSimSmemBytes =
+    kSimASlots * kStageBytesA + kSimStages * kStageBytesB + kSimPSlots * kSimPSlotBytes + 1024 + 512;
+// gradient GEMM: A (Q') and B (E) both stream.
+constexpr int kStages = 6;
 constexpr int kSmemBytes = kStages * (kStageBytesA + kStageBytesB) + 1024 /*align*/ + 256 /*barriers*/;
 
 // ---- similarity-tile kernel (pass 1: row statistics; pass 2: Q tiles) ----
@@ -28,10 +39,11 @@ struct SimSeg {
   int rows;                 // local anchors in this segment
   int a_row0;               // global index of local row 0 (diagonal masking)
   int cols;                 // contrast set size (global batch B)
-  const float2* row_stat;   // STATS: [rows] {S_ii, 1/t_i * log2(e)}
-  float2* partial;          // STATS: [rows][n_jt*2] {sum e, sum (s - s_ii) e}
-  const float4* row_par;    // Q: [rows] {S_ii, log2(e)/t_i, coef_i, 0}
-  const float4* col_par;    // Q: [cols] {S_jj, log2(e)/t_j, coef_j, 0}
+  const float2* row_stat;   // STATS: [rows] {S_ii, log2(e)/t_i}
+  float2* partial;          // STATS: [rows][n_jt*4] {sum e, sum (s - s_ii) e} per column quarter
+  // Q: exponent y = s*kappa + beta (= (s - S_aa) log2(e)/t_a), weight coef (SoA, fp32)
+  const float* row_kappa; const float* row_beta; const float* row_coef;   // [rows]
+  const float* col_kappa; const float* col_beta; const float* col_coef;   // [n_jt*256], zero padded
   __nv_bfloat16* q;         // Q: [rows][ldq]
 };
 struct SimParams {
@@ -47,6 +59,7 @@ struct SimParams {
 
 // ---- weighted-gradient GEMM: out = scale * (Q' X - r o X_local) ----
 struct GemmSeg {
+  int a_mn_major;            // 1: A = Q'^T read through an MN-major operand (K = 1 shares Q)
   int rows;                  // local anchors
   int x_row0;                // global index of local row 0 (for the r o X_local term)
   const float* r;            // [rows]
@@ -70,6 +83,8 @@ enum SimMode { kSimStats = 0, kSimQ = 1, kSimRaw = 2 };
 
 cudaError_t launch_sim(int mode, const SimParams& p, const CUtensorMap* mapA, const CUtensorMap* mapB,
                        int grid, cudaStream_t s, float* raw_out);
+cudaError_t sim_set_smem();
+cudaError_t gemm_set_smem();
 cudaError_t launch_gemm(const GemmParams& p, const CUtensorMap* mapQ, const CUtensorMap* mapX, int grid,
                         cudaStream_t s);
 

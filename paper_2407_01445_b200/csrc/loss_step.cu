@@ -109,25 +109,40 @@ struct LossStep {
   float2 *rowstat = nullptr, *partial = nullptr;
   unsigned long long* clamps = nullptr;
   double* f64 = nullptr;   // per-local-anchor fp64 arrays
-  double *send = nullptr, *recv = nullptr, *gt_recv = nullptr, *red = nullptr;
-  float4 *par1 = nullptr, *par2 = nullptr;
+  double *send = nullptr, *recv = nullptr, *gt_recv = nullptr, *red = nullptr, *blockpart = nullptr;
+  unsigned* counter = nullptr;
+  float* par = nullptr;   // 6 x [n_jt*256]: kap1, bet1, coef1, kap2, bet2, coef2
   float* rcoef = nullptr;
   __nv_bfloat16* q = nullptr;   // [2][Bl][ldq]
   int* err = nullptr;
   fc::StepResult* result_d = nullptr;
   fc::StepResult* result_h = nullptr;   // pinned
-  cudaEvent_t done{};
+  cudaEvent_t done{}, fork{};
+  cudaStream_t ws = nullptr;     // context stream (capturable), joined to the caller's stream
+  double* scal = nullptr;        // device {gamma_t, eps_t}
+  bool use_graph = true;
+  bool shared_q = true;          // K == 1: one Q pass, Q^T read by the dE2 GEMM
+  struct GraphEntry {
+    const void* key[5];
+    cudaGraphExec_t exec;
+  };
+  std::vector<GraphEntry> graphs;
   // optional per-phase CUDA events (bench roofline): phases of the last step
   static constexpr int kPhases = 6;   // gatherE, prep, pass1, scalars, pass2, gemm
-  bool timing = false;
+  bool timing = false, ev_created = false;
   cudaEvent_t ev[kPhases + 1]{};
+  bool debug_sync = false;
   void mark(int i, cudaStream_t st) {
+    if (debug_sync) {
+      cudaError_t e = cudaStreamSynchronize(st);
+      std::fprintf(stderr, "[fc] phase %d reached (%s)\n", i, cudaGetErrorString(e));
+    }
     if (timing) FC_CUDA(cudaEventRecord(ev[i], st));
   }
   // cached descriptors
   const void* map_e1 = nullptr;
   const void* map_e2 = nullptr;
-  CUtensorMap mE1k, mE2k, mE1n, mE2n, mQ[2];
+  CUtensorMap mE1k, mE2k, mE1n, mE2n, mQ[2], mQt;
   int n_split = 4;
   fc::StepArgs args{};
 
@@ -185,15 +200,18 @@ struct LossStep {
     }
     diag = dalloc<float>(B);
     rowstat = dalloc<float2>(2 * static_cast<size_t>(Bl));
-    partial = dalloc<float2>(2 * static_cast<size_t>(Bl) * n_jt * 2);
+    partial = dalloc<float2>(2 * static_cast<size_t>(Bl) * n_jt * 4);
     clamps = dalloc<unsigned long long>(1);
     f64 = dalloc<double>(static_cast<size_t>(Bl) * 18);
     send = dalloc<double>(5 * static_cast<size_t>(Bl));
     recv = K > 1 ? dalloc<double>(5 * static_cast<size_t>(B)) : send;
     gt_recv = K > 1 ? dalloc<double>(2 * static_cast<size_t>(B)) : nullptr;
     red = dalloc<double>(2);
-    par1 = dalloc<float4>(B);
-    par2 = dalloc<float4>(B);
+    blockpart = dalloc<double>(3 * static_cast<size_t>((B + 255) / 256));
+    counter = dalloc<unsigned>(1);
+    FC_CUDA(cudaMemset(counter, 0, sizeof(unsigned)));
+    par = dalloc<float>(6 * static_cast<size_t>(n_jt) * fc::kPairN);
+    FC_CUDA(cudaMemset(par, 0, 6 * static_cast<size_t>(n_jt) * fc::kPairN * 4));
     rcoef = dalloc<float>(Bl);
     q = dalloc<__nv_bfloat16>(2 * static_cast<size_t>(Bl) * ldq);
     err = dalloc<int>(1);
@@ -202,8 +220,19 @@ struct LossStep {
     FC_CUDA(cudaMallocHost(&result_h, sizeof(fc::StepResult)));
     std::memset(result_h, 0, sizeof(*result_h));
     FC_CUDA(cudaEventCreateWithFlags(&done, cudaEventDisableTiming));
+    FC_CUDA(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming));
+    FC_CUDA(cudaStreamCreateWithFlags(&ws, cudaStreamNonBlocking));
+    scal = dalloc<double>(2);
+    if (const char* e = std::getenv("FC_GRAPH")) use_graph = atoi(e) != 0;
+    shared_q = K == 1;
+    if (const char* e = std::getenv("FC_DEBUG_SYNC")) debug_sync = atoi(e) != 0;
+    if (debug_sync) use_graph = false;
+    if (const char* e = std::getenv("FC_SHARED_Q")) shared_q = shared_q && atoi(e) != 0;
+    FC_CUDA(fc::sim_set_smem());
+    FC_CUDA(fc::gemm_set_smem());
     mQ[0] = make_map(q, ldq, Bl, static_cast<uint64_t>(ldq) * 2, 64, 128);
     mQ[1] = make_map(q + static_cast<size_t>(Bl) * ldq, ldq, Bl, static_cast<uint64_t>(ldq) * 2, 64, 128);
+    mQt = make_map(q, ldq, Bl, static_cast<uint64_t>(ldq) * 2, 64, 64);   // Q^T as MN-major A (K = 1)
     build_args();
   }
 
@@ -220,7 +249,7 @@ struct LossStep {
     a.m1_tab = m1; a.v1_tab = v1; a.s1_tab = s1; a.m2_tab = m2; a.v2_tab = v2; a.s2_tab = s2;
     a.tau_state = tau_state;
     a.rowstat_R = rowstat; a.rowstat_C = rowstat + Bl;
-    a.partial_R = partial; a.partial_C = partial + static_cast<size_t>(Bl) * n_jt * 2;
+    a.partial_R = partial; a.partial_C = partial + static_cast<size_t>(Bl) * n_jt * 4;
     a.clamps = clamps;
     a.t_loc1 = F(0); a.t_loc2 = F(1);
     a.sum1 = F(2); a.dx1 = F(3); a.sum2 = F(4); a.dx2 = F(5);
@@ -229,7 +258,13 @@ struct LossStep {
     a.gt1 = F(13); a.gt2 = F(14);   // contiguous [gt1 | gt2]
     a.send = send; a.recv = recv;
     a.gt_recv = K > 1 ? gt_recv : F(13);
-    a.par1 = par1; a.par2 = par2; a.rcoef = rcoef; a.red = red; a.err = err; a.result = result_d;
+    const size_t np = static_cast<size_t>(n_jt) * fc::kPairN;
+    a.kap1 = par; a.bet1 = par + np; a.coef1 = par + 2 * np;
+    a.kap2 = par + 3 * np; a.bet2 = par + 4 * np; a.coef2 = par + 5 * np;
+    a.rcoef = rcoef;
+    a.blockpart = blockpart;
+    a.counter = counter;
+    a.fuse_finalize = K == 1 ? 1 : 0; a.red = red; a.err = err; a.result = result_d;
   }
 
   void ensure_maps(const void* e1, const void* e2) {
@@ -248,11 +283,53 @@ struct LossStep {
     return static_cast<int>(std::max<long>(1, pairs) * 2);
   }
 
-  void step(const fc_step_in* in, fc_step_out* out, cudaStream_t st) {
+  // Validates, stages the step scalars and runs the step on the context stream: replayed
+  // from a CUDA graph captured per (input, output) pointer set, or enqueued directly.
+  void step(const fc_step_in* in, fc_step_out* out, cudaStream_t caller) {
     if (!in || !out || !in->e1 || !in->e2 || !in->ids || !out->de1 || !out->de2)
       throw FcError{FC_ERR_SHAPE, "fc_loss_step: null input/output pointer"};
     if (in->eps < 0.0) throw FcError{FC_ERR_DOMAIN, "epsilon must be non-negative"};
     if (track_u && (!(in->gamma > 0.0) || in->gamma > 1.0)) throw FcError{FC_ERR_DOMAIN, "gamma must be in (0,1]"};
+    const double sc[2] = {in->gamma, in->eps};
+    FC_CUDA(cudaEventRecord(fork, caller));
+    FC_CUDA(cudaStreamWaitEvent(ws, fork, 0));
+    // pageable source: the values are staged at call time, the copy runs in stream order
+    FC_CUDA(cudaMemcpyAsync(scal, sc, sizeof(sc), cudaMemcpyHostToDevice, ws));
+    if (use_graph && !timing) {   // phase timing: direct launches (events between kernels)
+      const void* key[5] = {in->e1, in->e2, in->ids, out->de1, timing ? nullptr : out->de2};
+      cudaGraphExec_t exec = nullptr;
+      for (auto& g : graphs)
+        if (std::memcmp(g.key, key, sizeof(key)) == 0) exec = g.exec;
+      if (!exec) {
+        if (graphs.size() >= 8) {
+          cudaGraphExecDestroy(graphs.front().exec);
+          graphs.erase(graphs.begin());
+        }
+        cudaGraph_t graph;
+        FC_CUDA(cudaStreamBeginCapture(ws, cudaStreamCaptureModeThreadLocal));
+        try {
+          enqueue(in, out, ws);
+        } catch (...) {
+          cudaStreamEndCapture(ws, &graph);
+          throw;
+        }
+        FC_CUDA(cudaStreamEndCapture(ws, &graph));
+        FC_CUDA(cudaGraphInstantiate(&exec, graph, 0));
+        cudaGraphDestroy(graph);
+        GraphEntry ge;
+        std::memcpy(ge.key, key, sizeof(key));
+        ge.exec = exec;
+        graphs.push_back(ge);
+      }
+      FC_CUDA(cudaGraphLaunch(exec, ws));
+    } else {
+      enqueue(in, out, ws);
+    }
+    FC_CUDA(cudaEventRecord(done, ws));
+    FC_CUDA(cudaStreamWaitEvent(caller, done, 0));
+  }
+
+  void enqueue(const fc_step_in* in, fc_step_out* out, cudaStream_t st) {
     const __nv_bfloat16* E1 = static_cast<const __nv_bfloat16*>(in->e1);
     const __nv_bfloat16* E2 = static_cast<const __nv_bfloat16*>(in->e2);
     mark(0, st);
@@ -267,10 +344,10 @@ struct LossStep {
     ensure_maps(E1, E2);
     fc::StepArgs a = args;
     a.ids = in->ids;
+    a.scal = scal;
 
     mark(1, st);
-    fc::fc_diag_kernel<<<(B * 32 + 255) / 256, 256, 0, st>>>(E1, E2, B, d, diag);
-    fc::fc_rowpar_kernel<<<(Bl + 255) / 256, 256, 0, st>>>(a);
+    fc::fc_prep_kernel<<<(B * 32 + 255) / 256, 256, 0, st>>>(E1, E2, a);
     FC_CUDA(cudaGetLastError());
 
     // ---- pass 1: row statistics of S[L,G] (segment R) and S^T[L,G] (segment C) ----
@@ -296,18 +373,17 @@ struct LossStep {
 
     // ---- u table, payload, (all-gather), weights, reductions, tau update ----
     mark(3, st);
-    fc::fc_table_kernel<<<(Bl + 255) / 256, 256, 0, st>>>(a, in->gamma);
+    fc::fc_table_kernel<<<(Bl * 32 + 255) / 256, 256, 0, st>>>(a);
     FC_CUDA(cudaGetLastError());
     if (K > 1) FC_NCCL(ncclAllGather(send, recv, 5 * static_cast<size_t>(Bl), ncclFloat64, comm, st));
-    fc::fc_weights_kernel<<<(B + 255) / 256, 256, 0, st>>>(a, in->eps);
-    fc::fc_reduce_kernel<<<1, 1024, 0, st>>>(a);
+    fc::fc_weights_kernel<<<(B + 255) / 256, 256, 0, st>>>(a);   // + reduction (+ tau step at K = 1)
     FC_CUDA(cudaGetLastError());
     if (K > 1) FC_NCCL(ncclAllReduce(red, red, 2, ncclFloat64, ncclSum, comm, st));
     if (indiv) {
       if (K > 1) FC_NCCL(ncclAllGather(a.gt1, gt_recv, 2 * static_cast<size_t>(Bl), ncclFloat64, comm, st));
       fc::fc_indiv_update_kernel<<<(B + 255) / 256, 256, 0, st>>>(a);
     }
-    fc::fc_finalize_kernel<<<1, 32, 0, st>>>(a);
+    if (K > 1) fc::fc_finalize_kernel<<<1, 32, 0, st>>>(a);
     FC_CUDA(cudaGetLastError());
 
     // ---- pass 2: Q' tiles (bf16) for both segments ----
@@ -315,11 +391,21 @@ struct LossStep {
       fc::SimSeg& g = sp.seg[s];
       g.row_stat = nullptr;
       g.partial = nullptr;
-      g.row_par = (s ? par2 : par1) + rank * Bl;
-      g.col_par = s ? par1 : par2;
+      const int off = rank * Bl;
+      g.row_kappa = (s ? a.kap2 : a.kap1) + off;
+      g.row_beta = (s ? a.bet2 : a.bet1) + off;
+      g.row_coef = (s ? a.coef2 : a.coef1) + off;
+      g.col_kappa = s ? a.kap1 : a.kap2;
+      g.col_beta = s ? a.bet1 : a.bet2;
+      g.col_coef = s ? a.coef1 : a.coef2;
       g.q = q + static_cast<size_t>(s) * Bl * ldq;
     }
     mark(4, st);
+    if (shared_q) {   // K = 1: Q'_C = Q'_R^T -- one Q pass, the dE2 GEMM reads Q^T (MN-major A)
+      sp.nseg = 1;
+      sp.n_rb[1] = 0;
+      sp.n_items = sp.n_rb[0] * n_jt;
+    }
     FC_CUDA(fc::launch_sim(fc::kSimQ, sp, mA, mB, pair_grid(sp.n_items), st, nullptr));
 
     // ---- pass 2b: dE = c (Q' E - r o E_local) ----
@@ -336,6 +422,7 @@ struct LossStep {
     gp.scale = static_cast<float>(1.0 / (static_cast<double>(Bl) * static_cast<double>(B - 1)));
     for (int s = 0; s < 2; ++s) {
       fc::GemmSeg& g = gp.seg[s];
+      g.a_mn_major = (shared_q && s == 1) ? 1 : 0;
       g.rows = Bl;
       g.x_row0 = rank * Bl;
       g.r = rcoef;
@@ -346,15 +433,15 @@ struct LossStep {
     }
     gp.n_items = (gp.n_mb[0] + gp.n_mb[1]) * gp.n_nb * gp.n_split;
     CUtensorMap mX[2] = {mE2n, mE1n};
-    FC_CUDA(fc::launch_gemm(gp, mQ, mX, pair_grid(gp.n_items), st));
+    CUtensorMap mQs[2] = {mQ[0], shared_q ? mQt : mQ[1]};
+    FC_CUDA(fc::launch_gemm(gp, mQs, mX, pair_grid(gp.n_items), st));
     mark(6, st);
 
     FC_CUDA(cudaMemcpyAsync(result_h, result_d, sizeof(fc::StepResult), cudaMemcpyDeviceToHost, st));
-    FC_CUDA(cudaEventRecord(done, st));
   }
 
   int kernels_per_step() const {
-    return 2 /*diag,rowpar*/ + 1 /*pass1*/ + 1 /*table*/ + 2 /*weights,reduce*/ + (indiv ? 1 : 0) + 1 /*finalize*/ +
+    return 1 /*prep*/ + 1 /*pass1*/ + 1 /*table*/ + 1 /*weights+reduce*/ + (indiv ? 1 : 0) + (K > 1 ? 1 : 0) /*finalize*/ +
            1 /*pass2*/ + 1 /*gemm*/;
   }
 
@@ -362,14 +449,19 @@ struct LossStep {
     if (comm) ncclCommDestroy(comm);
     for (void* p : {(void*)u1, (void*)u2, (void*)tau1, (void*)tau2, (void*)m1, (void*)v1, (void*)m2, (void*)v2,
                     (void*)s1, (void*)s2, (void*)tau_state, (void*)e1g, (void*)e2g, (void*)diag, (void*)rowstat,
-                    (void*)partial, (void*)clamps, (void*)f64, (void*)red, (void*)par1, (void*)par2, (void*)rcoef,
+                    (void*)partial, (void*)clamps, (void*)f64, (void*)red, (void*)par, (void*)rcoef, (void*)blockpart, (void*)counter,
                     (void*)q, (void*)err, (void*)result_d, (void*)gt_recv})
       if (p) cudaFree(p);
     if (recv && recv != send) cudaFree(recv);
     if (send) cudaFree(send);
     if (result_h) cudaFreeHost(result_h);
+    for (auto& g : graphs) cudaGraphExecDestroy(g.exec);
+    graphs.clear();
+    if (scal) cudaFree(scal);
+    if (ws) cudaStreamDestroy(ws);
     cudaEventDestroy(done);
-    if (timing)
+    cudaEventDestroy(fork);
+    if (ev_created)
       for (auto& e : ev) cudaEventDestroy(e);
   }
 };
@@ -567,9 +659,11 @@ int fc_set_phase_timing(void* ctx, int32_t on) {
   if (!ctx) return FC_ERR_SHAPE;
   auto* s = static_cast<LossStep*>(ctx);
   return guarded([&] {
-    if (on && !s->timing)
+    if (on && !s->ev_created) {
       for (auto& e : s->ev) FC_CUDA(cudaEventCreate(&e));
-    s->timing = s->timing || on;
+      s->ev_created = true;
+    }
+    s->timing = on != 0;
   });
 }
 
@@ -577,7 +671,7 @@ int fc_phase_times(void* ctx, float* ms, int32_t n) {
   if (!ctx || !ms) return FC_ERR_SHAPE;
   auto* s = static_cast<LossStep*>(ctx);
   return guarded([&] {
-    if (!s->timing) throw FcError{FC_ERR_CONFIG, "phase timing not enabled"};
+    if (!s->ev_created) throw FcError{FC_ERR_CONFIG, "phase timing not enabled"};
     FC_CUDA(cudaEventSynchronize(s->ev[LossStep::kPhases]));
     for (int i = 0; i < n && i < LossStep::kPhases; ++i) FC_CUDA(cudaEventElapsedTime(&ms[i], s->ev[i], s->ev[i + 1]));
   });
@@ -604,6 +698,7 @@ int fc_debug_similarity(const void* a, const void* b, int32_t rows, int32_t cols
     sp.n_items = sp.n_rb[0] * sp.n_jt;
     int dev = 0;
     cudaGetDevice(&dev);
+    FC_CUDA(fc::sim_set_smem());
     const int pairs = std::min(sm_count(dev) / 2, sp.n_items);
     FC_CUDA(fc::launch_sim(fc::kSimRaw, sp, &ma, &mb, std::max(1, pairs) * 2, static_cast<cudaStream_t>(stream), out));
   });

@@ -1,18 +1,19 @@
 // sim_kernel.cu -- fused similarity-tile kernel (FastCLIP pass 1 and pass 2a) for sm_100a.
 //
-// A persistent CTA pair (cluster of 2, tcgen05 cta_group::2) walks (segment, row block,
-// column tile) items. Per item the pair computes one 256 x 256 tile of S' = A B^T (K = d)
-// into TMEM with bf16 UMMA (M = 256 split 128/128 over the pair, N = 256 with each CTA
-// supplying half of B), double-buffered so the epilogue of tile t overlaps the MMAs of t+1.
-// The epilogue never writes S:
+// A persistent CTA pair (cluster of 2, tcgen05 cta_group::2) walks a contiguous range of
+// (segment, row block, column tile) items. Per item the pair computes one 256 x 256 tile of
+// S' = A B^T (K = d) into TMEM with bf16 UMMA (M = 256 split 128/128 over the pair, N = 256
+// with each CTA supplying half of B), double-buffered so the epilogue of tile t overlaps the
+// MMAs of t+1. The anchor rows A stay resident in shared memory across the column tiles of a
+// row block; only the contrast rows B stream (TMA ring). The epilogue never writes S:
 //   STATS: per anchor row i, over the tile's columns j != i,
 //            e = exp(min((s_ij - s_ii)/t_i, 60))    (safe_exp, losses.cpp:22-28)
 //            sum e, sum (s_ij - s_ii) e             (engine.cpp:151-176, :182-204)
-//          -> one float2 partial per (row, column half-tile), reduced in fixed order later.
+//          -> one float2 partial per (row, column quarter-tile), reduced in fixed order later.
 //   Q:     Q'_ij = coef_i e_row(i,j) + coef_j e_col(i,j) (Q[i,j] = P1[i,j] + P2[j,i] of
 //          engine.cpp:91-118) -> bf16 tile of the weight matrix for the gradient GEMM.
-// Warp roles: w0 TMA producer, w1 MMA issuer (leader CTA), w2..w9 epilogue (2 warps per
-// TMEM lane quarter, one per column half).
+// Warp roles: w0 TMA producer, w1 MMA issuer (leader CTA), w2..w17 epilogue (4 warps per
+// TMEM lane quarter, 64 columns each).
 #include "kernels.cuh"
 #include "sm100.cuh"
 
@@ -20,16 +21,20 @@ namespace fc {
 
 namespace {
 
-constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kClampLog2 = 60.0f * 1.4426950408889634f;  // kExpClampMax in the log2 domain
 
 struct SmemLayout {
-  uint8_t* a;   // kStages x 16 KB
-  uint8_t* b;   // kStages x 16 KB
-  uint64_t* full;
+  uint8_t* a;          // kSimASlots x 16 KB: resident anchor rows (one K block per slot)
+  uint8_t* b;          // kSimStages x 16 KB: streamed contrast rows
+  float* par;          // kSimPSlots x {kappa[256], beta[256], coef[256]} (Q pass)
+  uint64_t* full;      // B ring
   uint64_t* empty;
-  uint64_t* tfull;
+  uint64_t* afull;     // A slots
+  uint64_t* aempty;
+  uint64_t* tfull;     // TMEM accumulators
   uint64_t* tempty;
+  uint64_t* pfull;     // column-parameter slots
+  uint64_t* pempty;
   uint32_t* tmem_ptr;
 };
 
@@ -37,13 +42,18 @@ __device__ __forceinline__ SmemLayout carve(uint8_t* base) {
   SmemLayout L;
   uint8_t* p = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(base) + 1023) & ~uintptr_t(1023));
   L.a = p;
-  L.b = p + kStages * kStageBytesA;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(L.b + kStages * kStageBytesB);
+  L.b = p + kSimASlots * kStageBytesA;
+  L.par = reinterpret_cast<float*>(L.b + kSimStages * kStageBytesB);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(L.par) + kSimPSlots * kSimPSlotBytes);
   L.full = bars;
-  L.empty = bars + kStages;
-  L.tfull = bars + 2 * kStages;
-  L.tempty = bars + 2 * kStages + 2;
-  L.tmem_ptr = reinterpret_cast<uint32_t*>(bars + 2 * kStages + 4);
+  L.empty = L.full + kSimStages;
+  L.afull = L.empty + kSimStages;
+  L.aempty = L.afull + kSimASlots;
+  L.tfull = L.aempty + kSimASlots;
+  L.tempty = L.tfull + 2;
+  L.pfull = L.tempty + 2;
+  L.pempty = L.pfull + kSimPSlots;
+  L.tmem_ptr = reinterpret_cast<uint32_t*>(L.pempty + kSimPSlots);
   return L;
 }
 
@@ -55,10 +65,98 @@ __device__ __forceinline__ void decode_item(const SimParams& p, int item, int& s
   jt = local % p.n_jt;
 }
 
+// Contiguous item range of a pair (keeps the resident A block across consecutive items).
+__device__ __forceinline__ void pair_range(int n_items, int pair, int n_pairs, int& lo, int& hi) {
+  lo = static_cast<int>((static_cast<long long>(n_items) * pair) / n_pairs);
+  hi = static_cast<int>((static_cast<long long>(n_items) * (pair + 1)) / n_pairs);
+}
+// Identity of the A block an (item, chunk) needs: segment, row block, 512-wide K chunk.
+__device__ __forceinline__ int a_key(const SimParams& p, int item, int chunk, int n_chunks) {
+  int s, rb, jt;
+  decode_item(p, item, s, rb, jt);
+  return ((s * 65536) + rb) * n_chunks + chunk;
+}
+
+__device__ __forceinline__ void bulk_load(void* smem, const void* gmem, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(smem)),
+      "l"(reinterpret_cast<uint64_t>(gmem)), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// ---- epilogue chunk processors (32 consecutive columns of one row per thread) ----
+// STATS, unmasked: every column valid and off-diagonal (warp-uniform fast path).
+__device__ __forceinline__ void stats_fast(const uint32_t (&r)[32], float d_i, float kap, float& se, float& sxe,
+                                           float& ymax) {
+#pragma unroll
+  for (int k = 0; k < 32; ++k) {
+    const float x = __uint_as_float(r[k]) - d_i;
+    const float y = x * kap;
+    ymax = fmaxf(ymax, y);
+    const float e = ex2_approx(fminf(y, kClampLog2));
+    se += e;
+    sxe = fmaf(x, e, sxe);
+  }
+}
+// STATS, masked: ragged tail / diagonal / rows past the segment.
+__device__ __forceinline__ void stats_masked(const uint32_t (&r)[32], float d_i, float kap, int col0, int cols, int gi,
+                                             bool row_ok, float& se, float& sxe, uint32_t& ncl) {
+#pragma unroll
+  for (int k = 0; k < 32; ++k) {
+    const int j = col0 + k;
+    const float x = __uint_as_float(r[k]) - d_i;
+    const float y = x * kap;
+    const bool ok = row_ok && (j < cols) && (j != gi);
+    const float e = ex2_approx(fminf(y, kClampLog2));
+    se += ok ? e : 0.f;
+    sxe += ok ? x * e : 0.f;
+    ncl += (ok && y > kClampLog2) ? 1u : 0u;
+  }
+}
+__device__ __forceinline__ uint32_t count_clamps(const uint32_t (&r)[32], float d_i, float kap) {
+  uint32_t n = 0;
+#pragma unroll
+  for (int k = 0; k < 32; ++k) n += ((__uint_as_float(r[k]) - d_i) * kap > kClampLog2) ? 1u : 0u;
+  return n;
+}
+
+// Q: 32 bf16 weights of one row; col params from shared memory (broadcast reads).
+template <bool kMasked>
+__device__ __forceinline__ void q_chunk(const uint32_t (&r)[32], float rk, float rb, float rc, const float* kc,
+                                        const float* bc, const float* cc, int col0, int cols, int gi,
+                                        uint32_t (&packed)[16]) {
+#pragma unroll
+  for (int k = 0; k < 32; k += 4) {
+    const float4 kk = *reinterpret_cast<const float4*>(kc + k);
+    const float4 bb = *reinterpret_cast<const float4*>(bc + k);
+    const float4 cf = *reinterpret_cast<const float4*>(cc + k);
+    const float kka[4] = {kk.x, kk.y, kk.z, kk.w};
+    const float bba[4] = {bb.x, bb.y, bb.z, bb.w};
+    const float cfa[4] = {cf.x, cf.y, cf.z, cf.w};
+    float q[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const float s = __uint_as_float(r[k + u]);
+      const float er = ex2_approx(fminf(fmaf(s, rk, rb), kClampLog2));
+      const float ec = ex2_approx(fminf(fmaf(s, kka[u], bba[u]), kClampLog2));
+      float v = fmaf(cfa[u], ec, rc * er);
+      if constexpr (kMasked) {
+        const int j = col0 + k + u;
+        v = (j < cols && j != gi) ? v : 0.f;
+      }
+      q[u] = v;
+    }
+    __nv_bfloat162 h0 = __floats2bfloat162_rn(q[0], q[1]);
+    __nv_bfloat162 h1 = __floats2bfloat162_rn(q[2], q[3]);
+    packed[k / 2] = *reinterpret_cast<uint32_t*>(&h0);
+    packed[k / 2 + 1] = *reinterpret_cast<uint32_t*>(&h1);
+  }
+}
+
 }  // namespace
 
 template <int kMode>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kSimThreads, 1)
     sim_tile_kernel(const __grid_constant__ SimParams p, const __grid_constant__ CUtensorMap mapA0,
                     const __grid_constant__ CUtensorMap mapB0, const __grid_constant__ CUtensorMap mapA1,
                     const __grid_constant__ CUtensorMap mapB1, float* __restrict__ raw_out) {
@@ -80,13 +178,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     }
   }
   if (warp == 1 && lane == 0) {
-    for (int i = 0; i < kStages; ++i) {
+    for (int i = 0; i < kSimStages; ++i) {
       mbar_init(&L.full[i], 2);   // leader's expect_tx arrive + peer's remote arrive
       mbar_init(&L.empty[i], 1);  // MMA commit (multicast to both CTAs)
     }
+    for (int i = 0; i < kSimASlots; ++i) {
+      mbar_init(&L.afull[i], 2);
+      mbar_init(&L.aempty[i], 1);
+    }
     for (int i = 0; i < 2; ++i) {
-      mbar_init(&L.tfull[i], 1);                 // MMA commit (multicast)
-      mbar_init(&L.tempty[i], 2 * kEpiWarps);    // one arrive per epilogue warp of the pair
+      mbar_init(&L.tfull[i], 1);                    // MMA commit (multicast)
+      mbar_init(&L.tempty[i], 2 * kSimEpiWarps);    // one arrive per epilogue warp of the pair
+    }
+    for (int i = 0; i < kSimPSlots; ++i) {
+      mbar_init(&L.pfull[i], 1);                    // local producer + bulk-copy bytes
+      mbar_init(&L.pempty[i], kSimEpiWarps);        // local epilogue warps
     }
     fence_barrier_init();
   }
@@ -96,26 +202,60 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   tc_fence_after();
   const uint32_t tmem_base = *L.tmem_ptr;
 
+  const int n_chunks = (nkb + kSimASlots - 1) / kSimASlots;
+  int it_lo, it_hi;
+  pair_range(p.n_items, pair, n_pairs, it_lo, it_hi);
+
   if (warp == 0) {
     // ===================== TMA producer (both CTAs) =====================
+    // A (anchor rows, own 128 of the pair's 256) is loaded once per (segment, row block,
+    // K chunk) into per-K-block slots; each slot is refilled as soon as the MMAs of the last
+    // tile that read it retire (aempty), so the switch to the next row block overlaps.
     if (elect_one()) {
       uint32_t stage = 0, phase = 0;
-      for (int item = pair; item < p.n_items; item += n_pairs) {
+      uint32_t sgen[kSimASlots] = {};   // per-slot load generation (phase parity of afull/aempty)
+      int cur_key = -1;
+      int it = 0;
+      for (int item = it_lo; item < it_hi; ++item, ++it) {
         int s, rb, jt;
         decode_item(p, item, s, rb, jt);
         const CUtensorMap* ma = s ? &mapA1 : &mapA0;
         const CUtensorMap* mb = s ? &mapB1 : &mapB0;
         const int a_row = p.seg[s].a_row0 + rb * kPairM + static_cast<int>(rank) * kCtaM;
         const int b_row = jt * kPairN + static_cast<int>(rank) * (kPairN / 2);
-        for (int kb = 0; kb < nkb; ++kb) {
-          mbar_wait(&L.empty[stage], phase ^ 1);
-          if (rank == 0)
-            mbar_arrive_expect_tx(&L.full[stage], 2 * (kStageBytesA + kStageBytesB));
-          else
-            mbar_arrive_cluster(&L.full[stage], 0);
-          tma_load_2d_pair(ma, &L.full[stage], L.a + stage * kStageBytesA, kb * kBlockK, a_row);
-          tma_load_2d_pair(mb, &L.full[stage], L.b + stage * kStageBytesB, kb * kBlockK, b_row);
-          if (++stage == kStages) { stage = 0; phase ^= 1; }
+        if constexpr (kMode == kSimQ) {
+          // this tile's column parameters (each CTA keeps its own copy)
+          const int ps = it % kSimPSlots;
+          mbar_wait(&L.pempty[ps], ((it / kSimPSlots) & 1) ^ 1);
+          mbar_arrive_expect_tx(&L.pfull[ps], kSimPSlotBytes);
+          float* dst = L.par + ps * (kSimPSlotBytes / 4);
+          const SimSeg& sg = p.seg[s];
+          bulk_load(dst, sg.col_kappa + jt * kPairN, kPairN * 4, &L.pfull[ps]);
+          bulk_load(dst + kPairN, sg.col_beta + jt * kPairN, kPairN * 4, &L.pfull[ps]);
+          bulk_load(dst + 2 * kPairN, sg.col_coef + jt * kPairN, kPairN * 4, &L.pfull[ps]);
+        }
+        for (int c = 0; c < n_chunks; ++c) {
+          const int kb_lo = c * kSimASlots;
+          const int kb_hi = min(nkb, kb_lo + kSimASlots);
+          const int key = a_key(p, item, c, n_chunks);
+          if (key != cur_key) {
+            for (int kb = kb_lo; kb < kb_hi; ++kb) {
+              const int slot = kb - kb_lo;
+              mbar_wait(&L.aempty[slot], (sgen[slot] & 1) ^ 1);
+              ++sgen[slot];
+              if (rank == 0) mbar_arrive_expect_tx(&L.afull[slot], 2 * kStageBytesA);
+              else mbar_arrive_cluster(&L.afull[slot], 0);
+              tma_load_2d_pair(ma, &L.afull[slot], L.a + slot * kStageBytesA, kb * kBlockK, a_row);
+            }
+            cur_key = key;
+          }
+          for (int kb = kb_lo; kb < kb_hi; ++kb) {
+            mbar_wait(&L.empty[stage], phase ^ 1);
+            if (rank == 0) mbar_arrive_expect_tx(&L.full[stage], 2 * kStageBytesB);
+            else mbar_arrive_cluster(&L.full[stage], 0);
+            tma_load_2d_pair(mb, &L.full[stage], L.b + stage * kStageBytesB, kb * kBlockK, b_row);
+            if (++stage == kSimStages) { stage = 0; phase ^= 1; }
+          }
         }
       }
     }
@@ -124,126 +264,148 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     if (rank == 0) {
       constexpr uint32_t idesc = make_idesc_bf16(kPairM, kPairN, 0, 0);
       uint32_t stage = 0, phase = 0;
+      uint32_t sgen[kSimASlots] = {};
+      int cur_key = -1;
       int it = 0;
-      for (int item = pair; item < p.n_items; item += n_pairs, ++it) {
+      for (int item = it_lo; item < it_hi; ++item, ++it) {
         const uint32_t acc = it & 1;
         const uint32_t acc_phase = (it >> 1) & 1;
         mbar_wait(&L.tempty[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * kPairN;
-        for (int kb = 0; kb < nkb; ++kb) {
-          mbar_wait(&L.full[stage], phase);
-          tc_fence_after();
-          if (elect_one()) {
-            const uint32_t a0 = smem_u32(L.a + stage * kStageBytesA);
-            const uint32_t b0 = smem_u32(L.b + stage * kStageBytesB);
-#pragma unroll
-            for (int k = 0; k < kBlockK / 16; ++k) {
-              const uint64_t ad = make_sdesc_sw128(a0 + k * 32, 0, 1024);
-              const uint64_t bd = make_sdesc_sw128(b0 + k * 32, 0, 1024);
-              mma_bf16_pair(d_tmem, ad, bd, idesc, (kb | k) != 0);
-            }
-            mma_commit_pair(&L.empty[stage], 0x3);
-            if (kb == nkb - 1) mma_commit_pair(&L.tfull[acc], 0x3);
+        for (int c = 0; c < n_chunks; ++c) {
+          const int kb_lo = c * kSimASlots;
+          const int kb_hi = min(nkb, kb_lo + kSimASlots);
+          const int key = a_key(p, item, c, n_chunks);
+          if (key != cur_key) {
+            cur_key = key;
+            for (int kb = kb_lo; kb < kb_hi; ++kb) ++sgen[kb - kb_lo];
           }
-          __syncwarp();
-          if (++stage == kStages) { stage = 0; phase ^= 1; }
+          // last use of this A generation: release each slot right after its MMAs
+          int nxt_key = -2;
+          if (c + 1 < n_chunks) nxt_key = a_key(p, item, c + 1, n_chunks);
+          else if (item + 1 < it_hi) nxt_key = a_key(p, item + 1, 0, n_chunks);
+          const bool last_use = nxt_key != key;
+          for (int kb = kb_lo; kb < kb_hi; ++kb) {
+            const int slot = kb - kb_lo;
+            mbar_wait(&L.afull[slot], (sgen[slot] - 1) & 1);
+            mbar_wait(&L.full[stage], phase);
+            tc_fence_after();
+            if (elect_one()) {
+              const uint32_t a0 = smem_u32(L.a + slot * kStageBytesA);
+              const uint32_t b0 = smem_u32(L.b + stage * kStageBytesB);
+#pragma unroll
+              for (int k = 0; k < kBlockK / 16; ++k) {
+                const uint64_t ad = make_sdesc_sw128(a0 + k * 32, 0, 1024);
+                const uint64_t bd = make_sdesc_sw128(b0 + k * 32, 0, 1024);
+                mma_bf16_pair(d_tmem, ad, bd, idesc, (kb | k) != 0);
+              }
+              mma_commit_pair(&L.empty[stage], 0x3);
+              if (last_use) mma_commit_pair(&L.aempty[slot], 0x3);
+              if (c == n_chunks - 1 && kb == kb_hi - 1) mma_commit_pair(&L.tfull[acc], 0x3);
+            }
+            __syncwarp();
+            if (++stage == kSimStages) { stage = 0; phase ^= 1; }
+          }
         }
       }
     }
   } else {
     // ===================== epilogue (both CTAs) =====================
-    const uint32_t q4 = warp & 3;               // TMEM lane quarter of this warp
-    const uint32_t half = (warp - 2) >> 2;      // column half of the 256-wide tile
-    const int row_in_cta = static_cast<int>(q4 * 32 + lane);
+    const uint32_t q4 = warp & 3;               // TMEM lane quarter accessible to this warp
+    const uint32_t cq = (warp - 2) >> 2;        // 64-column quarter of the 256-wide tile
     int it = 0;
-    for (int item = pair; item < p.n_items; item += n_pairs, ++it) {
+    for (int item = it_lo; item < it_hi; ++item, ++it) {
       int s, rb, jt;
       decode_item(p, item, s, rb, jt);
       const SimSeg& sg = p.seg[s];
       const uint32_t acc = it & 1;
       const uint32_t acc_phase = (it >> 1) & 1;
-      const int r_loc = rb * kPairM + static_cast<int>(rank) * kCtaM + row_in_cta;
+      const int warp_row0 = rb * kPairM + static_cast<int>(rank) * kCtaM + static_cast<int>(q4) * 32;
+      const int r_loc = warp_row0 + static_cast<int>(lane);
       const bool row_ok = r_loc < sg.rows;
-      const int gi = sg.a_row0 + r_loc;
+      const bool warp_rows_ok = warp_row0 + 32 <= sg.rows;
+      const int g0 = sg.a_row0 + warp_row0;     // global index of lane 0's anchor
+      const int gi = g0 + static_cast<int>(lane);
+      const int colq = jt * kPairN + static_cast<int>(cq) * 64;
+
       float2 rstat = make_float2(0.f, 0.f);
-      float4 rpar = make_float4(0.f, 0.f, 0.f, 0.f);
+      float rk = 0.f, rbeta = 0.f, rc = 0.f;
       if (row_ok) {
         if constexpr (kMode == kSimStats) rstat = sg.row_stat[r_loc];
-        if constexpr (kMode == kSimQ) rpar = sg.row_par[r_loc];
+        if constexpr (kMode == kSimQ) {
+          rk = sg.row_kappa[r_loc];
+          rbeta = sg.row_beta[r_loc];
+          rc = sg.row_coef[r_loc];
+        }
       }
-      float sum_e = 0.f, sum_xe = 0.f;
-      uint32_t nclamp = 0;
 
       mbar_wait(&L.tfull[acc], acc_phase);
       tc_fence_after();
-#pragma unroll 1
-      for (int c = 0; c < 4; ++c) {
-        const int col0 = jt * kPairN + static_cast<int>(half) * 128 + c * 32;
-        const uint32_t taddr = tmem_base + ((q4 * 32u) << 16) + acc * kPairN + half * 128u + c * 32u;
-        uint32_t r[32];
-        tmem_ld_32x32b_x32(taddr, r);
-        tmem_ld_wait();
-        if constexpr (kMode == kSimRaw) {
-          if (row_ok) {
-            float* dst = raw_out + static_cast<size_t>(r_loc) * sg.cols;
-#pragma unroll
-            for (int k = 0; k < 32; ++k)
-              if (col0 + k < sg.cols) dst[col0 + k] = __uint_as_float(r[k]);
-          }
-        } else if constexpr (kMode == kSimStats) {
-#pragma unroll
-          for (int k = 0; k < 32; ++k) {
-            const int j = col0 + k;
-            const float x = __uint_as_float(r[k]) - rstat.x;
-            float y = x * rstat.y;
-            const bool clamped = y > kClampLog2;
-            y = fminf(y, kClampLog2);
-            const float e = ex2_approx(y);
-            const bool ok = row_ok && (j < sg.cols) && (j != gi);
-            sum_e += ok ? e : 0.f;
-            sum_xe += ok ? x * e : 0.f;
-            nclamp += (ok && clamped) ? 1u : 0u;
-          }
-        } else {  // kSimQ
-          if (row_ok && col0 < p.ldq) {
-            uint32_t packed[16];
-#pragma unroll
-            for (int k = 0; k < 32; k += 2) {
-              float qv[2];
-#pragma unroll
-              for (int u = 0; u < 2; ++u) {
-                const int j = col0 + k + u;
-                const float sv = __uint_as_float(r[k + u]);
-                const bool ok = (j < sg.cols) && (j != gi);
-                const float4 cp = ok ? __ldg(&sg.col_par[j]) : make_float4(0.f, 0.f, 0.f, 0.f);
-                const float yr = fminf((sv - rpar.x) * rpar.y, kClampLog2);
-                const float yc = fminf((sv - cp.x) * cp.y, kClampLog2);
-                const float v = rpar.z * ex2_approx(yr) + cp.z * ex2_approx(yc);
-                qv[u] = ok ? v : 0.f;
-              }
-              __nv_bfloat162 h2 = __floats2bfloat162_rn(qv[0], qv[1]);
-              packed[k / 2] = *reinterpret_cast<uint32_t*>(&h2);
-            }
-            uint4* dst = reinterpret_cast<uint4*>(sg.q + static_cast<size_t>(r_loc) * p.ldq + col0);
-#pragma unroll
-            for (int v4 = 0; v4 < 4; ++v4)
-              dst[v4] = make_uint4(packed[4 * v4], packed[4 * v4 + 1], packed[4 * v4 + 2], packed[4 * v4 + 3]);
-          }
-        }
-      }
-      // TMEM buffer drained: hand it back to the MMA warp of the leader CTA.
+      uint32_t r0[32], r1[32];
+      const uint32_t taddr = tmem_base + ((q4 * 32u) << 16) + acc * kPairN + cq * 64u;
+      tmem_ld_32x32b_x32(taddr, r0);
+      tmem_ld_32x32b_x32(taddr + 32, r1);
+      tmem_ld_wait();
+      // the tile is in registers: hand the TMEM buffer back to the MMA warp right away
       tc_fence_before();
       __syncwarp();
       if (lane == 0) {
         if (rank == 0) mbar_arrive(&L.tempty[acc]);
         else mbar_arrive_cluster(&L.tempty[acc], 0);
       }
-      if constexpr (kMode == kSimStats) {
-        if (row_ok) sg.partial[static_cast<size_t>(r_loc) * (p.n_jt * 2) + jt * 2 + half] = make_float2(sum_e, sum_xe);
+
+      if constexpr (kMode == kSimRaw) {
+        if (row_ok) {
+          float* dst = raw_out + static_cast<size_t>(r_loc) * sg.cols;
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) nclamp += __shfl_xor_sync(0xffffffffu, nclamp, o);
-        if (lane == 0 && nclamp) atomicAdd(p.clamps, static_cast<unsigned long long>(nclamp));
+          for (int k = 0; k < 32; ++k) {
+            if (colq + k < sg.cols) dst[colq + k] = __uint_as_float(r0[k]);
+            if (colq + 32 + k < sg.cols) dst[colq + 32 + k] = __uint_as_float(r1[k]);
+          }
+        }
+      } else if constexpr (kMode == kSimStats) {
+        float se = 0.f, sxe = 0.f;
+        uint32_t ncl = 0;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const uint32_t(&rr)[32] = h ? r1 : r0;
+          const int col0 = colq + 32 * h;
+          const bool fast = warp_rows_ok && (col0 + 32 <= sg.cols) && !(col0 < g0 + 32 && g0 < col0 + 32);
+          if (fast) {
+            float ym = -INFINITY;
+            stats_fast(rr, rstat.x, rstat.y, se, sxe, ym);
+            if (__any_sync(0xffffffffu, ym > kClampLog2)) ncl += count_clamps(rr, rstat.x, rstat.y);
+          } else {
+            stats_masked(rr, rstat.x, rstat.y, col0, sg.cols, gi, row_ok, se, sxe, ncl);
+          }
+        }
+        if (row_ok) sg.partial[static_cast<size_t>(r_loc) * (p.n_jt * 4) + jt * 4 + cq] = make_float2(se, sxe);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) ncl += __shfl_xor_sync(0xffffffffu, ncl, o);
+        if (lane == 0 && ncl) atomicAdd(p.clamps, static_cast<unsigned long long>(ncl));
+      } else {  // kSimQ
+        const int ps = it % kSimPSlots;
+        mbar_wait(&L.pfull[ps], (it / kSimPSlots) & 1);
+        const float* par = L.par + ps * (kSimPSlotBytes / 4) + cq * 64;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const uint32_t(&rr)[32] = h ? r1 : r0;
+          const int col0 = colq + 32 * h;
+          const bool fast = (col0 + 32 <= sg.cols) && !(col0 < g0 + 32 && g0 < col0 + 32);
+          uint32_t packed[16];
+          const float* kc = par + 32 * h;
+          if (fast) q_chunk<false>(rr, rk, rbeta, rc, kc, kc + kPairN, kc + 2 * kPairN, col0, sg.cols, gi, packed);
+          else q_chunk<true>(rr, rk, rbeta, rc, kc, kc + kPairN, kc + 2 * kPairN, col0, sg.cols, gi, packed);
+          if (row_ok && col0 < p.ldq) {
+            uint4* dst = reinterpret_cast<uint4*>(sg.q + static_cast<size_t>(r_loc) * p.ldq + col0);
+#pragma unroll
+            for (int v4 = 0; v4 < 4; ++v4)
+              dst[v4] = make_uint4(packed[4 * v4], packed[4 * v4 + 1], packed[4 * v4 + 2], packed[4 * v4 + 3]);
+          }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&L.pempty[ps]);
       }
     }
   }
@@ -253,28 +415,28 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   if (warp == 2) tmem_dealloc<2>(tmem_base, 512);
 }
 
+cudaError_t sim_set_smem() {
+  cudaError_t e = cudaFuncSetAttribute(sim_tile_kernel<kSimStats>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSimSmemBytes);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(sim_tile_kernel<kSimQ>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSimSmemBytes);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(sim_tile_kernel<kSimRaw>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSimSmemBytes);
+  return e;
+}
+
 cudaError_t launch_sim(int mode, const SimParams& p, const CUtensorMap* mapA, const CUtensorMap* mapB, int grid,
                        cudaStream_t s, float* raw_out) {
   const CUtensorMap& a1 = p.nseg > 1 ? mapA[1] : mapA[0];
   const CUtensorMap& b1 = p.nseg > 1 ? mapB[1] : mapB[0];
   if (grid < 2) grid = 2;
   grid &= ~1;
-  cudaError_t e;
   switch (mode) {
     case kSimStats:
-      e = cudaFuncSetAttribute(sim_tile_kernel<kSimStats>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
-      if (e != cudaSuccess) return e;
-      sim_tile_kernel<kSimStats><<<grid, kThreads, kSmemBytes, s>>>(p, mapA[0], mapB[0], a1, b1, raw_out);
+      sim_tile_kernel<kSimStats><<<grid, kSimThreads, kSimSmemBytes, s>>>(p, mapA[0], mapB[0], a1, b1, raw_out);
       break;
     case kSimQ:
-      e = cudaFuncSetAttribute(sim_tile_kernel<kSimQ>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
-      if (e != cudaSuccess) return e;
-      sim_tile_kernel<kSimQ><<<grid, kThreads, kSmemBytes, s>>>(p, mapA[0], mapB[0], a1, b1, raw_out);
+      sim_tile_kernel<kSimQ><<<grid, kSimThreads, kSimSmemBytes, s>>>(p, mapA[0], mapB[0], a1, b1, raw_out);
       break;
     default:
-      e = cudaFuncSetAttribute(sim_tile_kernel<kSimRaw>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
-      if (e != cudaSuccess) return e;
-      sim_tile_kernel<kSimRaw><<<grid, kThreads, kSmemBytes, s>>>(p, mapA[0], mapB[0], a1, b1, raw_out);
+      sim_tile_kernel<kSimRaw><<<grid, kSimThreads, kSimSmemBytes, s>>>(p, mapA[0], mapB[0], a1, b1, raw_out);
       break;
   }
   return cudaGetLastError();

@@ -26,17 +26,21 @@ namespace {
 constexpr double kLog2eD = 1.4426950408889634073599;
 }
 
-__global__ void fc_diag_kernel(const __nv_bfloat16* __restrict__ e1, const __nv_bfloat16* __restrict__ e2,
-                               int B, int d, float* __restrict__ diag) {
-  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) / 32;
+// Warp per global anchor w: S_ww = <E1_w, E2_w> (fp32 from bf16); the warps of this rank's
+// anchors also snapshot tau^t (global tau, or IndividualTemp by id, state.cpp:112-122) and
+// emit the pass-1 row parameters.
+__global__ void fc_prep_kernel(const __nv_bfloat16* __restrict__ e1, const __nv_bfloat16* __restrict__ e2,
+                               StepArgs a) {
+  const int w = (blockIdx.x * blockDim.x + threadIdx.x) / 32;
   const int lane = threadIdx.x & 31;
-  if (warp >= B) return;
-  const uint4* a = reinterpret_cast<const uint4*>(e1 + static_cast<size_t>(warp) * d);
-  const uint4* b = reinterpret_cast<const uint4*>(e2 + static_cast<size_t>(warp) * d);
+  if (w == 0 && lane == 0) *a.clamps = 0ull;
+  if (w >= a.B) return;
+  const uint4* x4 = reinterpret_cast<const uint4*>(e1 + static_cast<size_t>(w) * a.d);
+  const uint4* y4 = reinterpret_cast<const uint4*>(e2 + static_cast<size_t>(w) * a.d);
   float acc = 0.f;
-  for (int v = lane; v < d / 8; v += 32) {
-    const uint4 x = __ldg(a + v);
-    const uint4 y = __ldg(b + v);
+  for (int v = lane; v < a.d / 8; v += 32) {
+    const uint4 x = __ldg(x4 + v);
+    const uint4 y = __ldg(y4 + v);
     const uint32_t xs[4] = {x.x, x.y, x.z, x.w};
     const uint32_t ys[4] = {y.x, y.y, y.z, y.w};
 #pragma unroll
@@ -49,13 +53,10 @@ __global__ void fc_diag_kernel(const __nv_bfloat16* __restrict__ e1, const __nv_
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-  if (lane == 0) diag[warp] = acc;
-}
-
-__global__ void fc_rowpar_kernel(StepArgs a) {
-  const int r = blockIdx.x * blockDim.x + threadIdx.x;
-  if (r == 0) *a.clamps = 0ull;
-  if (r >= a.Bl) return;
+  if (lane != 0) return;
+  a.diag[w] = acc;
+  const int r = w - a.row0;
+  if (r < 0 || r >= a.Bl) return;
   double t1, t2;
   if (a.individual) {
     const int id = a.ids[r];
@@ -66,24 +67,36 @@ __global__ void fc_rowpar_kernel(StepArgs a) {
   }
   a.t_loc1[r] = t1;
   a.t_loc2[r] = t2;
-  const float s_ii = a.diag[a.row0 + r];
-  a.rowstat_R[r] = make_float2(s_ii, static_cast<float>(kLog2eD / t1));
-  a.rowstat_C[r] = make_float2(s_ii, static_cast<float>(kLog2eD / t2));
+  a.rowstat_R[r] = make_float2(acc, static_cast<float>(kLog2eD / t1));
+  a.rowstat_C[r] = make_float2(acc, static_cast<float>(kLog2eD / t2));
 }
 
-__global__ void fc_table_kernel(StepArgs a, double gamma) {
-  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+// Warp per local anchor: fixed-order (lane-strided + xor tree) reduction of the pass-1
+// partials, then g (engine.cpp:151-176), the fp64 EMA of the owned u entries (state.cpp:52-53)
+// and the snapshot (state.cpp:57-71), written straight into the all-gather payload.
+__global__ void fc_table_kernel(StepArgs a) {
+  const double gamma = a.scal[0];   // gamma_t of this step (device, so the step can be graph-replayed)
+  const int r = (blockIdx.x * blockDim.x + threadIdx.x) / 32;
+  const int lane = threadIdx.x & 31;
   if (r >= a.Bl) return;
-  const int nparts = a.n_jt * 2;
+  const int nparts = a.n_jt * 4;
   const float2* pr = a.partial_R + static_cast<size_t>(r) * nparts;
   const float2* pc = a.partial_C + static_cast<size_t>(r) * nparts;
   double s1 = 0.0, x1 = 0.0, s2 = 0.0, x2 = 0.0;
-  for (int q = 0; q < nparts; ++q) {  // fixed order: deterministic
+  for (int q = lane; q < nparts; q += 32) {
     const float2 u = pr[q];
     const float2 v = pc[q];
     s1 += u.x; x1 += u.y;
     s2 += v.x; x2 += v.y;
   }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+    x1 += __shfl_xor_sync(0xffffffffu, x1, o);
+    s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+    x2 += __shfl_xor_sync(0xffffffffu, x2, o);
+  }
+  if (lane != 0) return;
   a.sum1[r] = s1; a.dx1[r] = x1;
   a.sum2[r] = s2; a.dx2[r] = x2;
   const double inv = 1.0 / static_cast<double>(a.B - 1);
@@ -110,9 +123,21 @@ __global__ void fc_table_kernel(StepArgs a, double gamma) {
   snd[4 * a.Bl + r] = static_cast<double>(id);
 }
 
-__global__ void fc_weights_kernel(StepArgs a, double eps) {
+__device__ void block_reduce_and_finish(const StepArgs& a, double ta, double tb, double tl);
+__device__ __forceinline__ void weights_one(const StepArgs& a, int i, double eps, double& ta, double& tb,
+                                            double& tl);
+
+__global__ void fc_weights_kernel(StepArgs a) {
+  const double eps = a.scal[1];     // eps_t of this step
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= a.B) return;
+  double ta = 0.0, tb = 0.0, tl = 0.0;
+  // every thread reaches the block reduction from the same place (warp-synchronous shuffles)
+  if (i < a.B) weights_one(a, i, eps, ta, tb, tl);
+  block_reduce_and_finish(a, ta, tb, tl);
+}
+
+__device__ __forceinline__ void weights_one(const StepArgs& a, int i, double eps, double& ta, double& tb,
+                                            double& tl) {
   const int k = i / a.Bl;
   const int r = i % a.Bl;
   const double* blk = a.recv + static_cast<size_t>(k) * 5 * a.Bl;
@@ -137,69 +162,38 @@ __global__ void fc_weights_kernel(StepArgs a, double eps) {
   const double c1 = w1 / t1;   // P1 coefficient: w1_a / t1_a  (engine.cpp:104,118)
   const double c2 = w2 / t2;   // P2 coefficient: w2_a / t2_a
   const float s_ii = a.diag[i];
-  a.par1[i] = make_float4(s_ii, static_cast<float>(kLog2eD / t1), static_cast<float>(c1), 0.f);
-  a.par2[i] = make_float4(s_ii, static_cast<float>(kLog2eD / t2), static_cast<float>(c2), 0.f);
+  const float k1 = static_cast<float>(kLog2eD / t1);
+  const float k2 = static_cast<float>(kLog2eD / t2);
+  a.kap1[i] = k1; a.bet1[i] = -s_ii * k1; a.coef1[i] = static_cast<float>(c1);
+  a.kap2[i] = k2; a.bet2[i] = -s_ii * k2; a.coef2[i] = static_cast<float>(c2);
 
-  if (k != a.rank) return;
-  // ---- local anchor: r_i, tau-gradient terms, loss term ----
-  a.rcoef[r] = static_cast<float>(c1 * a.sum1[r] + c2 * a.sum2[r]);
-  const double inv = 1.0 / static_cast<double>(a.B - 1);
-  const double ds1 = (-(a.dx1[r] / (t1 * t1))) * inv;   // engine.cpp:198-205
-  const double ds2 = (-(a.dx2[r] / (t2 * t2))) * inv;
-  const double g1 = a.g1[r], g2 = a.g2[r];
-  if (a.variant == 0) {
-    const double c = inv;
-    a.term_a[r] = ds1 / (c + g1) + ds2 / (c + g2);          // grad_tau_mbcl (engine.cpp:261-266)
-    a.term_b[r] = 0.0;
-    a.term_loss[r] = log(c + g1) + log(c + g2);             // eval_mbcl (losses.cpp:168-180)
-  } else if (a.individual) {
-    const double inv_n = 1.0 / static_cast<double>(a.n_train);   // engine.cpp:240-259
-    a.gt1[r] = inv_n * (log(eps + u1) + a.rho + t1 * ds1 / (eps + u1));
-    a.gt2[r] = inv_n * (log(eps + u2) + a.rho + t2 * ds2 / (eps + u2));
-    a.term_a[r] = 0.0;
-    a.term_b[r] = 0.0;
-    a.term_loss[r] = t1 * (log(eps + g1) + a.rho) + t2 * (log(eps + g2) + a.rho);  // eval_rgcl
-  } else {
-    a.term_a[r] = ds1 / (eps + u1) + ds2 / (eps + u2);        // grad_tau_unscaled (engine.cpp:208-224)
-    a.term_b[r] = log(eps + u1) + log(eps + u2);              // grad_tau_margin logs (engine.cpp:226-238)
-    a.term_loss[r] = log(eps + g1) + log(eps + g2);           // eval_gcl (losses.cpp:126-138)
-  }
-}
-
-// One block; fixed-order strided accumulation + fixed tree => deterministic sums.
-__global__ void fc_reduce_kernel(StepArgs a) {
-  __shared__ double sh[3][1024];
-  double s0 = 0.0, s1 = 0.0, s2 = 0.0;
-  for (int r = threadIdx.x; r < a.Bl; r += blockDim.x) {
-    s0 += a.term_a[r];
-    s1 += a.term_b[r];
-    s2 += a.term_loss[r];
-  }
-  sh[0][threadIdx.x] = s0;
-  sh[1][threadIdx.x] = s1;
-  sh[2][threadIdx.x] = s2;
-  __syncthreads();
-  for (int w = blockDim.x / 2; w > 0; w >>= 1) {
-    if (threadIdx.x < w) {
-      sh[0][threadIdx.x] += sh[0][threadIdx.x + w];
-      sh[1][threadIdx.x] += sh[1][threadIdx.x + w];
-      sh[2][threadIdx.x] += sh[2][threadIdx.x + w];
+  if (k == a.rank) {
+    // ---- local anchor: r_i, tau-gradient terms, loss term ----
+    a.rcoef[r] = static_cast<float>(c1 * a.sum1[r] + c2 * a.sum2[r]);
+    const double inv = 1.0 / static_cast<double>(a.B - 1);
+    const double ds1 = (-(a.dx1[r] / (t1 * t1))) * inv;   // engine.cpp:198-205
+    const double ds2 = (-(a.dx2[r] / (t2 * t2))) * inv;
+    const double g1 = a.g1[r], g2 = a.g2[r];
+    if (a.variant == 0) {
+      const double c = inv;
+      ta = ds1 / (c + g1) + ds2 / (c + g2);                 // grad_tau_mbcl (engine.cpp:261-266)
+      tl = log(c + g1) + log(c + g2);                       // eval_mbcl (losses.cpp:168-180)
+    } else if (a.individual) {
+      const double inv_n = 1.0 / static_cast<double>(a.n_train);   // engine.cpp:240-259
+      a.gt1[r] = inv_n * (log(eps + u1) + a.rho + t1 * ds1 / (eps + u1));
+      a.gt2[r] = inv_n * (log(eps + u2) + a.rho + t2 * ds2 / (eps + u2));
+      tl = t1 * (log(eps + g1) + a.rho) + t2 * (log(eps + g2) + a.rho);  // eval_rgcl
+    } else {
+      ta = ds1 / (eps + u1) + ds2 / (eps + u2);             // grad_tau_unscaled (engine.cpp:208-224)
+      tb = log(eps + u1) + log(eps + u2);                   // grad_tau_margin logs (engine.cpp:226-238)
+      tl = log(eps + g1) + log(eps + g2);                   // eval_gcl (losses.cpp:126-138)
     }
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) {
-    const double bl = static_cast<double>(a.Bl);
-    const double unscaled = sh[0][0] / bl;
-    double gtl = unscaled;                                   // v0 / MBCL
-    if (a.variant == 6) gtl = sh[1][0] / bl + 2.0 * a.rho + a.tau_state->tau * unscaled;  // v3
-    a.red[0] = gtl;        // all-reduced (sum) across ranks, then * 1/K (fabric.cpp:73-83)
-    a.red[1] = sh[2][0];   // loss numerator, summed across ranks
   }
 }
+
 
 // trainer.cpp:557-577 for the global-temperature schemes + step scalars for every variant.
-__global__ void fc_finalize_kernel(StepArgs a) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+__device__ void finalize_step(const StepArgs& a) {
   TauState* ts = a.tau_state;
   const double tau_t = ts->tau;
   const double nB = static_cast<double>(a.B);
@@ -237,6 +231,53 @@ __global__ void fc_finalize_kernel(StepArgs a) {
   res->tau = ts->tau;
   res->latched = ts->latched;
   res->err = *a.err;
+}
+
+// Deterministic two-level reduction of the local tau-gradient / loss terms: fixed warp
+// trees into per-block partials, then the LAST block to finish (threadfence + ticket) sums
+// the partials in block order, forms G_tau,k (engine.cpp:208-238) and, when no all-reduce
+// separates them (K = 1), runs the temperature step.
+__device__ void block_reduce_and_finish(const StepArgs& a, double ta, double tb, double tl) {
+  __shared__ double sh[3][32];
+  __shared__ bool last;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    ta += __shfl_xor_sync(0xffffffffu, ta, o);
+    tb += __shfl_xor_sync(0xffffffffu, tb, o);
+    tl += __shfl_xor_sync(0xffffffffu, tl, o);
+  }
+  if (lane == 0) { sh[0][wid] = ta; sh[1][wid] = tb; sh[2][wid] = tl; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double b0 = 0.0, b1 = 0.0, b2 = 0.0;
+    for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) { b0 += sh[0][w]; b1 += sh[1][w]; b2 += sh[2][w]; }
+    double* bp = a.blockpart + 3 * blockIdx.x;
+    bp[0] = b0; bp[1] = b1; bp[2] = b2;
+    __threadfence();
+    const unsigned ticket = atomicAdd(a.counter, 1u);
+    last = ticket == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!last || threadIdx.x != 0) return;
+  __threadfence();
+  double s0 = 0.0, s1 = 0.0, s2 = 0.0;
+  for (unsigned b = 0; b < gridDim.x; ++b) {
+    const volatile double* bp = a.blockpart + 3 * b;
+    s0 += bp[0]; s1 += bp[1]; s2 += bp[2];
+  }
+  *a.counter = 0u;   // re-arm for the next step
+  const double bl = static_cast<double>(a.Bl);
+  const double unscaled = s0 / bl;
+  double gtl = unscaled;                                                   // v0 / MBCL
+  if (a.variant == 6) gtl = s1 / bl + 2.0 * a.rho + a.tau_state->tau * unscaled;  // v3
+  a.red[0] = gtl;   // all-reduced (sum) across ranks, then * 1/K (fabric.cpp:73-83)
+  a.red[1] = s2;    // loss numerator, summed across ranks
+  if (a.fuse_finalize) finalize_step(a);
+}
+
+__global__ void fc_finalize_kernel(StepArgs a) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) finalize_step(a);
 }
 
 // v2 / iSogCLR: IndividualTemp::update for every id of the global batch (state.cpp:124-131);

@@ -34,7 +34,8 @@ struct StepArgs {
   double rho, tau_lr, tau0, beta1, beta2, adam_eps, lr_decay_threshold, lr_decay_factor;
   // inputs
   const int32_t* ids;          // [Bl]
-  const float* diag;           // [B]
+  const double* scal;          // [2] step scalars {gamma_t, eps_t}
+  float* diag;                 // [B]
   // dataset-sized tables (fp64 SoA)
   double* u1_tab; double* u2_tab;
   double* tau1_tab; double* tau2_tab;
@@ -55,19 +56,22 @@ struct StepArgs {
   const double* recv;                    // [K][5][Bl] (== send when K == 1)
   const double* gt_recv;                 // [K][2][Bl] (== gt1 when K == 1)
   // pass-2 parameters
-  float4* par1; float4* par2;            // [B]
+  // per-anchor exponent parameters y = s*kappa + beta and weights coef (SoA, [n_jt*256])
+  float* kap1; float* bet1; float* coef1;   // track 1: kappa = log2e/t1, coef = w1/t1
+  float* kap2; float* bet2; float* coef2;   // track 2: kappa = log2e/t2, coef = w2/t2
   float* rcoef;                          // [Bl]
   double* red;                           // [2] local G_tau, loss numerator (all-reduced)
+  double* blockpart;                     // [grid][3] per-block partial sums (weights kernel)
+  unsigned* counter;                     // last-block ticket
+  int fuse_finalize;                     // K == 1: temperature step in the weights kernel
   int* err;
   StepResult* result;
 };
 
-__global__ void fc_diag_kernel(const __nv_bfloat16* __restrict__ e1, const __nv_bfloat16* __restrict__ e2,
-                               int B, int d, float* __restrict__ diag);
-__global__ void fc_rowpar_kernel(StepArgs a);
-__global__ void fc_table_kernel(StepArgs a, double gamma);
-__global__ void fc_weights_kernel(StepArgs a, double eps);
-__global__ void fc_reduce_kernel(StepArgs a);
+__global__ void fc_prep_kernel(const __nv_bfloat16* __restrict__ e1, const __nv_bfloat16* __restrict__ e2,
+                               StepArgs a);
+__global__ void fc_table_kernel(StepArgs a);
+__global__ void fc_weights_kernel(StepArgs a);
 __global__ void fc_finalize_kernel(StepArgs a);
 __global__ void fc_indiv_update_kernel(StepArgs a);
 

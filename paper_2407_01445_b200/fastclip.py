@@ -210,6 +210,9 @@ class LossStep:
     def enable_phase_timing(self):
         _check(lib().fc_set_phase_timing(self._h, 1))
 
+    def disable_phase_timing(self):
+        _check(lib().fc_set_phase_timing(self._h, 0))
+
     def phase_times(self) -> dict:
         ms = (C.c_float * len(PHASES))()
         _check(lib().fc_phase_times(self._h, ms, len(PHASES)))
