@@ -29,7 +29,9 @@ constexpr int kSimSmemBytes =
     kSimASlots * kStageBytesA + kSimStages * kStageBytesB + kSimPSlots * kSimPSlotBytes + 1024 + 512;
 // gradient GEMM: A (Q') and B (E) both stream.
 constexpr int kStages = 6;
-constexpr int kSmemBytes = kStages * (kStageBytesA + kStageBytesB) + 1024 /*align*/ + 256 /*barriers*/;
+constexpr int kGemmStageOut = 32 * 32 * 4;   // per epilogue warp: 32 rows x 32 fp32 (128-byte swizzled rows)
+constexpr int kSmemBytes = kStages * (kStageBytesA + kStageBytesB) + kEpiWarps * kGemmStageOut + 1024 /*align*/ +
+                           256 /*barriers*/;
 
 // ---- similarity-tile kernel (pass 1: row statistics; pass 2: Q tiles) ----
 // One "segment" is an S block S' = A B^T with A = E_rows[a_row0 .. a_row0+rows) and
@@ -55,6 +57,7 @@ struct SimParams {
   int n_rb[2];
   int n_items;
   unsigned long long* clamps;  // STATS: exponent clamps (safe_exp, losses.cpp:22-28)
+  int debug;                   // perf experiments: 1 = skip epilogue math, 2 = also skip B loads
 };
 
 // ---- weighted-gradient GEMM: out = scale * (Q' X - r o X_local) ----
@@ -72,11 +75,10 @@ struct GemmParams {
   int d;
   int n_mb[2];
   int n_nb;
-  int n_split;
+  int n_tiles;       // sum over segments of n_mb * n_nb
   int kb_total;      // K blocks of 64 over ldq
-  int kb_per_split;
-  int n_items;
   float scale;       // 1 / (Bl (B-1)), engine.cpp:84-85
+  int debug;         // perf experiments: 1 = skip epilogue stores, 2 = also skip loads after the first stage
 };
 
 enum SimMode { kSimStats = 0, kSimQ = 1, kSimRaw = 2 };
@@ -85,7 +87,7 @@ cudaError_t launch_sim(int mode, const SimParams& p, const CUtensorMap* mapA, co
                        int grid, cudaStream_t s, float* raw_out);
 cudaError_t sim_set_smem();
 cudaError_t gemm_set_smem();
-cudaError_t launch_gemm(const GemmParams& p, const CUtensorMap* mapQ, const CUtensorMap* mapX, int grid,
-                        cudaStream_t s);
+cudaError_t launch_gemm(const GemmParams& p, const CUtensorMap* mapQ, const CUtensorMap* mapX,
+                        const CUtensorMap* mapOut, int grid, cudaStream_t s);
 
 }  // namespace fc

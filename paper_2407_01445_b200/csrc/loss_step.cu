@@ -62,15 +62,15 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   return fn;
 }
 
-// bf16 2D map over a row-major [outer x inner] array with a 128-byte swizzled box.
+// 2D map over a row-major [outer x inner] array with a 128-byte swizzled box (bf16 or fp32).
 CUtensorMap make_map(const void* base, uint64_t inner, uint64_t outer, uint64_t row_bytes, uint32_t box_inner,
-                     uint32_t box_outer) {
+                     uint32_t box_outer, CUtensorMapDataType dt = CU_TENSOR_MAP_DATA_TYPE_BFLOAT16) {
   CUtensorMap m;
   cuuint64_t dims[2] = {inner, outer};
   cuuint64_t strides[1] = {row_bytes};
   cuuint32_t box[2] = {box_inner, box_outer};
   cuuint32_t es[2] = {1, 1};
-  CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, es,
+  CUresult r = encode_fn()(&m, dt, 2, const_cast<void*>(base), dims, strides, box, es,
                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) throw FcError{FC_ERR_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string(r) + ")"};
@@ -122,6 +122,7 @@ struct LossStep {
   double* scal = nullptr;        // device {gamma_t, eps_t}
   bool use_graph = true;
   bool shared_q = true;          // K == 1: one Q pass, Q^T read by the dE2 GEMM
+  int sim_debug = 0, gemm_debug = 0;             // FC_SIM_DEBUG perf experiments (results invalid when set)
   struct GraphEntry {
     const void* key[5];
     cudaGraphExec_t exec;
@@ -142,8 +143,10 @@ struct LossStep {
   // cached descriptors
   const void* map_e1 = nullptr;
   const void* map_e2 = nullptr;
+  const void* map_o1 = nullptr;
+  const void* map_o2 = nullptr;
+  CUtensorMap mO[2];
   CUtensorMap mE1k, mE2k, mE1n, mE2n, mQ[2], mQt;
-  int n_split = 4;
   fc::StepArgs args{};
 
   double* F(int i) const { return f64 + static_cast<size_t>(i) * Bl; }
@@ -169,7 +172,6 @@ struct LossStep {
     n_jt = (B + fc::kPairN - 1) / fc::kPairN;
     FC_CUDA(cudaSetDevice(cfg.device));
     n_sm = sm_count(cfg.device);
-    if (const char* e = std::getenv("FC_GEMM_SPLIT")) n_split = std::max(1, atoi(e));
 
     const size_t N = static_cast<size_t>(cfg.n_train);
     u1 = dalloc<double>(N);
@@ -226,6 +228,8 @@ struct LossStep {
     if (const char* e = std::getenv("FC_GRAPH")) use_graph = atoi(e) != 0;
     shared_q = K == 1;
     if (const char* e = std::getenv("FC_DEBUG_SYNC")) debug_sync = atoi(e) != 0;
+    if (const char* e = std::getenv("FC_SIM_DEBUG")) sim_debug = atoi(e);
+    if (const char* e = std::getenv("FC_GEMM_DEBUG")) gemm_debug = atoi(e);
     if (debug_sync) use_graph = false;
     if (const char* e = std::getenv("FC_SHARED_Q")) shared_q = shared_q && atoi(e) != 0;
     FC_CUDA(fc::sim_set_smem());
@@ -367,6 +371,7 @@ struct LossStep {
     }
     sp.n_items = (sp.n_rb[0] + sp.n_rb[1]) * n_jt;
     sp.clamps = clamps;
+    sp.debug = sim_debug;
     CUtensorMap mA[2] = {mE1k, mE2k}, mB[2] = {mE2k, mE1k};
     mark(2, st);
     FC_CUDA(fc::launch_sim(fc::kSimStats, sp, mA, mB, pair_grid(sp.n_items), st, nullptr));
@@ -415,11 +420,8 @@ struct LossStep {
     gp.d = d;
     gp.n_nb = (d + fc::kPairN - 1) / fc::kPairN;
     gp.kb_total = ldq / fc::kBlockK;
-    int split = std::max(1, std::min(n_split, gp.kb_total));
-    gp.kb_per_split = (gp.kb_total + split - 1) / split;
-    split = (gp.kb_total + gp.kb_per_split - 1) / gp.kb_per_split;
-    gp.n_split = split;
     gp.scale = static_cast<float>(1.0 / (static_cast<double>(Bl) * static_cast<double>(B - 1)));
+    gp.debug = gemm_debug;
     for (int s = 0; s < 2; ++s) {
       fc::GemmSeg& g = gp.seg[s];
       g.a_mn_major = (shared_q && s == 1) ? 1 : 0;
@@ -429,12 +431,34 @@ struct LossStep {
       g.x = s ? E1 : E2;
       g.out = s ? out->de2 : out->de1;
       gp.n_mb[s] = (Bl + fc::kPairM - 1) / fc::kPairM;
-      if (split > 1) FC_CUDA(cudaMemsetAsync(g.out, 0, static_cast<size_t>(Bl) * d * 4, st));
     }
-    gp.n_items = (gp.n_mb[0] + gp.n_mb[1]) * gp.n_nb * gp.n_split;
+    gp.n_tiles = (gp.n_mb[0] + gp.n_mb[1]) * gp.n_nb;
+    const int gemm_pairs = n_sm / 2;
+    {
+      // tiles past the data-parallel rounds are split over all pairs and reduced with
+      // atomics: zero their row blocks first (they form the tail in (segment, row block) order)
+      const int dp = (gp.n_tiles / gemm_pairs) * gemm_pairs;
+      if (dp < gp.n_tiles) {
+        const int per0 = gp.n_mb[0] * gp.n_nb;
+        const int s0 = dp < per0 ? 0 : 1;
+        const int mb0 = (dp - (s0 ? per0 : 0)) / gp.n_nb;
+        for (int s = s0; s < 2; ++s) {
+          const size_t r0 = s == s0 ? static_cast<size_t>(mb0) * fc::kPairM : 0;
+          if (r0 < static_cast<size_t>(Bl))
+            FC_CUDA(cudaMemsetAsync(gp.seg[s].out + r0 * d, 0, (Bl - r0) * d * 4, st));
+        }
+      }
+    }
     CUtensorMap mX[2] = {mE2n, mE1n};
     CUtensorMap mQs[2] = {mQ[0], shared_q ? mQt : mQ[1]};
-    FC_CUDA(fc::launch_gemm(gp, mQs, mX, pair_grid(gp.n_items), st));
+    if (out->de1 != map_o1 || out->de2 != map_o2) {
+      const uint64_t rb = static_cast<uint64_t>(d) * 4;
+      mO[0] = make_map(out->de1, d, Bl, rb, 32, 32, CU_TENSOR_MAP_DATA_TYPE_FLOAT32);
+      mO[1] = make_map(out->de2, d, Bl, rb, 32, 32, CU_TENSOR_MAP_DATA_TYPE_FLOAT32);
+      map_o1 = out->de1;
+      map_o2 = out->de2;
+    }
+    FC_CUDA(fc::launch_gemm(gp, mQs, mX, mO, gemm_pairs * 2, st));
     mark(6, st);
 
     FC_CUDA(cudaMemcpyAsync(result_h, result_d, sizeof(fc::StepResult), cudaMemcpyDeviceToHost, st));

@@ -251,6 +251,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kSimThreads, 1)
           }
           for (int kb = kb_lo; kb < kb_hi; ++kb) {
             mbar_wait(&L.empty[stage], phase ^ 1);
+            if (p.debug == 2 && item != it_lo) {   // perf experiment: no B traffic after the first tile
+              if (rank == 0) mbar_arrive(&L.full[stage]);
+              else mbar_arrive_cluster(&L.full[stage], 0);
+              if (++stage == kSimStages) { stage = 0; phase ^= 1; }
+              continue;
+            }
             if (rank == 0) mbar_arrive_expect_tx(&L.full[stage], 2 * kStageBytesB);
             else mbar_arrive_cluster(&L.full[stage], 0);
             tma_load_2d_pair(mb, &L.full[stage], L.b + stage * kStageBytesB, kb * kBlockK, b_row);
@@ -288,9 +294,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kSimThreads, 1)
           const bool last_use = nxt_key != key;
           for (int kb = kb_lo; kb < kb_hi; ++kb) {
             const int slot = kb - kb_lo;
-            mbar_wait(&L.afull[slot], (sgen[slot] - 1) & 1);
+            if (p.debug < 4 || it == 0) mbar_wait(&L.afull[slot], (sgen[slot] - 1) & 1);
             mbar_wait(&L.full[stage], phase);
-            tc_fence_after();
+            if (p.debug < 4) tc_fence_after();
             if (elect_one()) {
               const uint32_t a0 = smem_u32(L.a + slot * kStageBytesA);
               const uint32_t b0 = smem_u32(L.b + stage * kStageBytesB);
@@ -344,9 +350,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kSimThreads, 1)
       tc_fence_after();
       uint32_t r0[32], r1[32];
       const uint32_t taddr = tmem_base + ((q4 * 32u) << 16) + acc * kPairN + cq * 64u;
-      tmem_ld_32x32b_x32(taddr, r0);
-      tmem_ld_32x32b_x32(taddr + 32, r1);
-      tmem_ld_wait();
+      if (p.debug >= 3) {
+#pragma unroll
+        for (int k = 0; k < 32; ++k) { r0[k] = 0; r1[k] = 0; }
+      } else {
+        tmem_ld_32x32b_x32(taddr, r0);
+        tmem_ld_32x32b_x32(taddr + 32, r1);
+        tmem_ld_wait();
+      }
       // the tile is in registers: hand the TMEM buffer back to the MMA warp right away
       tc_fence_before();
       __syncwarp();
@@ -355,7 +366,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kSimThreads, 1)
         else mbar_arrive_cluster(&L.tempty[acc], 0);
       }
 
-      if constexpr (kMode == kSimRaw) {
+      if (p.debug) {
+        if constexpr (kMode == kSimQ) {
+          const int ps = it % kSimPSlots;
+          mbar_wait(&L.pfull[ps], (it / kSimPSlots) & 1);
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&L.pempty[ps]);
+        }
+        if (r0[3] == 0x7fffffffu && r1[5] == 0x7fffffffu) sg.partial[0] = make_float2(0.f, 0.f);  // keep loads live
+      } else if constexpr (kMode == kSimRaw) {
         if (row_ok) {
           float* dst = raw_out + static_cast<size_t>(r_loc) * sg.cols;
 #pragma unroll

@@ -1,4 +1,4 @@
 mkdir -p gpurun_out
 timeout -s KILL 400 python -m pytest tests -m gpu -q --timeout 120 2>&1 | tail -4
-timeout -s KILL 300 python bench.py --steps 20 --warmup 5 --no-cpu-baseline > gpurun_out/bench4.json 2> gpurun_out/bench4.err; echo "rc=$?"
-tail -2 gpurun_out/bench4.err; python -c "import json; d=json.load(open('gpurun_out/bench4.json')); print(d['ms_per_step'], d['value'], d['step_roofline']['frac'], d['e2e']['value'], d['phases_ms'])"
+timeout -s KILL 300 python bench.py --steps 20 --warmup 5 --no-cpu-baseline > gpurun_out/bench5.json 2> gpurun_out/bench5.err; echo "rc=$?"
+tail -2 gpurun_out/bench5.err; python -c "import json; d=json.load(open('gpurun_out/bench5.json')); print(d['ms_per_step'], d['value'], d['step_roofline']['frac'], d['e2e']['value'], {k:round(v*1e3,1) for k,v in d['phases_ms'].items()})"
