@@ -20,13 +20,17 @@ constexpr int kStageBytesB = (kPairN / 2) * kBlockK * 2;  // 16 KB (own half of 
 // similarity kernel: A (the anchor rows) stays resident for up to 8 K blocks (d <= 512;
 // larger d streams A in 512-wide chunks through the same slots), B streams through a ring.
 constexpr int kSimASlots = 8;
-constexpr int kSimStages = 5;
+constexpr int kSimStagesStats = 5;   // B ring depth, statistics pass
+constexpr int kSimStagesQ = 3;       // B ring depth, Q pass (smem goes to the Q store staging)
+constexpr int kSimStageOutQ = 32 * 64;   // per epilogue warp: 32 rows x 32 bf16 (64-byte swizzled rows)
 constexpr int kSimEpiWarps = 16;   // 4 per TMEM lane quarter, 64 columns each
 constexpr int kSimThreads = (2 + kSimEpiWarps) * 32;
 constexpr int kSimPSlots = 3;      // column-parameter slots (Q pass): kappa, beta, coef x 256
 constexpr int kSimPSlotBytes = 3 * kPairN * 4;
-constexpr int kSimSmemBytes =
-    kSimASlots * kStageBytesA + kSimStages * kStageBytesB + kSimPSlots * kSimPSlotBytes + 1024 + 512;
+constexpr int kSimSmemStats = kSimASlots * kStageBytesA + kSimStagesStats * kStageBytesB + kSimPSlots * kSimPSlotBytes;
+constexpr int kSimSmemQ = kSimASlots * kStageBytesA + kSimStagesQ * kStageBytesB + kSimPSlots * kSimPSlotBytes +
+                          kSimEpiWarps * kSimStageOutQ;
+constexpr int kSimSmemBytes = (kSimSmemStats > kSimSmemQ ? kSimSmemStats : kSimSmemQ) + 1024 + 512;
 // gradient GEMM: A (Q') and B (E) both stream.
 constexpr int kStages = 6;
 constexpr int kGemmStageOut = 32 * 32 * 4;   // per epilogue warp: 32 rows x 32 fp32 (128-byte swizzled rows)
@@ -84,7 +88,7 @@ struct GemmParams {
 enum SimMode { kSimStats = 0, kSimQ = 1, kSimRaw = 2 };
 
 cudaError_t launch_sim(int mode, const SimParams& p, const CUtensorMap* mapA, const CUtensorMap* mapB,
-                       int grid, cudaStream_t s, float* raw_out);
+                       const CUtensorMap* mapQout, int grid, cudaStream_t s, float* raw_out);
 cudaError_t sim_set_smem();
 cudaError_t gemm_set_smem();
 cudaError_t launch_gemm(const GemmParams& p, const CUtensorMap* mapQ, const CUtensorMap* mapX,

@@ -64,14 +64,15 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 
 // 2D map over a row-major [outer x inner] array with a 128-byte swizzled box (bf16 or fp32).
 CUtensorMap make_map(const void* base, uint64_t inner, uint64_t outer, uint64_t row_bytes, uint32_t box_inner,
-                     uint32_t box_outer, CUtensorMapDataType dt = CU_TENSOR_MAP_DATA_TYPE_BFLOAT16) {
+                     uint32_t box_outer, CUtensorMapDataType dt = CU_TENSOR_MAP_DATA_TYPE_BFLOAT16,
+                     CUtensorMapSwizzle sw = CU_TENSOR_MAP_SWIZZLE_128B) {
   CUtensorMap m;
   cuuint64_t dims[2] = {inner, outer};
   cuuint64_t strides[1] = {row_bytes};
   cuuint32_t box[2] = {box_inner, box_outer};
   cuuint32_t es[2] = {1, 1};
   CUresult r = encode_fn()(&m, dt, 2, const_cast<void*>(base), dims, strides, box, es,
-                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) throw FcError{FC_ERR_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string(r) + ")"};
   return m;
@@ -146,7 +147,7 @@ struct LossStep {
   const void* map_o1 = nullptr;
   const void* map_o2 = nullptr;
   CUtensorMap mO[2];
-  CUtensorMap mE1k, mE2k, mE1n, mE2n, mQ[2], mQt;
+  CUtensorMap mE1k, mE2k, mE1n, mE2n, mQ[2], mQt, mQo[2];
   fc::StepArgs args{};
 
   double* F(int i) const { return f64 + static_cast<size_t>(i) * Bl; }
@@ -237,6 +238,9 @@ struct LossStep {
     mQ[0] = make_map(q, ldq, Bl, static_cast<uint64_t>(ldq) * 2, 64, 128);
     mQ[1] = make_map(q + static_cast<size_t>(Bl) * ldq, ldq, Bl, static_cast<uint64_t>(ldq) * 2, 64, 128);
     mQt = make_map(q, ldq, Bl, static_cast<uint64_t>(ldq) * 2, 64, 64);   // Q^T as MN-major A (K = 1)
+    for (int s2 = 0; s2 < 2; ++s2)   // Q-pass tile stores: 32 rows x 32 bf16, 64-byte swizzle
+      mQo[s2] = make_map(q + static_cast<size_t>(s2) * Bl * ldq, ldq, Bl, static_cast<uint64_t>(ldq) * 2, 32, 32,
+                         CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, CU_TENSOR_MAP_SWIZZLE_64B);
     build_args();
   }
 
@@ -374,7 +378,7 @@ struct LossStep {
     sp.debug = sim_debug;
     CUtensorMap mA[2] = {mE1k, mE2k}, mB[2] = {mE2k, mE1k};
     mark(2, st);
-    FC_CUDA(fc::launch_sim(fc::kSimStats, sp, mA, mB, pair_grid(sp.n_items), st, nullptr));
+    FC_CUDA(fc::launch_sim(fc::kSimStats, sp, mA, mB, nullptr, pair_grid(sp.n_items), st, nullptr));
 
     // ---- u table, payload, (all-gather), weights, reductions, tau update ----
     mark(3, st);
@@ -411,7 +415,7 @@ struct LossStep {
       sp.n_rb[1] = 0;
       sp.n_items = sp.n_rb[0] * n_jt;
     }
-    FC_CUDA(fc::launch_sim(fc::kSimQ, sp, mA, mB, pair_grid(sp.n_items), st, nullptr));
+    FC_CUDA(fc::launch_sim(fc::kSimQ, sp, mA, mB, mQo, pair_grid(sp.n_items), st, nullptr));
 
     // ---- pass 2b: dE = c (Q' E - r o E_local) ----
     mark(5, st);
@@ -724,7 +728,7 @@ int fc_debug_similarity(const void* a, const void* b, int32_t rows, int32_t cols
     cudaGetDevice(&dev);
     FC_CUDA(fc::sim_set_smem());
     const int pairs = std::min(sm_count(dev) / 2, sp.n_items);
-    FC_CUDA(fc::launch_sim(fc::kSimRaw, sp, &ma, &mb, std::max(1, pairs) * 2, static_cast<cudaStream_t>(stream), out));
+    FC_CUDA(fc::launch_sim(fc::kSimRaw, sp, &ma, &mb, nullptr, std::max(1, pairs) * 2, static_cast<cudaStream_t>(stream), out));
   });
 }
 

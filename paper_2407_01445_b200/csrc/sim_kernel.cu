@@ -25,8 +25,9 @@ constexpr float kClampLog2 = 60.0f * 1.4426950408889634f;  // kExpClampMax in th
 
 struct SmemLayout {
   uint8_t* a;          // kSimASlots x 16 KB: resident anchor rows (one K block per slot)
-  uint8_t* b;          // kSimStages x 16 KB: streamed contrast rows
+  uint8_t* b;          // kStagesB x 16 KB: streamed contrast rows
   float* par;          // kSimPSlots x {kappa[256], beta[256], coef[256]} (Q pass)
+  uint8_t* qout;       // kSimEpiWarps x 2 KB: Q store staging (Q pass)
   uint64_t* full;      // B ring
   uint64_t* empty;
   uint64_t* afull;     // A slots
@@ -38,16 +39,18 @@ struct SmemLayout {
   uint32_t* tmem_ptr;
 };
 
+template <int kStagesB>
 __device__ __forceinline__ SmemLayout carve(uint8_t* base) {
   SmemLayout L;
   uint8_t* p = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(base) + 1023) & ~uintptr_t(1023));
   L.a = p;
   L.b = p + kSimASlots * kStageBytesA;
-  L.par = reinterpret_cast<float*>(L.b + kSimStages * kStageBytesB);
+  L.qout = L.b + kStagesB * kStageBytesB;
+  L.par = reinterpret_cast<float*>(L.qout + (kStagesB == kSimStagesQ ? kSimEpiWarps * kSimStageOutQ : 0));
   uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(L.par) + kSimPSlots * kSimPSlotBytes);
   L.full = bars;
-  L.empty = L.full + kSimStages;
-  L.afull = L.empty + kSimStages;
+  L.empty = L.full + kStagesB;
+  L.afull = L.empty + kStagesB;
   L.aempty = L.afull + kSimASlots;
   L.tfull = L.aempty + kSimASlots;
   L.tempty = L.tfull + 2;
@@ -124,7 +127,7 @@ __device__ __forceinline__ uint32_t count_clamps(const uint32_t (&r)[32], float 
 template <bool kMasked>
 __device__ __forceinline__ void q_chunk(const uint32_t (&r)[32], float rk, float rb, float rc, const float* kc,
                                         const float* bc, const float* cc, int col0, int cols, int gi,
-                                        uint32_t (&packed)[16]) {
+                                        uint32_t (&packed)[16], int dbg) {
 #pragma unroll
   for (int k = 0; k < 32; k += 4) {
     const float4 kk = *reinterpret_cast<const float4*>(kc + k);
@@ -138,7 +141,8 @@ __device__ __forceinline__ void q_chunk(const uint32_t (&r)[32], float rk, float
     for (int u = 0; u < 4; ++u) {
       const float s = __uint_as_float(r[k + u]);
       const float er = ex2_approx(fminf(fmaf(s, rk, rb), kClampLog2));
-      const float ec = ex2_approx(fminf(fmaf(s, kka[u], bba[u]), kClampLog2));
+      const float yc = fminf(fmaf(s, kka[u], bba[u]), kClampLog2);
+      const float ec = (dbg == 5 || dbg == 7) ? yc : ex2_approx(yc);
       float v = fmaf(cfa[u], ec, rc * er);
       if constexpr (kMasked) {
         const int j = col0 + k + u;
@@ -159,9 +163,11 @@ template <int kMode>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kSimThreads, 1)
     sim_tile_kernel(const __grid_constant__ SimParams p, const __grid_constant__ CUtensorMap mapA0,
                     const __grid_constant__ CUtensorMap mapB0, const __grid_constant__ CUtensorMap mapA1,
-                    const __grid_constant__ CUtensorMap mapB1, float* __restrict__ raw_out) {
+                    const __grid_constant__ CUtensorMap mapB1, const __grid_constant__ CUtensorMap mapQo0,
+                    const __grid_constant__ CUtensorMap mapQo1, float* __restrict__ raw_out) {
+  constexpr int kStagesB = kMode == kSimQ ? kSimStagesQ : kSimStagesStats;
   extern __shared__ uint8_t smem_raw[];
-  const SmemLayout L = carve(smem_raw);
+  const SmemLayout L = carve<kStagesB>(smem_raw);
   const uint32_t warp = threadIdx.x / 32;
   const uint32_t lane = lane_id();
   const uint32_t rank = cluster_ctarank();
@@ -178,7 +184,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kSimThreads, 1)
     }
   }
   if (warp == 1 && lane == 0) {
-    for (int i = 0; i < kSimStages; ++i) {
+    for (int i = 0; i < kStagesB; ++i) {
       mbar_init(&L.full[i], 2);   // leader's expect_tx arrive + peer's remote arrive
       mbar_init(&L.empty[i], 1);  // MMA commit (multicast to both CTAs)
     }
@@ -251,16 +257,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kSimThreads, 1)
           }
           for (int kb = kb_lo; kb < kb_hi; ++kb) {
             mbar_wait(&L.empty[stage], phase ^ 1);
-            if (p.debug == 2 && item != it_lo) {   // perf experiment: no B traffic after the first tile
+            if ((p.debug == 2 || p.debug == 3 || p.debug == 4) && item != it_lo) {   // perf experiment: no B traffic after the first tile
               if (rank == 0) mbar_arrive(&L.full[stage]);
               else mbar_arrive_cluster(&L.full[stage], 0);
-              if (++stage == kSimStages) { stage = 0; phase ^= 1; }
+              if (++stage == kStagesB) { stage = 0; phase ^= 1; }
               continue;
             }
             if (rank == 0) mbar_arrive_expect_tx(&L.full[stage], 2 * kStageBytesB);
             else mbar_arrive_cluster(&L.full[stage], 0);
             tma_load_2d_pair(mb, &L.full[stage], L.b + stage * kStageBytesB, kb * kBlockK, b_row);
-            if (++stage == kSimStages) { stage = 0; phase ^= 1; }
+            if (++stage == kStagesB) { stage = 0; phase ^= 1; }
           }
         }
       }
@@ -294,9 +300,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kSimThreads, 1)
           const bool last_use = nxt_key != key;
           for (int kb = kb_lo; kb < kb_hi; ++kb) {
             const int slot = kb - kb_lo;
-            if (p.debug < 4 || it == 0) mbar_wait(&L.afull[slot], (sgen[slot] - 1) & 1);
+            if (p.debug != 4 || it == 0) mbar_wait(&L.afull[slot], (sgen[slot] - 1) & 1);
             mbar_wait(&L.full[stage], phase);
-            if (p.debug < 4) tc_fence_after();
+            if (p.debug != 4) tc_fence_after();
             if (elect_one()) {
               const uint32_t a0 = smem_u32(L.a + slot * kStageBytesA);
               const uint32_t b0 = smem_u32(L.b + stage * kStageBytesB);
@@ -311,7 +317,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kSimThreads, 1)
               if (c == n_chunks - 1 && kb == kb_hi - 1) mma_commit_pair(&L.tfull[acc], 0x3);
             }
             __syncwarp();
-            if (++stage == kSimStages) { stage = 0; phase ^= 1; }
+            if (++stage == kStagesB) { stage = 0; phase ^= 1; }
           }
         }
       }
@@ -350,7 +356,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kSimThreads, 1)
       tc_fence_after();
       uint32_t r0[32], r1[32];
       const uint32_t taddr = tmem_base + ((q4 * 32u) << 16) + acc * kPairN + cq * 64u;
-      if (p.debug >= 3) {
+      if (p.debug >= 3 && p.debug < 5) {
 #pragma unroll
         for (int k = 0; k < 32; ++k) { r0[k] = 0; r1[k] = 0; }
       } else {
@@ -366,7 +372,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kSimThreads, 1)
         else mbar_arrive_cluster(&L.tempty[acc], 0);
       }
 
-      if (p.debug) {
+      if (p.debug && p.debug < 5) {
         if constexpr (kMode == kSimQ) {
           const int ps = it % kSimPSlots;
           mbar_wait(&L.pfull[ps], (it / kSimPSlots) & 1);
@@ -414,13 +420,26 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kSimThreads, 1)
           const bool fast = (col0 + 32 <= sg.cols) && !(col0 < g0 + 32 && g0 < col0 + 32);
           uint32_t packed[16];
           const float* kc = par + 32 * h;
-          if (fast) q_chunk<false>(rr, rk, rbeta, rc, kc, kc + kPairN, kc + 2 * kPairN, col0, sg.cols, gi, packed);
-          else q_chunk<true>(rr, rk, rbeta, rc, kc, kc + kPairN, kc + 2 * kPairN, col0, sg.cols, gi, packed);
-          if (row_ok && col0 < p.ldq) {
-            uint4* dst = reinterpret_cast<uint4*>(sg.q + static_cast<size_t>(r_loc) * p.ldq + col0);
+          if (fast) q_chunk<false>(rr, rk, rbeta, rc, kc, kc + kPairN, kc + 2 * kPairN, col0, sg.cols, gi, packed, p.debug);
+          else q_chunk<true>(rr, rk, rbeta, rc, kc, kc + kPairN, kc + 2 * kPairN, col0, sg.cols, gi, packed, p.debug);
+          if (col0 < p.ldq && p.debug != 6 && p.debug != 7) {
+            // 32 rows x 64 B through 64-byte-swizzled staging -> one TMA tile store (rows past
+            // the segment and columns past ldq are clipped by the tensor map)
+            uint8_t* stg = L.qout + (warp - 2) * kSimStageOutQ;
+            if (lane == 0) bulk_wait_read0();
+            __syncwarp();
+            uint8_t* rowp = stg + lane * 64;
+            const uint32_t sw = (lane >> 1) & 3;
 #pragma unroll
             for (int v4 = 0; v4 < 4; ++v4)
-              dst[v4] = make_uint4(packed[4 * v4], packed[4 * v4 + 1], packed[4 * v4 + 2], packed[4 * v4 + 3]);
+              *reinterpret_cast<uint4*>(rowp + ((v4 ^ sw) << 4)) =
+                  make_uint4(packed[4 * v4], packed[4 * v4 + 1], packed[4 * v4 + 2], packed[4 * v4 + 3]);
+            fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) {
+              tma_store_2d(s ? &mapQo1 : &mapQo0, stg, col0, warp_row0);
+              bulk_commit();
+            }
           }
         }
         __syncwarp();
@@ -429,6 +448,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kSimThreads, 1)
     }
   }
 
+  if constexpr (kMode == kSimQ) {
+    if (warp >= 2 && lane == 0) bulk_wait0();
+  }
   tc_fence_before();
   cluster_sync();
   if (warp == 2) tmem_dealloc<2>(tmem_base, 512);
@@ -441,21 +463,23 @@ cudaError_t sim_set_smem() {
   return e;
 }
 
-cudaError_t launch_sim(int mode, const SimParams& p, const CUtensorMap* mapA, const CUtensorMap* mapB, int grid,
-                       cudaStream_t s, float* raw_out) {
+cudaError_t launch_sim(int mode, const SimParams& p, const CUtensorMap* mapA, const CUtensorMap* mapB,
+                       const CUtensorMap* mapQout, int grid, cudaStream_t s, float* raw_out) {
   const CUtensorMap& a1 = p.nseg > 1 ? mapA[1] : mapA[0];
   const CUtensorMap& b1 = p.nseg > 1 ? mapB[1] : mapB[0];
+  const CUtensorMap& q0 = mapQout ? mapQout[0] : mapA[0];
+  const CUtensorMap& q1 = mapQout ? (p.nseg > 1 ? mapQout[1] : mapQout[0]) : mapA[0];
   if (grid < 2) grid = 2;
   grid &= ~1;
   switch (mode) {
     case kSimStats:
-      sim_tile_kernel<kSimStats><<<grid, kSimThreads, kSimSmemBytes, s>>>(p, mapA[0], mapB[0], a1, b1, raw_out);
+      sim_tile_kernel<kSimStats><<<grid, kSimThreads, kSimSmemBytes, s>>>(p, mapA[0], mapB[0], a1, b1, q0, q1, raw_out);
       break;
     case kSimQ:
-      sim_tile_kernel<kSimQ><<<grid, kSimThreads, kSimSmemBytes, s>>>(p, mapA[0], mapB[0], a1, b1, raw_out);
+      sim_tile_kernel<kSimQ><<<grid, kSimThreads, kSimSmemBytes, s>>>(p, mapA[0], mapB[0], a1, b1, q0, q1, raw_out);
       break;
     default:
-      sim_tile_kernel<kSimRaw><<<grid, kSimThreads, kSimSmemBytes, s>>>(p, mapA[0], mapB[0], a1, b1, raw_out);
+      sim_tile_kernel<kSimRaw><<<grid, kSimThreads, kSimSmemBytes, s>>>(p, mapA[0], mapB[0], a1, b1, q0, q1, raw_out);
       break;
   }
   return cudaGetLastError();
