@@ -334,12 +334,11 @@ def main():
     # SURVEY.md §8d algorithmic flops: K=1: 6 B^2 d (S once + two weight GEMMs);
     # K>1: 8 Bl B d per rank (row block + column block + two GEMMs).
     step_flops = 6.0 * B * B * d if world == 1 else 8.0 * Bd
-    per_kernel_flops = {
-        "pass1_stats": (2.0 * B * B * d) if world == 1 else 4.0 * Bd,   # S (counted once at K=1)
-        "pass2_q": 0.0,                                                  # S recompute (not algorithmic)
-        "grad_gemm": 4.0 * Bd,                                           # Q'_R E2 + Q'_C E1
-    }
-    exec_flops = {"pass1_stats": 4.0 * Bd, "pass2_q": 4.0 * Bd, "grad_gemm": 4.0 * Bd}
+    # the step's algorithmic flops split over the three tensor kernels (shares sum to F):
+    # S (2 B^2 d at K=1, 4 Bl B d at K>1) is credited half to each similarity pass.
+    s_share = (1.0 * B * B * d) if world == 1 else 2.0 * Bd
+    per_kernel_flops = {"pass1_stats": s_share, "pass2_q": s_share, "grad_gemm": 4.0 * Bd}
+    exec_flops = {"pass1_stats": 4.0 * Bd, "pass2_q": (2.0 if world == 1 else 4.0) * Bd, "grad_gemm": 4.0 * Bd}
     tensor_phases = ["pass1_stats", "pass2_q", "grad_gemm"]
     dom = max(tensor_phases, key=lambda k: phases[k])
     t_dom = phases[dom] * 1e-3

@@ -62,6 +62,7 @@ struct SimParams {
   int n_items;
   unsigned long long* clamps;  // STATS: exponent clamps (safe_exp, losses.cpp:22-28)
   int debug;                   // perf experiments: 1 = skip epilogue math, 2 = also skip B loads
+  long long* dbg_out;          // debug == 9: per-pair MMA-warp cycle counters [pair][8]
 };
 
 // ---- weighted-gradient GEMM: out = scale * (Q' X - r o X_local) ----
@@ -90,6 +91,8 @@ enum SimMode { kSimStats = 0, kSimQ = 1, kSimRaw = 2 };
 cudaError_t launch_sim(int mode, const SimParams& p, const CUtensorMap* mapA, const CUtensorMap* mapB,
                        const CUtensorMap* mapQout, int grid, cudaStream_t s, float* raw_out);
 cudaError_t sim_set_smem();
+cudaError_t launch_ring_probe(int n_pairs, int n_kb, int tile_kb, int epi, long long* cycles, cudaStream_t s);
+cudaError_t launch_mma_probe(int n_pairs, int n_mma, int commit_every, long long* cycles, cudaStream_t s);
 cudaError_t gemm_set_smem();
 cudaError_t launch_gemm(const GemmParams& p, const CUtensorMap* mapQ, const CUtensorMap* mapX,
                         const CUtensorMap* mapOut, int grid, cudaStream_t s);

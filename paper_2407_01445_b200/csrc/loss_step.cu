@@ -123,7 +123,8 @@ struct LossStep {
   double* scal = nullptr;        // device {gamma_t, eps_t}
   bool use_graph = true;
   bool shared_q = true;          // K == 1: one Q pass, Q^T read by the dE2 GEMM
-  int sim_debug = 0, gemm_debug = 0;             // FC_SIM_DEBUG perf experiments (results invalid when set)
+  int sim_debug = 0, gemm_debug = 0;
+  long long* dbg_buf = nullptr;   // FC_SIM_DEBUG=9 MMA-warp counters: [launch 0: pass 1, 1: pass 2][pair][8]             // FC_SIM_DEBUG perf experiments (results invalid when set)
   struct GraphEntry {
     const void* key[5];
     cudaGraphExec_t exec;
@@ -230,6 +231,7 @@ struct LossStep {
     shared_q = K == 1;
     if (const char* e = std::getenv("FC_DEBUG_SYNC")) debug_sync = atoi(e) != 0;
     if (const char* e = std::getenv("FC_SIM_DEBUG")) sim_debug = atoi(e);
+    if (sim_debug == 9) dbg_buf = dalloc<long long>(2 * 1664);
     if (const char* e = std::getenv("FC_GEMM_DEBUG")) gemm_debug = atoi(e);
     if (debug_sync) use_graph = false;
     if (const char* e = std::getenv("FC_SHARED_Q")) shared_q = shared_q && atoi(e) != 0;
@@ -376,6 +378,7 @@ struct LossStep {
     sp.n_items = (sp.n_rb[0] + sp.n_rb[1]) * n_jt;
     sp.clamps = clamps;
     sp.debug = sim_debug;
+    if (sim_debug == 9) sp.dbg_out = dbg_buf;
     CUtensorMap mA[2] = {mE1k, mE2k}, mB[2] = {mE2k, mE1k};
     mark(2, st);
     FC_CUDA(fc::launch_sim(fc::kSimStats, sp, mA, mB, nullptr, pair_grid(sp.n_items), st, nullptr));
@@ -415,6 +418,7 @@ struct LossStep {
       sp.n_rb[1] = 0;
       sp.n_items = sp.n_rb[0] * n_jt;
     }
+    if (sim_debug == 9) sp.dbg_out = dbg_buf + 1664;   // pass-2 counters / timelines
     FC_CUDA(fc::launch_sim(fc::kSimQ, sp, mA, mB, mQo, pair_grid(sp.n_items), st, nullptr));
 
     // ---- pass 2b: dE = c (Q' E - r o E_local) ----
@@ -513,6 +517,19 @@ int guarded(Fn&& fn) {
 extern "C" {
 
 const char* fc_last_error(void) { return g_last_error.c_str(); }
+
+int fc_debug_ring_probe(int32_t n_pairs, int32_t n_kb, int32_t tile_kb, int32_t epi, long long* cycles_dev,
+                        void* stream) {
+  return guarded([&] {
+    FC_CUDA(fc::launch_ring_probe(n_pairs, n_kb, tile_kb, epi, cycles_dev, static_cast<cudaStream_t>(stream)));
+  });
+}
+
+int fc_debug_mma_probe(int32_t n_pairs, int32_t n_mma, int32_t commit_every, long long* cycles_dev, void* stream) {
+  return guarded([&] {
+    FC_CUDA(fc::launch_mma_probe(n_pairs, n_mma, commit_every, cycles_dev, static_cast<cudaStream_t>(stream)));
+  });
+}
 
 int fc_config_defaults(int32_t variant, int64_t n_train, fc_config* out) {
   if (!out) return FC_ERR_SHAPE;
@@ -702,6 +719,15 @@ int fc_phase_times(void* ctx, float* ms, int32_t n) {
     if (!s->ev_created) throw FcError{FC_ERR_CONFIG, "phase timing not enabled"};
     FC_CUDA(cudaEventSynchronize(s->ev[LossStep::kPhases]));
     for (int i = 0; i < n && i < LossStep::kPhases; ++i) FC_CUDA(cudaEventElapsedTime(&ms[i], s->ev[i], s->ev[i + 1]));
+  });
+}
+
+int fc_debug_counters(void* ctx, long long* out /* host [2*128*8] */) {
+  if (!ctx) return FC_ERR_SHAPE;
+  auto* s = static_cast<LossStep*>(ctx);
+  return guarded([&] {
+    FC_CUDA(cudaDeviceSynchronize());
+    if (s->dbg_buf) FC_CUDA(cudaMemcpy(out, s->dbg_buf, 2 * 1664 * 8, cudaMemcpyDeviceToHost));
   });
 }
 

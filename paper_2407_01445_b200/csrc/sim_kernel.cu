@@ -167,6 +167,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kSimThreads, 1)
                     const __grid_constant__ CUtensorMap mapQo1, float* __restrict__ raw_out) {
   constexpr int kStagesB = kMode == kSimQ ? kSimStagesQ : kSimStagesStats;
   extern __shared__ uint8_t smem_raw[];
+  long long g_entry = 0;
+  if (p.debug == 9) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_entry));
   const SmemLayout L = carve<kStagesB>(smem_raw);
   const uint32_t warp = threadIdx.x / 32;
   const uint32_t lane = lane_id();
@@ -175,7 +177,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kSimThreads, 1)
   const int n_pairs = gridDim.x / 2;
   const int nkb = (p.d + kBlockK - 1) / kBlockK;
 
-  if (warp == 0 && lane == 0) {
+  // warp roles: epilogue warps first, producer and MMA issuer LAST -- the SMSP arbiter
+  // favours the highest warp id, so the single-thread TMA/MMA issue never waits behind
+  // the epilogue math.
+  constexpr uint32_t kProdWarp = kSimEpiWarps, kMmaWarp = kSimEpiWarps + 1;
+  if (warp == kProdWarp && lane == 0) {
     tma_prefetch(&mapA0);
     tma_prefetch(&mapB0);
     if (p.nseg > 1) {
@@ -183,7 +189,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kSimThreads, 1)
       tma_prefetch(&mapB1);
     }
   }
-  if (warp == 1 && lane == 0) {
+  if (warp == kMmaWarp && lane == 0) {
     for (int i = 0; i < kStagesB; ++i) {
       mbar_init(&L.full[i], 2);   // leader's expect_tx arrive + peer's remote arrive
       mbar_init(&L.empty[i], 1);  // MMA commit (multicast to both CTAs)
@@ -202,7 +208,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kSimThreads, 1)
     }
     fence_barrier_init();
   }
-  if (warp == 2) tmem_alloc<2>(L.tmem_ptr, 512);
+  if (warp == 0) tmem_alloc<2>(L.tmem_ptr, 512);
   tc_fence_before();
   cluster_sync();
   tc_fence_after();
@@ -212,12 +218,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kSimThreads, 1)
   int it_lo, it_hi;
   pair_range(p.n_items, pair, n_pairs, it_lo, it_hi);
 
-  if (warp == 0) {
+  if (warp == kProdWarp) {
     // ===================== TMA producer (both CTAs) =====================
     // A (anchor rows, own 128 of the pair's 256) is loaded once per (segment, row block,
     // K chunk) into per-K-block slots; each slot is refilled as soon as the MMAs of the last
     // tile that read it retire (aempty), so the switch to the next row block overlaps.
-    if (elect_one()) {
+    // The whole warp walks the loop (warp-uniform waits); lane 0 issues. A single-thread loop
+    // in a diverged warp wakes from mbarrier waits noticeably later.
+    {
+      const bool issuer = lane == 0;
       uint32_t stage = 0, phase = 0;
       uint32_t sgen[kSimASlots] = {};   // per-slot load generation (phase parity of afull/aempty)
       int cur_key = -1;
@@ -233,12 +242,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kSimThreads, 1)
           // this tile's column parameters (each CTA keeps its own copy)
           const int ps = it % kSimPSlots;
           mbar_wait(&L.pempty[ps], ((it / kSimPSlots) & 1) ^ 1);
-          mbar_arrive_expect_tx(&L.pfull[ps], kSimPSlotBytes);
-          float* dst = L.par + ps * (kSimPSlotBytes / 4);
-          const SimSeg& sg = p.seg[s];
-          bulk_load(dst, sg.col_kappa + jt * kPairN, kPairN * 4, &L.pfull[ps]);
-          bulk_load(dst + kPairN, sg.col_beta + jt * kPairN, kPairN * 4, &L.pfull[ps]);
-          bulk_load(dst + 2 * kPairN, sg.col_coef + jt * kPairN, kPairN * 4, &L.pfull[ps]);
+          if (issuer) {
+            mbar_arrive_expect_tx(&L.pfull[ps], kSimPSlotBytes);
+            float* dst = L.par + ps * (kSimPSlotBytes / 4);
+            const SimSeg& sg = p.seg[s];
+            bulk_load(dst, sg.col_kappa + jt * kPairN, kPairN * 4, &L.pfull[ps]);
+            bulk_load(dst + kPairN, sg.col_beta + jt * kPairN, kPairN * 4, &L.pfull[ps]);
+            bulk_load(dst + 2 * kPairN, sg.col_coef + jt * kPairN, kPairN * 4, &L.pfull[ps]);
+          }
+          __syncwarp();
         }
         for (int c = 0; c < n_chunks; ++c) {
           const int kb_lo = c * kSimASlots;
@@ -249,40 +261,55 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kSimThreads, 1)
               const int slot = kb - kb_lo;
               mbar_wait(&L.aempty[slot], (sgen[slot] & 1) ^ 1);
               ++sgen[slot];
-              if (rank == 0) mbar_arrive_expect_tx(&L.afull[slot], 2 * kStageBytesA);
-              else mbar_arrive_cluster(&L.afull[slot], 0);
-              tma_load_2d_pair(ma, &L.afull[slot], L.a + slot * kStageBytesA, kb * kBlockK, a_row);
+              if (issuer) {
+                if (rank == 0) mbar_arrive_expect_tx(&L.afull[slot], 2 * kStageBytesA);
+                else mbar_arrive_cluster(&L.afull[slot], 0);
+                tma_load_2d_pair(ma, &L.afull[slot], L.a + slot * kStageBytesA, kb * kBlockK, a_row);
+              }
+              __syncwarp();
             }
             cur_key = key;
           }
           for (int kb = kb_lo; kb < kb_hi; ++kb) {
             mbar_wait(&L.empty[stage], phase ^ 1);
-            if ((p.debug == 2 || p.debug == 3 || p.debug == 4) && item != it_lo) {   // perf experiment: no B traffic after the first tile
-              if (rank == 0) mbar_arrive(&L.full[stage]);
-              else mbar_arrive_cluster(&L.full[stage], 0);
-              if (++stage == kStagesB) { stage = 0; phase ^= 1; }
-              continue;
+            if (issuer) {
+              if ((p.debug == 2 || p.debug == 3 || p.debug == 4) && item != it_lo) {   // perf experiment: no B traffic
+                if (rank == 0) mbar_arrive(&L.full[stage]);
+                else mbar_arrive_cluster(&L.full[stage], 0);
+              } else {
+                if (rank == 0) mbar_arrive_expect_tx(&L.full[stage], 2 * kStageBytesB);
+                else mbar_arrive_cluster(&L.full[stage], 0);
+                tma_load_2d_pair(mb, &L.full[stage], L.b + stage * kStageBytesB, kb * kBlockK, b_row);
+              }
             }
-            if (rank == 0) mbar_arrive_expect_tx(&L.full[stage], 2 * kStageBytesB);
-            else mbar_arrive_cluster(&L.full[stage], 0);
-            tma_load_2d_pair(mb, &L.full[stage], L.b + stage * kStageBytesB, kb * kBlockK, b_row);
+            __syncwarp();
             if (++stage == kStagesB) { stage = 0; phase ^= 1; }
           }
         }
       }
     }
-  } else if (warp == 1) {
-    // ===================== MMA issuer (leader CTA only) =====================
+  } else if (warp == kMmaWarp) {
+    // ===================== MMA issuer (leader CTA only, one thread) =====================
+    // The issue loop is kept lean (precomputed descriptors, no per-MMA address math, no
+    // warp-wide election per k block): with ~100+ cycles of scalar work per MMA the single
+    // issuing thread, not the tensor pipe, would set the pace (128 cycles per 256x256x16).
     if (rank == 0) {
       constexpr uint32_t idesc = make_idesc_bf16(kPairM, kPairN, 0, 0);
+      const uint64_t a_desc0 = make_sdesc_sw128(smem_u32(L.a), 0, 1024);
+      const uint64_t b_desc0 = make_sdesc_sw128(smem_u32(L.b), 0, 1024);
       uint32_t stage = 0, phase = 0;
       uint32_t sgen[kSimASlots] = {};
+      uint32_t ready = 0;   // bit per A slot: afull of the current generation observed
       int cur_key = -1;
       int it = 0;
+      const bool prof = p.debug == 9;
+      long long c_start = clock64(), c_tempty = 0, c_afull = 0, c_full = 0, c_first = 0, n_mma = 0;
       for (int item = it_lo; item < it_hi; ++item, ++it) {
         const uint32_t acc = it & 1;
         const uint32_t acc_phase = (it >> 1) & 1;
+        long long t0 = prof ? clock64() : 0;
         mbar_wait(&L.tempty[acc], acc_phase ^ 1);
+        if (prof) c_tempty += clock64() - t0;
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * kPairN;
         for (int c = 0; c < n_chunks; ++c) {
@@ -291,6 +318,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kSimThreads, 1)
           const int key = a_key(p, item, c, n_chunks);
           if (key != cur_key) {
             cur_key = key;
+            ready = 0;
             for (int kb = kb_lo; kb < kb_hi; ++kb) ++sgen[kb - kb_lo];
           }
           // last use of this A generation: release each slot right after its MMAs
@@ -298,34 +326,49 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kSimThreads, 1)
           if (c + 1 < n_chunks) nxt_key = a_key(p, item, c + 1, n_chunks);
           else if (item + 1 < it_hi) nxt_key = a_key(p, item + 1, 0, n_chunks);
           const bool last_use = nxt_key != key;
+          const bool last_chunk = c == n_chunks - 1;
           for (int kb = kb_lo; kb < kb_hi; ++kb) {
             const int slot = kb - kb_lo;
-            if (p.debug != 4 || it == 0) mbar_wait(&L.afull[slot], (sgen[slot] - 1) & 1);
+            if (!(ready & (1u << slot))) {
+              long long t1 = prof ? clock64() : 0;
+              mbar_wait(&L.afull[slot], (sgen[slot] - 1) & 1);
+              if (prof) c_afull += clock64() - t1;
+              ready |= 1u << slot;
+            }
+            long long t2 = prof ? clock64() : 0;
             mbar_wait(&L.full[stage], phase);
-            if (p.debug != 4) tc_fence_after();
+            if (prof) {
+              c_full += clock64() - t2;
+              if (n_mma == 0) c_first = clock64() - c_start;
+              n_mma += 4;
+            }
+            tc_fence_after();
             if (elect_one()) {
-              const uint32_t a0 = smem_u32(L.a + slot * kStageBytesA);
-              const uint32_t b0 = smem_u32(L.b + stage * kStageBytesB);
-#pragma unroll
-              for (int k = 0; k < kBlockK / 16; ++k) {
-                const uint64_t ad = make_sdesc_sw128(a0 + k * 32, 0, 1024);
-                const uint64_t bd = make_sdesc_sw128(b0 + k * 32, 0, 1024);
-                mma_bf16_pair(d_tmem, ad, bd, idesc, (kb | k) != 0);
-              }
+              const uint64_t ad = a_desc0 + static_cast<uint64_t>((slot * kStageBytesA) >> 4);
+              const uint64_t bd = b_desc0 + static_cast<uint64_t>((stage * kStageBytesB) >> 4);
+              mma_bf16_pair(d_tmem, ad, bd, idesc, kb != 0);
+              mma_bf16_pair(d_tmem, ad + 2, bd + 2, idesc, 1);
+              mma_bf16_pair(d_tmem, ad + 4, bd + 4, idesc, 1);
+              mma_bf16_pair(d_tmem, ad + 6, bd + 6, idesc, 1);
               mma_commit_pair(&L.empty[stage], 0x3);
               if (last_use) mma_commit_pair(&L.aempty[slot], 0x3);
-              if (c == n_chunks - 1 && kb == kb_hi - 1) mma_commit_pair(&L.tfull[acc], 0x3);
+              if (last_chunk && kb == kb_hi - 1) mma_commit_pair(&L.tfull[acc], 0x3);
             }
             __syncwarp();
             if (++stage == kStagesB) { stage = 0; phase ^= 1; }
           }
         }
       }
+      if (prof && lane == 0) {
+        long long* o = p.dbg_out + pair * 8;
+        o[0] = clock64() - c_start; o[1] = c_tempty; o[2] = c_afull; o[3] = c_full; o[4] = c_first; o[5] = n_mma;
+        o[6] = it_hi - it_lo;
+      }
     }
   } else {
     // ===================== epilogue (both CTAs) =====================
     const uint32_t q4 = warp & 3;               // TMEM lane quarter accessible to this warp
-    const uint32_t cq = (warp - 2) >> 2;        // 64-column quarter of the 256-wide tile
+    const uint32_t cq = warp >> 2;        // 64-column quarter of the 256-wide tile
     int it = 0;
     for (int item = it_lo; item < it_hi; ++item, ++it) {
       int s, rb, jt;
@@ -425,7 +468,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kSimThreads, 1)
           if (col0 < p.ldq && p.debug != 6 && p.debug != 7) {
             // 32 rows x 64 B through 64-byte-swizzled staging -> one TMA tile store (rows past
             // the segment and columns past ldq are clipped by the tensor map)
-            uint8_t* stg = L.qout + (warp - 2) * kSimStageOutQ;
+            uint8_t* stg = L.qout + warp * kSimStageOutQ;
             if (lane == 0) bulk_wait_read0();
             __syncwarp();
             uint8_t* rowp = stg + lane * 64;
@@ -449,11 +492,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kSimThreads, 1)
   }
 
   if constexpr (kMode == kSimQ) {
-    if (warp >= 2 && lane == 0) bulk_wait0();
+    if (warp < kProdWarp && lane == 0) bulk_wait0();
   }
+  __syncwarp();   // single-thread producer / MMA roles reconverge before the aligned cluster barrier
+  long long g_work_end = 0;
+  if (p.debug == 9) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_work_end));
   tc_fence_before();
   cluster_sync();
-  if (warp == 2) tmem_dealloc<2>(tmem_base, 512);
+  if (warp == 0) tmem_dealloc<2>(tmem_base, 512);
+  if (p.debug == 9 && threadIdx.x == 0) {
+    long long g_exit;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_exit));
+    long long* o = p.dbg_out + 1024 + blockIdx.x * 4;   // per-CTA timeline (ns)
+    o[0] = g_entry; o[1] = g_work_end; o[2] = g_exit;
+  }
 }
 
 cudaError_t sim_set_smem() {
