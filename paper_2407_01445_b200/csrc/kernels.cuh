@@ -45,8 +45,8 @@ struct SimSeg {
   int rows;                 // local anchors in this segment
   int a_row0;               // global index of local row 0 (diagonal masking)
   int cols;                 // contrast set size (global batch B)
-  const float2* row_stat;   // STATS: [rows] {S_ii, log2(e)/t_i}
-  float2* partial;          // STATS: [rows][n_jt*4] {sum e, sum (s - s_ii) e} per column quarter
+  const float2* row_stat;   // STATS: [rows] {kappa_i = log2(e)/t_i, beta_i = -S_ii kappa_i}
+  float2* partial;          // STATS: [rows][n_jt*4] {sum e, sum y e} per column quarter
   // Q: exponent y = s*kappa + beta (= (s - S_aa) log2(e)/t_a), weight coef (SoA, fp32)
   const float* row_kappa; const float* row_beta; const float* row_coef;   // [rows]
   const float* col_kappa; const float* col_beta; const float* col_coef;   // [n_jt*256], zero padded
@@ -61,6 +61,7 @@ struct SimParams {
   int n_rb[2];
   int n_items;
   unsigned long long* clamps;  // STATS: exponent clamps (safe_exp, losses.cpp:22-28)
+  const float* bounds;         // {max |E1_i|^2, max |E2_j|^2, max kappa over G}: clamp-free fast paths
   int debug;                   // perf experiments: 1 = skip epilogue math, 2 = also skip B loads
   long long* dbg_out;          // debug == 9: per-pair MMA-warp cycle counters [pair][8]
 };

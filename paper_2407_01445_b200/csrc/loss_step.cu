@@ -109,6 +109,7 @@ struct LossStep {
   float* diag = nullptr;
   float2 *rowstat = nullptr, *partial = nullptr;
   unsigned long long* clamps = nullptr;
+  float* bounds = nullptr;
   double* f64 = nullptr;   // per-local-anchor fp64 arrays
   double *send = nullptr, *recv = nullptr, *gt_recv = nullptr, *red = nullptr, *blockpart = nullptr;
   unsigned* counter = nullptr;
@@ -206,6 +207,7 @@ struct LossStep {
     rowstat = dalloc<float2>(2 * static_cast<size_t>(Bl));
     partial = dalloc<float2>(2 * static_cast<size_t>(Bl) * n_jt * 4);
     clamps = dalloc<unsigned long long>(1);
+    bounds = dalloc<float>(4);
     f64 = dalloc<double>(static_cast<size_t>(Bl) * 18);
     send = dalloc<double>(5 * static_cast<size_t>(Bl));
     recv = K > 1 ? dalloc<double>(5 * static_cast<size_t>(B)) : send;
@@ -261,6 +263,7 @@ struct LossStep {
     a.rowstat_R = rowstat; a.rowstat_C = rowstat + Bl;
     a.partial_R = partial; a.partial_C = partial + static_cast<size_t>(Bl) * n_jt * 4;
     a.clamps = clamps;
+    a.bounds = bounds;
     a.t_loc1 = F(0); a.t_loc2 = F(1);
     a.sum1 = F(2); a.dx1 = F(3); a.sum2 = F(4); a.dx2 = F(5);
     a.g1 = F(6); a.g2 = F(7); a.u1 = F(8); a.u2 = F(9);
@@ -357,6 +360,7 @@ struct LossStep {
     a.scal = scal;
 
     mark(1, st);
+    FC_CUDA(cudaMemsetAsync(bounds, 0, 4 * sizeof(float), st));
     fc::fc_prep_kernel<<<(B * 32 + 255) / 256, 256, 0, st>>>(E1, E2, a);
     FC_CUDA(cudaGetLastError());
 
@@ -377,6 +381,7 @@ struct LossStep {
     }
     sp.n_items = (sp.n_rb[0] + sp.n_rb[1]) * n_jt;
     sp.clamps = clamps;
+    sp.bounds = bounds;
     sp.debug = sim_debug;
     if (sim_debug == 9) sp.dbg_out = dbg_buf;
     CUtensorMap mA[2] = {mE1k, mE2k}, mB[2] = {mE2k, mE1k};
@@ -481,7 +486,7 @@ struct LossStep {
     if (comm) ncclCommDestroy(comm);
     for (void* p : {(void*)u1, (void*)u2, (void*)tau1, (void*)tau2, (void*)m1, (void*)v1, (void*)m2, (void*)v2,
                     (void*)s1, (void*)s2, (void*)tau_state, (void*)e1g, (void*)e2g, (void*)diag, (void*)rowstat,
-                    (void*)partial, (void*)clamps, (void*)f64, (void*)red, (void*)par, (void*)rcoef, (void*)blockpart, (void*)counter,
+                    (void*)partial, (void*)clamps, (void*)bounds, (void*)f64, (void*)red, (void*)par, (void*)rcoef, (void*)blockpart, (void*)counter,
                     (void*)q, (void*)err, (void*)result_d, (void*)gt_recv})
       if (p) cudaFree(p);
     if (recv && recv != send) cudaFree(recv);
@@ -750,6 +755,13 @@ int fc_debug_similarity(const void* a, const void* b, int32_t rows, int32_t cols
     sp.seg[0].a_row0 = 0;
     sp.seg[0].cols = cols;
     sp.n_items = sp.n_rb[0] * sp.n_jt;
+    static float* dbg_bounds = nullptr;
+    if (!dbg_bounds) {
+      dbg_bounds = dalloc<float>(4);
+      const float big[4] = {1e30f, 1e30f, 1e30f, 0.f};
+      FC_CUDA(cudaMemcpy(dbg_bounds, big, sizeof(big), cudaMemcpyHostToDevice));
+    }
+    sp.bounds = dbg_bounds;
     int dev = 0;
     cudaGetDevice(&dev);
     FC_CUDA(fc::sim_set_smem());

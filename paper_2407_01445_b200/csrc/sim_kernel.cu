@@ -88,72 +88,73 @@ __device__ __forceinline__ void bulk_load(void* smem, const void* gmem, uint32_t
 }
 
 // ---- epilogue chunk processors (32 consecutive columns of one row per thread) ----
-// STATS, unmasked: every column valid and off-diagonal (warp-uniform fast path).
-__device__ __forceinline__ void stats_fast(const uint32_t (&r)[32], float d_i, float kap, float& se, float& sxe,
-                                           float& ymax) {
+// Exponents are formed directly in the log2 domain with one FMA, y = s*kappa + beta where
+// kappa = log2(e)/t and beta = -S_aa*kappa, and the packed fp32x2 pipe (FFMA2/FADD2) does
+// two elements per instruction. The fast paths skip the safe_exp clamp and the masks; a
+// warp-uniform check of the chunk's max exponent routes the (rare) clamped chunks, and the
+// ragged/diagonal chunks, to the exact slow path.
+__device__ __forceinline__ float2 f2(float a, float b) { return make_float2(a, b); }
+
+// STATS fast path: chunk sums of e and y*e (sum (s - S_ii) e = sum(y e) / kappa).
+__device__ __forceinline__ void stats_fast(const uint32_t (&r)[32], float kap, float beta, float2& se, float2& sye) {
+  const float2 k2 = f2(kap, kap), b2 = f2(beta, beta);
 #pragma unroll
-  for (int k = 0; k < 32; ++k) {
-    const float x = __uint_as_float(r[k]) - d_i;
-    const float y = x * kap;
-    ymax = fmaxf(ymax, y);
-    const float e = ex2_approx(fminf(y, kClampLog2));
-    se += e;
-    sxe = fmaf(x, e, sxe);
+  for (int k = 0; k < 32; k += 2) {
+    const float2 y = __ffma2_rn(f2(__uint_as_float(r[k]), __uint_as_float(r[k + 1])), k2, b2);
+    const float2 e = f2(ex2_approx(y.x), ex2_approx(y.y));
+    se = __fadd2_rn(se, e);
+    sye = __ffma2_rn(y, e, sye);
   }
 }
-// STATS, masked: ragged tail / diagonal / rows past the segment.
-__device__ __forceinline__ void stats_masked(const uint32_t (&r)[32], float d_i, float kap, int col0, int cols, int gi,
-                                             bool row_ok, float& se, float& sxe, uint32_t& ncl) {
+// STATS exact path: clamp (safe_exp), masks, clamp count.
+__device__ __forceinline__ void stats_masked(const uint32_t (&r)[32], float kap, float beta, int col0, int cols, int gi,
+                                             bool row_ok, float& se, float& sye, uint32_t& ncl) {
 #pragma unroll
   for (int k = 0; k < 32; ++k) {
     const int j = col0 + k;
-    const float x = __uint_as_float(r[k]) - d_i;
-    const float y = x * kap;
+    const float y = fmaf(__uint_as_float(r[k]), kap, beta);
     const bool ok = row_ok && (j < cols) && (j != gi);
     const float e = ex2_approx(fminf(y, kClampLog2));
     se += ok ? e : 0.f;
-    sxe += ok ? x * e : 0.f;
+    sye += ok ? y * e : 0.f;
     ncl += (ok && y > kClampLog2) ? 1u : 0u;
   }
 }
-__device__ __forceinline__ uint32_t count_clamps(const uint32_t (&r)[32], float d_i, float kap) {
-  uint32_t n = 0;
-#pragma unroll
-  for (int k = 0; k < 32; ++k) n += ((__uint_as_float(r[k]) - d_i) * kap > kClampLog2) ? 1u : 0u;
-  return n;
-}
 
 // Q: 32 bf16 weights of one row; col params from shared memory (broadcast reads).
-template <bool kMasked>
+template <bool kExact>
 __device__ __forceinline__ void q_chunk(const uint32_t (&r)[32], float rk, float rb, float rc, const float* kc,
-                                        const float* bc, const float* cc, int col0, int cols, int gi,
-                                        uint32_t (&packed)[16], int dbg) {
+                                         const float* bc, const float* cc, int col0, int cols, int gi,
+                                         uint32_t (&packed)[16]) {
+  const float2 rk2 = f2(rk, rk), rb2 = f2(rb, rb), rc2 = f2(rc, rc);
 #pragma unroll
   for (int k = 0; k < 32; k += 4) {
     const float4 kk = *reinterpret_cast<const float4*>(kc + k);
     const float4 bb = *reinterpret_cast<const float4*>(bc + k);
     const float4 cf = *reinterpret_cast<const float4*>(cc + k);
-    const float kka[4] = {kk.x, kk.y, kk.z, kk.w};
-    const float bba[4] = {bb.x, bb.y, bb.z, bb.w};
-    const float cfa[4] = {cf.x, cf.y, cf.z, cf.w};
-    float q[4];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const float s = __uint_as_float(r[k + u]);
-      const float er = ex2_approx(fminf(fmaf(s, rk, rb), kClampLog2));
-      const float yc = fminf(fmaf(s, kka[u], bba[u]), kClampLog2);
-      const float ec = (dbg == 5 || dbg == 7) ? yc : ex2_approx(yc);
-      float v = fmaf(cfa[u], ec, rc * er);
-      if constexpr (kMasked) {
-        const int j = col0 + k + u;
-        v = (j < cols && j != gi) ? v : 0.f;
+    for (int h = 0; h < 2; ++h) {
+      const float2 s = f2(__uint_as_float(r[k + 2 * h]), __uint_as_float(r[k + 2 * h + 1]));
+      const float2 kc2 = h ? f2(kk.z, kk.w) : f2(kk.x, kk.y);
+      const float2 bc2 = h ? f2(bb.z, bb.w) : f2(bb.x, bb.y);
+      const float2 cc2 = h ? f2(cf.z, cf.w) : f2(cf.x, cf.y);
+      float2 yr = __ffma2_rn(s, rk2, rb2);
+      float2 yc = __ffma2_rn(s, kc2, bc2);
+      if constexpr (kExact) {
+        yr = f2(fminf(yr.x, kClampLog2), fminf(yr.y, kClampLog2));
+        yc = f2(fminf(yc.x, kClampLog2), fminf(yc.y, kClampLog2));
       }
-      q[u] = v;
+      const float2 er = f2(ex2_approx(yr.x), ex2_approx(yr.y));
+      const float2 ec = f2(ex2_approx(yc.x), ex2_approx(yc.y));
+      float2 q = __ffma2_rn(cc2, ec, __fmul2_rn(rc2, er));
+      if constexpr (kExact) {
+        const int j = col0 + k + 2 * h;
+        q.x = (j < cols && j != gi) ? q.x : 0.f;
+        q.y = (j + 1 < cols && j + 1 != gi) ? q.y : 0.f;
+      }
+      __nv_bfloat162 hq = __floats2bfloat162_rn(q.x, q.y);
+      packed[k / 2 + h] = *reinterpret_cast<uint32_t*>(&hq);
     }
-    __nv_bfloat162 h0 = __floats2bfloat162_rn(q[0], q[1]);
-    __nv_bfloat162 h1 = __floats2bfloat162_rn(q[2], q[3]);
-    packed[k / 2] = *reinterpret_cast<uint32_t*>(&h0);
-    packed[k / 2 + 1] = *reinterpret_cast<uint32_t*>(&h1);
   }
 }
 
@@ -368,6 +369,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kSimThreads, 1)
   } else {
     // ===================== epilogue (both CTAs) =====================
     const uint32_t q4 = warp & 3;               // TMEM lane quarter accessible to this warp
+    long long e_wait = 0, e_ld = 0, e_math = 0, e_t0 = clock64();
+    const bool eprof = p.debug == 9 && warp == 5;
     const uint32_t cq = warp >> 2;        // 64-column quarter of the 256-wide tile
     int it = 0;
     for (int item = it_lo; item < it_hi; ++item, ++it) {
@@ -395,76 +398,63 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kSimThreads, 1)
         }
       }
 
+      long long ta = eprof ? clock64() : 0;
       mbar_wait(&L.tfull[acc], acc_phase);
+      long long tb = eprof ? clock64() : 0;
+      if (eprof) e_wait += tb - ta;
       tc_fence_after();
-      uint32_t r0[32], r1[32];
+      // safe_exp can only clamp if some exponent may exceed 60: |s| <= |E1|max |E2|max bounds it
+      const float smax = sqrtf(p.bounds[0] * p.bounds[1]) * 1.0001f;
       const uint32_t taddr = tmem_base + ((q4 * 32u) << 16) + acc * kPairN + cq * 64u;
-      if (p.debug >= 3 && p.debug < 5) {
-#pragma unroll
-        for (int k = 0; k < 32; ++k) { r0[k] = 0; r1[k] = 0; }
-      } else {
-        tmem_ld_32x32b_x32(taddr, r0);
-        tmem_ld_32x32b_x32(taddr + 32, r1);
-        tmem_ld_wait();
-      }
-      // the tile is in registers: hand the TMEM buffer back to the MMA warp right away
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) {
-        if (rank == 0) mbar_arrive(&L.tempty[acc]);
-        else mbar_arrive_cluster(&L.tempty[acc], 0);
-      }
-
-      if (p.debug && p.debug < 5) {
-        if constexpr (kMode == kSimQ) {
-          const int ps = it % kSimPSlots;
-          mbar_wait(&L.pfull[ps], (it / kSimPSlots) & 1);
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&L.pempty[ps]);
-        }
-        if (r0[3] == 0x7fffffffu && r1[5] == 0x7fffffffu) sg.partial[0] = make_float2(0.f, 0.f);  // keep loads live
-      } else if constexpr (kMode == kSimRaw) {
-        if (row_ok) {
-          float* dst = raw_out + static_cast<size_t>(r_loc) * sg.cols;
-#pragma unroll
-          for (int k = 0; k < 32; ++k) {
-            if (colq + k < sg.cols) dst[colq + k] = __uint_as_float(r0[k]);
-            if (colq + 32 + k < sg.cols) dst[colq + 32 + k] = __uint_as_float(r1[k]);
-          }
-        }
-      } else if constexpr (kMode == kSimStats) {
-        float se = 0.f, sxe = 0.f;
-        uint32_t ncl = 0;
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const uint32_t(&rr)[32] = h ? r1 : r0;
-          const int col0 = colq + 32 * h;
-          const bool fast = warp_rows_ok && (col0 + 32 <= sg.cols) && !(col0 < g0 + 32 && g0 < col0 + 32);
-          if (fast) {
-            float ym = -INFINITY;
-            stats_fast(rr, rstat.x, rstat.y, se, sxe, ym);
-            if (__any_sync(0xffffffffu, ym > kClampLog2)) ncl += count_clamps(rr, rstat.x, rstat.y);
-          } else {
-            stats_masked(rr, rstat.x, rstat.y, col0, sg.cols, gi, row_ok, se, sxe, ncl);
-          }
-        }
-        if (row_ok) sg.partial[static_cast<size_t>(r_loc) * (p.n_jt * 4) + jt * 4 + cq] = make_float2(se, sxe);
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) ncl += __shfl_xor_sync(0xffffffffu, ncl, o);
-        if (lane == 0 && ncl) atomicAdd(p.clamps, static_cast<unsigned long long>(ncl));
-      } else {  // kSimQ
-        const int ps = it % kSimPSlots;
+      float2 se2 = f2(0.f, 0.f), sye2 = f2(0.f, 0.f);
+      float se = 0.f, sye = 0.f;
+      uint32_t ncl = 0;
+      int ps = 0;
+      const float* par = nullptr;
+      bool q_col_safe = false;
+      if constexpr (kMode == kSimQ) {
+        ps = it % kSimPSlots;
         mbar_wait(&L.pfull[ps], (it / kSimPSlots) & 1);
-        const float* par = L.par + ps * (kSimPSlotBytes / 4) + cq * 64;
+        par = L.par + ps * (kSimPSlotBytes / 4) + cq * 64;
+        q_col_safe = 2.f * smax * p.bounds[2] <= kClampLog2;
+      }
+      const float row_kap = kMode == kSimQ ? rk : rstat.x;
+      const float row_beta = kMode == kSimQ ? rbeta : rstat.y;
+      const bool row_safe = !__any_sync(0xffffffffu, row_ok && fmaf(smax, row_kap, row_beta) > kClampLog2);
+#pragma unroll 1
+      for (int h = 0; h < 2; ++h) {
+        uint32_t rr[32];
+        tmem_ld_32x32b_x32(taddr + 32 * h, rr);
+        tmem_ld_wait();
+        if (h == 1) {   // the tile is in registers: hand the TMEM buffer back to the MMA warp
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) {
+            if (rank == 0) mbar_arrive(&L.tempty[acc]);
+            else mbar_arrive_cluster(&L.tempty[acc], 0);
+          }
+        }
+        const int col0 = colq + 32 * h;
+        const bool interior = (col0 + 32 <= sg.cols) && !(col0 < g0 + 32 && g0 < col0 + 32);
+        if (p.debug && p.debug < 5) {
+          if (rr[3] == 0x7fffffffu) sg.partial[0] = make_float2(0.f, 0.f);  // keep loads live
+        } else if constexpr (kMode == kSimRaw) {
+          if (row_ok) {
+            float* dst = raw_out + static_cast<size_t>(r_loc) * sg.cols;
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const uint32_t(&rr)[32] = h ? r1 : r0;
-          const int col0 = colq + 32 * h;
-          const bool fast = (col0 + 32 <= sg.cols) && !(col0 < g0 + 32 && g0 < col0 + 32);
+            for (int k = 0; k < 32; ++k)
+              if (col0 + k < sg.cols) dst[col0 + k] = __uint_as_float(rr[k]);
+          }
+        } else if constexpr (kMode == kSimStats) {
+          if (interior && warp_rows_ok && row_safe) stats_fast(rr, rstat.x, rstat.y, se2, sye2);
+          else stats_masked(rr, rstat.x, rstat.y, col0, sg.cols, gi, row_ok, se, sye, ncl);
+        } else {  // kSimQ
           uint32_t packed[16];
           const float* kc = par + 32 * h;
-          if (fast) q_chunk<false>(rr, rk, rbeta, rc, kc, kc + kPairN, kc + 2 * kPairN, col0, sg.cols, gi, packed, p.debug);
-          else q_chunk<true>(rr, rk, rbeta, rc, kc, kc + kPairN, kc + 2 * kPairN, col0, sg.cols, gi, packed, p.debug);
+          if (interior && row_safe && q_col_safe)
+            q_chunk<false>(rr, rk, rbeta, rc, kc, kc + kPairN, kc + 2 * kPairN, col0, sg.cols, gi, packed);
+          else
+            q_chunk<true>(rr, rk, rbeta, rc, kc, kc + kPairN, kc + 2 * kPairN, col0, sg.cols, gi, packed);
           if (col0 < p.ldq && p.debug != 6 && p.debug != 7) {
             // 32 rows x 64 B through 64-byte-swizzled staging -> one TMA tile store (rows past
             // the segment and columns past ldq are clipped by the tensor map)
@@ -485,9 +475,25 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kSimThreads, 1)
             }
           }
         }
+      }
+      long long tc = eprof ? clock64() : 0;
+      if constexpr (kMode == kSimStats) {
+        const float sxe = sye2.x + sye2.y + sye;   // sum y e; the table kernel divides by kappa
+        se += se2.x + se2.y;
+        if (row_ok) sg.partial[static_cast<size_t>(r_loc) * (p.n_jt * 4) + jt * 4 + cq] = make_float2(se, sxe);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) ncl += __shfl_xor_sync(0xffffffffu, ncl, o);
+        if (lane == 0 && ncl) atomicAdd(p.clamps, static_cast<unsigned long long>(ncl));
+      }
+      if constexpr (kMode == kSimQ) {
         __syncwarp();
         if (lane == 0) mbar_arrive(&L.pempty[ps]);
       }
+      if (eprof) e_math += clock64() - tc;
+    }
+    if (eprof && lane == 0 && rank == 0) {   // epilogue counters of one warp per pair
+      long long* o = p.dbg_out + (pair + 80) * 8;
+      o[0] = clock64() - e_t0; o[1] = e_wait; o[2] = e_ld; o[3] = e_math;
     }
   }
 

@@ -37,7 +37,7 @@ __global__ void fc_prep_kernel(const __nv_bfloat16* __restrict__ e1, const __nv_
   if (w >= a.B) return;
   const uint4* x4 = reinterpret_cast<const uint4*>(e1 + static_cast<size_t>(w) * a.d);
   const uint4* y4 = reinterpret_cast<const uint4*>(e2 + static_cast<size_t>(w) * a.d);
-  float acc = 0.f;
+  float acc = 0.f, n1 = 0.f, n2 = 0.f;
   for (int v = lane; v < a.d / 8; v += 32) {
     const uint4 x = __ldg(x4 + v);
     const uint4 y = __ldg(y4 + v);
@@ -49,11 +49,21 @@ __global__ void fc_prep_kernel(const __nv_bfloat16* __restrict__ e1, const __nv_
       const float2 fy = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&ys[t]));
       acc = fmaf(fx.x, fy.x, acc);
       acc = fmaf(fx.y, fy.y, acc);
+      n1 = fmaf(fx.x, fx.x, fmaf(fx.y, fx.y, n1));
+      n2 = fmaf(fy.x, fy.x, fmaf(fy.y, fy.y, n2));
     }
   }
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  for (int o = 16; o > 0; o >>= 1) {
+    acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    n1 += __shfl_xor_sync(0xffffffffu, n1, o);
+    n2 += __shfl_xor_sync(0xffffffffu, n2, o);
+  }
   if (lane != 0) return;
+  // norm bounds for the clamp-free fast paths of the similarity kernels (non-negative floats
+  // order like their bit patterns)
+  atomicMax(reinterpret_cast<int*>(a.bounds) + 0, __float_as_int(n1));
+  atomicMax(reinterpret_cast<int*>(a.bounds) + 1, __float_as_int(n2));
   a.diag[w] = acc;
   const int r = w - a.row0;
   if (r < 0 || r >= a.Bl) return;
@@ -67,8 +77,9 @@ __global__ void fc_prep_kernel(const __nv_bfloat16* __restrict__ e1, const __nv_
   }
   a.t_loc1[r] = t1;
   a.t_loc2[r] = t2;
-  a.rowstat_R[r] = make_float2(acc, static_cast<float>(kLog2eD / t1));
-  a.rowstat_C[r] = make_float2(acc, static_cast<float>(kLog2eD / t2));
+  const float k1 = static_cast<float>(kLog2eD / t1), k2 = static_cast<float>(kLog2eD / t2);
+  a.rowstat_R[r] = make_float2(k1, -acc * k1);   // y = s * kappa + beta (log2-domain exponent)
+  a.rowstat_C[r] = make_float2(k2, -acc * k2);
 }
 
 // Warp per local anchor: fixed-order (lane-strided + xor tree) reduction of the pass-1
@@ -97,8 +108,9 @@ __global__ void fc_table_kernel(StepArgs a) {
     x2 += __shfl_xor_sync(0xffffffffu, x2, o);
   }
   if (lane != 0) return;
-  a.sum1[r] = s1; a.dx1[r] = x1;
-  a.sum2[r] = s2; a.dx2[r] = x2;
+  // pass 1 accumulates sum(y e) with y = (s - S_ii) kappa: divide back by kappa
+  a.sum1[r] = s1; a.dx1[r] = x1 / static_cast<double>(a.rowstat_R[r].x);
+  a.sum2[r] = s2; a.dx2[r] = x2 / static_cast<double>(a.rowstat_C[r].x);
   const double inv = 1.0 / static_cast<double>(a.B - 1);
   const double g1 = s1 * inv;   // engine.cpp:176
   const double g2 = s2 * inv;
@@ -166,6 +178,7 @@ __device__ __forceinline__ void weights_one(const StepArgs& a, int i, double eps
   const float k2 = static_cast<float>(kLog2eD / t2);
   a.kap1[i] = k1; a.bet1[i] = -s_ii * k1; a.coef1[i] = static_cast<float>(c1);
   a.kap2[i] = k2; a.bet2[i] = -s_ii * k2; a.coef2[i] = static_cast<float>(c2);
+  atomicMax(reinterpret_cast<int*>(a.bounds) + 2, __float_as_int(fmaxf(k1, k2)));
 
   if (k == a.rank) {
     // ---- local anchor: r_i, tau-gradient terms, loss term ----

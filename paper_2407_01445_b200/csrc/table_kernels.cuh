@@ -46,6 +46,7 @@ struct StepArgs {
   float2* rowstat_R; float2* rowstat_C;   // [Bl]
   float2* partial_R; float2* partial_C;   // [Bl][n_jt*2]
   unsigned long long* clamps;
+  float* bounds;                         // {max |E1|^2, max |E2|^2, max kappa} (atomicMax on float bits)
   // per-local-anchor fp64 state of the step
   double* t_loc1; double* t_loc2;
   double* sum1; double* dx1; double* sum2; double* dx2;

@@ -22,3 +22,7 @@ for k, name in enumerate(('pass1', 'pass2')):
     print(name, 'MMA-warp cycles: total', o[:, 0].mean(), 'max', o[:, 0].max(), 'tempty', o[:, 1].mean(), 'afull', o[:, 2].mean(), 'full', o[:, 3].mean(), 'first', o[:, 4].mean())
     e0 = tl[:, 0].min()
     print('   timeline us: entry spread', (tl[:, 0].max() - e0) / 1e3, 'work_end min/max', (tl[:, 1].min() - e0) / 1e3, (tl[:, 1].max() - e0) / 1e3, 'exit max', (tl[:, 2].max() - e0) / 1e3)
+for k, name in enumerate(('pass1', 'pass2')):
+    reg = out[k * 1664:(k + 1) * 1664]
+    e = reg[:1024].reshape(128, 8)[80:80 + 48]
+    print(name, 'epilogue warp cycles: total', e[:, 0].mean(), 'wait tfull', e[:, 1].mean(), 'tmem ld', e[:, 2].mean(), 'math', e[:, 3].mean())
