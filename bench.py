@@ -272,16 +272,20 @@ def main():
 
     # ---------------- per-kernel durations: CUDA events between the step's phases ----------------
     # (event-record nodes inside the replayed graph, same stream, same inputs; K more steps)
-    step.enable_phase_timing()
+    step.enable_phase_timing(args.steps)
     for i in range(2):
         e1, e2, ids = dev_sets[i % n_sets]
         step.step(e1, e2, ids, gamma, eps, de1, de2, stream)
-    phase_sum = {k: 0.0 for k in P.fastclip.PHASES}
+    torch.cuda.synchronize()
+    step.enable_phase_timing(args.steps)   # fresh event ring: slot i <-> timed step i
     for i in range(args.steps):
         flush.zero_()
         e1, e2, ids = dev_sets[i % n_sets]
         step.step(e1, e2, ids, gamma, eps, de1, de2, stream)
-        for k, v in step.phase_times().items():
+    torch.cuda.synchronize()
+    phase_sum = {k: 0.0 for k in P.fastclip.PHASES}
+    for i in range(args.steps):
+        for k, v in step.phase_times(i).items():
             phase_sum[k] += v
     phases = {k: v / args.steps for k, v in phase_sum.items()}
     step.disable_phase_timing()

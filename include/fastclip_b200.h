@@ -141,12 +141,13 @@ int fc_table_upload(void* ctx, const double* u1, const double* u2, const double*
 int fc_tau_state_get(void* ctx, double* tau, double* m, double* v, int64_t* step, int32_t* latched);
 int fc_tau_state_set(void* ctx, double tau, double m, double v, int64_t step, int32_t latched);
 
-/* Per-phase CUDA-event timing of the step (off by default). Phases: 0 embedding all-gather,
- * 1 diag + tau^t row parameters, 2 pass-1 similarity statistics, 3 tables/weights/tau update
- * (+ scalar collectives), 4 pass-2 Q tiles, 5 gradient GEMM. fc_phase_times waits for the
- * last step and returns milliseconds per phase. */
-int fc_set_phase_timing(void* ctx, int32_t on);
-int fc_phase_times(void* ctx, float* ms, int32_t n);
+/* Per-phase CUDA-event timing of the step (off by default; slots = 0 turns it off). Phases:
+ * 0 embedding all-gather, 1 diag + tau^t row parameters, 2 pass-1 similarity statistics,
+ * 3 tables/weights/tau update (+ scalar collectives), 4 pass-2 Q tiles, 5 gradient GEMM.
+ * Steps cycle through `slots` event sets, so timed steps need no host synchronisation;
+ * fc_phase_times(slot) waits for that set (slot < 0: the last step) and returns ms per phase. */
+int fc_set_phase_timing(void* ctx, int32_t slots);
+int fc_phase_times(void* ctx, int32_t slot, float* ms, int32_t n);
 
 /* Number of CUDA kernels fc_loss_step enqueues per step (launch accounting for the bench). */
 int fc_kernels_per_step(void* ctx);

@@ -133,15 +133,16 @@ struct LossStep {
   std::vector<GraphEntry> graphs;
   // optional per-phase CUDA events (bench roofline): phases of the last step
   static constexpr int kPhases = 6;   // gatherE, prep, pass1, scalars, pass2, gemm
-  bool timing = false, ev_created = false;
-  cudaEvent_t ev[kPhases + 1]{};
+  bool timing = false;
+  int ev_slots = 0, ev_cur = 0;        // ring of per-step event sets (no host sync between steps)
+  std::vector<cudaEvent_t> ev;        // [ev_slots][kPhases + 1]
   bool debug_sync = false;
   void mark(int i, cudaStream_t st) {
     if (debug_sync) {
       cudaError_t e = cudaStreamSynchronize(st);
       std::fprintf(stderr, "[fc] phase %d reached (%s)\n", i, cudaGetErrorString(e));
     }
-    if (timing) FC_CUDA(cudaEventRecord(ev[i], st));
+    if (timing) FC_CUDA(cudaEventRecord(ev[ev_cur * (kPhases + 1) + i], st));
   }
   // cached descriptors
   const void* map_e1 = nullptr;
@@ -340,7 +341,9 @@ struct LossStep {
     }
     FC_CUDA(cudaEventRecord(done, ws));
     FC_CUDA(cudaStreamWaitEvent(caller, done, 0));
+    if (timing) ev_last = ev_cur, ev_cur = (ev_cur + 1) % ev_slots;
   }
+  int ev_last = 0;
 
   void enqueue(const fc_step_in* in, fc_step_out* out, cudaStream_t st) {
     const __nv_bfloat16* E1 = static_cast<const __nv_bfloat16*>(in->e1);
@@ -498,8 +501,8 @@ struct LossStep {
     if (ws) cudaStreamDestroy(ws);
     cudaEventDestroy(done);
     cudaEventDestroy(fork);
-    if (ev_created)
-      for (auto& e : ev) cudaEventDestroy(e);
+    for (auto& e : ev) cudaEventDestroy(e);
+    ev.clear();
   }
 };
 
@@ -705,25 +708,31 @@ int fc_tau_state_set(void* ctx, double tau, double m, double v, int64_t step, in
   });
 }
 
-int fc_set_phase_timing(void* ctx, int32_t on) {
+int fc_set_phase_timing(void* ctx, int32_t slots) {
   if (!ctx) return FC_ERR_SHAPE;
   auto* s = static_cast<LossStep*>(ctx);
   return guarded([&] {
-    if (on && !s->ev_created) {
-      for (auto& e : s->ev) FC_CUDA(cudaEventCreate(&e));
-      s->ev_created = true;
-    }
-    s->timing = on != 0;
+    FC_CUDA(cudaDeviceSynchronize());
+    for (auto& e : s->ev) cudaEventDestroy(e);
+    s->ev.clear();
+    s->ev_slots = slots > 0 ? slots : 0;
+    s->ev.resize(static_cast<size_t>(s->ev_slots) * (LossStep::kPhases + 1));
+    for (auto& e : s->ev) FC_CUDA(cudaEventCreate(&e));
+    s->ev_cur = 0;
+    s->ev_last = 0;
+    s->timing = s->ev_slots > 0;
   });
 }
 
-int fc_phase_times(void* ctx, float* ms, int32_t n) {
+int fc_phase_times(void* ctx, int32_t slot, float* ms, int32_t n) {
   if (!ctx || !ms) return FC_ERR_SHAPE;
   auto* s = static_cast<LossStep*>(ctx);
   return guarded([&] {
-    if (!s->ev_created) throw FcError{FC_ERR_CONFIG, "phase timing not enabled"};
-    FC_CUDA(cudaEventSynchronize(s->ev[LossStep::kPhases]));
-    for (int i = 0; i < n && i < LossStep::kPhases; ++i) FC_CUDA(cudaEventElapsedTime(&ms[i], s->ev[i], s->ev[i + 1]));
+    if (s->ev_slots == 0) throw FcError{FC_ERR_CONFIG, "phase timing not enabled"};
+    const int k = slot < 0 ? s->ev_last : slot % s->ev_slots;
+    cudaEvent_t* e = s->ev.data() + static_cast<size_t>(k) * (LossStep::kPhases + 1);
+    FC_CUDA(cudaEventSynchronize(e[LossStep::kPhases]));
+    for (int i = 0; i < n && i < LossStep::kPhases; ++i) FC_CUDA(cudaEventElapsedTime(&ms[i], e[i], e[i + 1]));
   });
 }
 

@@ -99,7 +99,7 @@ def lib():
         L.fc_tau_state_set.argtypes = [P, D, D, D, I64, I32]
         L.fc_kernels_per_step.argtypes = [P]
         L.fc_set_phase_timing.argtypes = [P, I32]
-        L.fc_phase_times.argtypes = [P, C.POINTER(C.c_float), I32]
+        L.fc_phase_times.argtypes = [P, I32, C.POINTER(C.c_float), I32]
         L.fc_debug_similarity.argtypes = [P, P, I32, I32, I32, P, P]
         L.fc_last_error.restype = C.c_char_p
         _lib = L
@@ -207,15 +207,15 @@ class LossStep:
         _check(lib().fc_loss_step(self._h, C.byref(sin), C.byref(sout), C.c_void_p(stream.cuda_stream)))
         return de1, de2
 
-    def enable_phase_timing(self):
-        _check(lib().fc_set_phase_timing(self._h, 1))
+    def enable_phase_timing(self, slots: int = 1):
+        _check(lib().fc_set_phase_timing(self._h, slots))
 
     def disable_phase_timing(self):
         _check(lib().fc_set_phase_timing(self._h, 0))
 
-    def phase_times(self) -> dict:
+    def phase_times(self, slot: int = -1) -> dict:
         ms = (C.c_float * len(PHASES))()
-        _check(lib().fc_phase_times(self._h, ms, len(PHASES)))
+        _check(lib().fc_phase_times(self._h, slot, ms, len(PHASES)))
         return dict(zip(PHASES, list(ms)))
 
     def scalars(self) -> StepScalars:
