@@ -14,6 +14,7 @@
 //   pass 2: tcgen05 S tiles -> bf16 Q' tiles              engine.cpp:91-118 (weights)
 //   tcgen05 GEMM Q' E -> dE1, dE2                         engine.cpp:77-121
 #include <cuda.h>
+#include <algorithm>
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
 #include <nccl.h>
@@ -112,15 +113,15 @@ struct LossStep {
   float* bounds = nullptr;
   double* f64 = nullptr;   // per-local-anchor fp64 arrays
   double *send = nullptr, *recv = nullptr, *gt_recv = nullptr, *red = nullptr, *blockpart = nullptr;
-  unsigned* counter = nullptr;
   float* par = nullptr;   // 6 x [n_jt*256]: kap1, bet1, coef1, kap2, bet2, coef2
   float* rcoef = nullptr;
   __nv_bfloat16* q = nullptr;   // [2][Bl][ldq]
   int* err = nullptr;
   fc::StepResult* result_d = nullptr;
   fc::StepResult* result_h = nullptr;   // pinned
-  cudaEvent_t done{}, fork{};
+  cudaEvent_t done{}, fork{}, side_fork{}, side_join{};
   cudaStream_t ws = nullptr;     // context stream (capturable), joined to the caller's stream
+  cudaStream_t ws2 = nullptr;    // side branch: reductions / tau updates off the critical path
   double* scal = nullptr;        // device {gamma_t, eps_t}
   bool use_graph = true;
   bool shared_q = true;          // K == 1: one Q pass, Q^T read by the dE2 GEMM
@@ -132,7 +133,9 @@ struct LossStep {
   };
   std::vector<GraphEntry> graphs;
   // optional per-phase CUDA events (bench roofline): phases of the last step
-  static constexpr int kPhases = 6;   // gatherE, prep, pass1, scalars, pass2, gemm
+  static constexpr int kPhases = 6;
+  static constexpr int kAnchorBlock = 128;   // fc_anchor_kernel: 16 anchors (8-lane groups) per block
+  static constexpr int kWeightsBlock = 64;   // fc_weights_kernel: thread per anchor, >= 80 blocks at B = 5120   // gatherE, prep, pass1, scalars, pass2, gemm
   bool timing = false;
   int ev_slots = 0, ev_cur = 0;        // ring of per-step event sets (no host sync between steps)
   std::vector<cudaEvent_t> ev;        // [ev_slots][kPhases + 1]
@@ -214,9 +217,8 @@ struct LossStep {
     recv = K > 1 ? dalloc<double>(5 * static_cast<size_t>(B)) : send;
     gt_recv = K > 1 ? dalloc<double>(2 * static_cast<size_t>(B)) : nullptr;
     red = dalloc<double>(2);
-    blockpart = dalloc<double>(3 * static_cast<size_t>((B + 255) / 256));
-    counter = dalloc<unsigned>(1);
-    FC_CUDA(cudaMemset(counter, 0, sizeof(unsigned)));
+    blockpart = dalloc<double>(3 * static_cast<size_t>(std::max((B + kWeightsBlock - 1) / kWeightsBlock,
+                                                                 (Bl * 8 + kAnchorBlock - 1) / kAnchorBlock)));
     par = dalloc<float>(6 * static_cast<size_t>(n_jt) * fc::kPairN);
     FC_CUDA(cudaMemset(par, 0, 6 * static_cast<size_t>(n_jt) * fc::kPairN * 4));
     rcoef = dalloc<float>(Bl);
@@ -229,6 +231,9 @@ struct LossStep {
     FC_CUDA(cudaEventCreateWithFlags(&done, cudaEventDisableTiming));
     FC_CUDA(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming));
     FC_CUDA(cudaStreamCreateWithFlags(&ws, cudaStreamNonBlocking));
+    FC_CUDA(cudaStreamCreateWithFlags(&ws2, cudaStreamNonBlocking));
+    FC_CUDA(cudaEventCreateWithFlags(&side_fork, cudaEventDisableTiming));
+    FC_CUDA(cudaEventCreateWithFlags(&side_join, cudaEventDisableTiming));
     scal = dalloc<double>(2);
     if (const char* e = std::getenv("FC_GRAPH")) use_graph = atoi(e) != 0;
     shared_q = K == 1;
@@ -270,6 +275,7 @@ struct LossStep {
     a.g1 = F(6); a.g2 = F(7); a.u1 = F(8); a.u2 = F(9);
     a.term_a = F(10); a.term_b = F(11); a.term_loss = F(12);
     a.gt1 = F(13); a.gt2 = F(14);   // contiguous [gt1 | gt2]
+    a.uold1 = F(15); a.uold2 = F(16);
     a.send = send; a.recv = recv;
     a.gt_recv = K > 1 ? gt_recv : F(13);
     const size_t np = static_cast<size_t>(n_jt) * fc::kPairN;
@@ -277,7 +283,6 @@ struct LossStep {
     a.kap2 = par + 3 * np; a.bet2 = par + 4 * np; a.coef2 = par + 5 * np;
     a.rcoef = rcoef;
     a.blockpart = blockpart;
-    a.counter = counter;
     a.fuse_finalize = K == 1 ? 1 : 0; a.red = red; a.err = err; a.result = result_d;
   }
 
@@ -364,7 +369,7 @@ struct LossStep {
 
     mark(1, st);
     FC_CUDA(cudaMemsetAsync(bounds, 0, 4 * sizeof(float), st));
-    fc::fc_prep_kernel<<<(B * 32 + 255) / 256, 256, 0, st>>>(E1, E2, a);
+    fc::fc_prep_kernel<<<(B * 32 + 511) / 512, 512, 0, st>>>(E1, E2, a);
     FC_CUDA(cudaGetLastError());
 
     // ---- pass 1: row statistics of S[L,G] (segment R) and S^T[L,G] (segment C) ----
@@ -393,18 +398,34 @@ struct LossStep {
 
     // ---- u table, payload, (all-gather), weights, reductions, tau update ----
     mark(3, st);
-    fc::fc_table_kernel<<<(Bl * 32 + 255) / 256, 256, 0, st>>>(a);
-    FC_CUDA(cudaGetLastError());
-    if (K > 1) FC_NCCL(ncclAllGather(send, recv, 5 * static_cast<size_t>(Bl), ncclFloat64, comm, st));
-    fc::fc_weights_kernel<<<(B + 255) / 256, 256, 0, st>>>(a);   // + reduction (+ tau step at K = 1)
-    FC_CUDA(cudaGetLastError());
-    if (K > 1) FC_NCCL(ncclAllReduce(red, red, 2, ncclFloat64, ncclSum, comm, st));
-    if (indiv) {
-      if (K > 1) FC_NCCL(ncclAllGather(a.gt1, gt_recv, 2 * static_cast<size_t>(Bl), ncclFloat64, comm, st));
-      fc::fc_indiv_update_kernel<<<(B + 255) / 256, 256, 0, st>>>(a);
+    if (K == 1) {
+      // table + weights in one kernel; the G_tau reduction, temperature step and IndividualTemp
+      // update only feed the next step and the step scalars: they run on the side branch
+      a.n_blockpart = (Bl * 8 + kAnchorBlock - 1) / kAnchorBlock;
+      fc::fc_anchor_kernel<<<a.n_blockpart, kAnchorBlock, 0, st>>>(a);
+      FC_CUDA(cudaGetLastError());
+      FC_CUDA(cudaEventRecord(side_fork, st));
+      FC_CUDA(cudaStreamWaitEvent(ws2, side_fork, 0));
+      fc::fc_reduce_kernel<<<1, 256, 0, ws2>>>(a);
+      if (indiv) fc::fc_indiv_update_kernel<<<(B + 255) / 256, 256, 0, ws2>>>(a);
+      FC_CUDA(cudaGetLastError());
+      FC_CUDA(cudaEventRecord(side_join, ws2));
+    } else {
+      fc::fc_table_kernel<<<(Bl * 8 + 255) / 256, 256, 0, st>>>(a);
+      FC_CUDA(cudaGetLastError());
+      FC_NCCL(ncclAllGather(send, recv, 5 * static_cast<size_t>(Bl), ncclFloat64, comm, st));
+      a.n_blockpart = (B + kWeightsBlock - 1) / kWeightsBlock;
+      fc::fc_weights_kernel<<<a.n_blockpart, kWeightsBlock, 0, st>>>(a);
+      fc::fc_reduce_kernel<<<1, 256, 0, st>>>(a);
+      FC_CUDA(cudaGetLastError());
+      FC_NCCL(ncclAllReduce(red, red, 2, ncclFloat64, ncclSum, comm, st));
+      if (indiv) {
+        FC_NCCL(ncclAllGather(a.gt1, gt_recv, 2 * static_cast<size_t>(Bl), ncclFloat64, comm, st));
+        fc::fc_indiv_update_kernel<<<(B + 255) / 256, 256, 0, st>>>(a);
+      }
+      fc::fc_finalize_kernel<<<1, 32, 0, st>>>(a);
+      FC_CUDA(cudaGetLastError());
     }
-    if (K > 1) fc::fc_finalize_kernel<<<1, 32, 0, st>>>(a);
-    FC_CUDA(cudaGetLastError());
 
     // ---- pass 2: Q' tiles (bf16) for both segments ----
     for (int s = 0; s < 2; ++s) {
@@ -477,19 +498,20 @@ struct LossStep {
     FC_CUDA(fc::launch_gemm(gp, mQs, mX, mO, gemm_pairs * 2, st));
     mark(6, st);
 
+    if (K == 1) FC_CUDA(cudaStreamWaitEvent(st, side_join, 0));
     FC_CUDA(cudaMemcpyAsync(result_h, result_d, sizeof(fc::StepResult), cudaMemcpyDeviceToHost, st));
   }
 
   int kernels_per_step() const {
-    return 1 /*prep*/ + 1 /*pass1*/ + 1 /*table*/ + 1 /*weights+reduce*/ + (indiv ? 1 : 0) + (K > 1 ? 1 : 0) /*finalize*/ +
-           1 /*pass2*/ + 1 /*gemm*/;
+    return 1 /*prep*/ + 1 /*pass1*/ + (K > 1 ? 2 : 1) /*table (+weights)*/ + 1 /*reduce*/ + (indiv ? 1 : 0) +
+           (K > 1 ? 1 : 0) /*finalize*/ + 1 /*pass2*/ + 1 /*gemm*/;
   }
 
   void destroy() {
     if (comm) ncclCommDestroy(comm);
     for (void* p : {(void*)u1, (void*)u2, (void*)tau1, (void*)tau2, (void*)m1, (void*)v1, (void*)m2, (void*)v2,
                     (void*)s1, (void*)s2, (void*)tau_state, (void*)e1g, (void*)e2g, (void*)diag, (void*)rowstat,
-                    (void*)partial, (void*)clamps, (void*)bounds, (void*)f64, (void*)red, (void*)par, (void*)rcoef, (void*)blockpart, (void*)counter,
+                    (void*)partial, (void*)clamps, (void*)bounds, (void*)f64, (void*)red, (void*)par, (void*)rcoef, (void*)blockpart,
                     (void*)q, (void*)err, (void*)result_d, (void*)gt_recv})
       if (p) cudaFree(p);
     if (recv && recv != send) cudaFree(recv);
@@ -499,6 +521,9 @@ struct LossStep {
     graphs.clear();
     if (scal) cudaFree(scal);
     if (ws) cudaStreamDestroy(ws);
+    if (ws2) cudaStreamDestroy(ws2);
+    cudaEventDestroy(side_fork);
+    cudaEventDestroy(side_join);
     cudaEventDestroy(done);
     cudaEventDestroy(fork);
     for (auto& e : ev) cudaEventDestroy(e);

@@ -34,11 +34,11 @@ __global__ void fc_prep_kernel(const __nv_bfloat16* __restrict__ e1, const __nv_
   const int w = (blockIdx.x * blockDim.x + threadIdx.x) / 32;
   const int lane = threadIdx.x & 31;
   if (w == 0 && lane == 0) *a.clamps = 0ull;
-  if (w >= a.B) return;
   const uint4* x4 = reinterpret_cast<const uint4*>(e1 + static_cast<size_t>(w) * a.d);
   const uint4* y4 = reinterpret_cast<const uint4*>(e2 + static_cast<size_t>(w) * a.d);
   float acc = 0.f, n1 = 0.f, n2 = 0.f;
-  for (int v = lane; v < a.d / 8; v += 32) {
+#pragma unroll 4
+  for (int v = lane; w < a.B && v < a.d / 8; v += 32) {
     const uint4 x = __ldg(x4 + v);
     const uint4 y = __ldg(y4 + v);
     const uint32_t xs[4] = {x.x, x.y, x.z, x.w};
@@ -59,17 +59,28 @@ __global__ void fc_prep_kernel(const __nv_bfloat16* __restrict__ e1, const __nv_
     n1 += __shfl_xor_sync(0xffffffffu, n1, o);
     n2 += __shfl_xor_sync(0xffffffffu, n2, o);
   }
-  if (lane != 0) return;
   // norm bounds for the clamp-free fast paths of the similarity kernels (non-negative floats
-  // order like their bit patterns)
-  atomicMax(reinterpret_cast<int*>(a.bounds) + 0, __float_as_int(n1));
-  atomicMax(reinterpret_cast<int*>(a.bounds) + 1, __float_as_int(n2));
+  // order like their bit patterns): block max first, one atomic per block
+  __shared__ float bmax[2][32];
+  const int wid = threadIdx.x >> 5;
+  if (lane == 0) { bmax[0][wid] = n1; bmax[1][wid] = n2; }
+  __syncthreads();
+  if (threadIdx.x < 2) {
+    float m = 0.f;
+    for (int k = 0; k < static_cast<int>(blockDim.x >> 5); ++k) m = fmaxf(m, bmax[threadIdx.x][k]);
+    atomicMax(reinterpret_cast<int*>(a.bounds) + threadIdx.x, __float_as_int(m));
+  }
+  if (lane != 0 || w >= a.B) return;
   a.diag[w] = acc;
   const int r = w - a.row0;
   if (r < 0 || r >= a.Bl) return;
   double t1, t2;
+  const int id = a.ids[r];
+  if (a.track_u) {   // u^{t-1} for the table kernel, off its dependent-load chain
+    a.uold1[r] = a.u1_tab[id];
+    a.uold2[r] = a.u2_tab[id];
+  }
   if (a.individual) {
-    const int id = a.ids[r];
     t1 = a.tau1_tab[id];
     t2 = a.tau2_tab[id];
   } else {
@@ -82,80 +93,67 @@ __global__ void fc_prep_kernel(const __nv_bfloat16* __restrict__ e1, const __nv_
   a.rowstat_C[r] = make_float2(k2, -acc * k2);
 }
 
-// Warp per local anchor: fixed-order (lane-strided + xor tree) reduction of the pass-1
-// partials, then g (engine.cpp:151-176), the fp64 EMA of the owned u entries (state.cpp:52-53)
-// and the snapshot (state.cpp:57-71), written straight into the all-gather payload.
-__global__ void fc_table_kernel(StepArgs a) {
-  const double gamma = a.scal[0];   // gamma_t of this step (device, so the step can be graph-replayed)
-  const int r = (blockIdx.x * blockDim.x + threadIdx.x) / 32;
-  const int lane = threadIdx.x & 31;
-  if (r >= a.Bl) return;
+// ---- per-anchor arithmetic as pure functions of register values; the kernels below do the
+// loads up front and the stores at the end, so one anchor is a single memory round trip ----
+
+// Anchors per warp of the per-anchor kernels: kGroup lanes reduce one anchor's partials, and
+// the scalar fp64 chain then runs on the group leaders, four anchors per warp instruction.
+constexpr int kGroup = 8;
+
+// Fixed-order (group-lane-strided + xor tree) reduction of one anchor's pass-1 partials; every
+// lane of the warp must call it (valid = false contributes nothing).
+__device__ __forceinline__ void reduce_partials(const StepArgs& a, int r, bool valid, int sub, double& s1,
+                                                double& x1, double& s2, double& x2) {
   const int nparts = a.n_jt * 4;
   const float2* pr = a.partial_R + static_cast<size_t>(r) * nparts;
   const float2* pc = a.partial_C + static_cast<size_t>(r) * nparts;
-  double s1 = 0.0, x1 = 0.0, s2 = 0.0, x2 = 0.0;
-  for (int q = lane; q < nparts; q += 32) {
-    const float2 u = pr[q];
-    const float2 v = pc[q];
+  s1 = 0.0; x1 = 0.0; s2 = 0.0; x2 = 0.0;
+  for (int q = sub; valid && q < nparts; q += kGroup) {
+    const float2 u = __ldg(pr + q);
+    const float2 v = __ldg(pc + q);
     s1 += u.x; x1 += u.y;
     s2 += v.x; x2 += v.y;
   }
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
+  for (int o = kGroup / 2; o > 0; o >>= 1) {
     s1 += __shfl_xor_sync(0xffffffffu, s1, o);
     x1 += __shfl_xor_sync(0xffffffffu, x1, o);
     s2 += __shfl_xor_sync(0xffffffffu, s2, o);
     x2 += __shfl_xor_sync(0xffffffffu, x2, o);
   }
-  if (lane != 0) return;
-  // pass 1 accumulates sum(y e) with y = (s - S_ii) kappa: divide back by kappa
-  a.sum1[r] = s1; a.dx1[r] = x1 / static_cast<double>(a.rowstat_R[r].x);
-  a.sum2[r] = s2; a.dx2[r] = x2 / static_cast<double>(a.rowstat_C[r].x);
+}
+
+struct TableVals {
+  double dx1, dx2, g1, g2, u1, u2;
+};
+
+// g (engine.cpp:151-176) and the fp64 EMA of the u entry (state.cpp:52-53); pass 1
+// accumulates sum(y e) with y = (s - S_ii) kappa, so dx divides kappa back out.
+__device__ __forceinline__ TableVals table_math(const StepArgs& a, double s1, double x1, double s2, double x2,
+                                                float kap_r, float kap_c, double uo1, double uo2, double gamma) {
+  TableVals v;
+  v.dx1 = x1 / static_cast<double>(kap_r);
+  v.dx2 = x2 / static_cast<double>(kap_c);
   const double inv = 1.0 / static_cast<double>(a.B - 1);
-  const double g1 = s1 * inv;   // engine.cpp:176
-  const double g2 = s2 * inv;
-  a.g1[r] = g1;
-  a.g2[r] = g2;
-  double u1 = g1, u2 = g2;      // MBCL: the "u" gathered is the current-batch g (trainer.cpp:456)
-  const int id = a.ids[r];
-  if (a.track_u) {              // state.cpp:52-53 (fp64 EMA), then snapshot (state.cpp:57-71)
-    u1 = (1.0 - gamma) * a.u1_tab[id] + gamma * g1;
-    u2 = (1.0 - gamma) * a.u2_tab[id] + gamma * g2;
-    a.u1_tab[id] = u1;
-    a.u2_tab[id] = u2;
+  v.g1 = s1 * inv;   // engine.cpp:176
+  v.g2 = s2 * inv;
+  v.u1 = v.g1;       // MBCL: the "u" gathered is the current-batch g (trainer.cpp:456)
+  v.u2 = v.g2;
+  if (a.track_u) {
+    v.u1 = (1.0 - gamma) * uo1 + gamma * v.g1;
+    v.u2 = (1.0 - gamma) * uo2 + gamma * v.g2;
   }
-  a.u1[r] = u1;
-  a.u2[r] = u2;
-  // packed payload [u1 | u2 | t1 | t2 | id] (trainer.cpp:459-487 "u-gather" + "tau-gather")
-  double* snd = a.send;
-  snd[r] = u1;
-  snd[a.Bl + r] = u2;
-  snd[2 * a.Bl + r] = a.t_loc1[r];
-  snd[3 * a.Bl + r] = a.t_loc2[r];
-  snd[4 * a.Bl + r] = static_cast<double>(id);
+  return v;
 }
 
-__device__ void block_reduce_and_finish(const StepArgs& a, double ta, double tb, double tl);
-__device__ __forceinline__ void weights_one(const StepArgs& a, int i, double eps, double& ta, double& tb,
-                                            double& tl);
+struct AnchorParams {
+  double c1, c2, t1, t2;
+  float k1, k2;
+};
 
-__global__ void fc_weights_kernel(StepArgs a) {
-  const double eps = a.scal[1];     // eps_t of this step
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  double ta = 0.0, tb = 0.0, tl = 0.0;
-  // every thread reaches the block reduction from the same place (warp-synchronous shuffles)
-  if (i < a.B) weights_one(a, i, eps, ta, tb, tl);
-  block_reduce_and_finish(a, ta, tb, tl);
-}
-
-__device__ __forceinline__ void weights_one(const StepArgs& a, int i, double eps, double& ta, double& tb,
-                                            double& tl) {
-  const int k = i / a.Bl;
-  const int r = i % a.Bl;
-  const double* blk = a.recv + static_cast<size_t>(k) * 5 * a.Bl;
-  const double u1 = blk[r], u2 = blk[a.Bl + r];
-  double t1 = blk[2 * a.Bl + r], t2 = blk[3 * a.Bl + r];
-  const double tau = a.tau_state->tau;
+// PairWeights of one anchor (engine.cpp:37-75) -> pass-2 exponent / coefficient parameters.
+__device__ __forceinline__ AnchorParams anchor_params(const StepArgs& a, double u1, double u2, double t1, double t2,
+                                                      double tau, double eps) {
   double w1, w2;
   if (a.variant == 0) {  // MBCL: weights_mbcl (engine.cpp:65-75)
     const double c = 1.0 / static_cast<double>(a.B - 1);
@@ -171,37 +169,143 @@ __device__ __forceinline__ void weights_one(const StepArgs& a, int i, double eps
     if (a.scale_by_tau) { w1 *= tau; w2 *= tau; }
     t1 = t2 = tau;
   }
-  const double c1 = w1 / t1;   // P1 coefficient: w1_a / t1_a  (engine.cpp:104,118)
-  const double c2 = w2 / t2;   // P2 coefficient: w2_a / t2_a
-  const float s_ii = a.diag[i];
-  const float k1 = static_cast<float>(kLog2eD / t1);
-  const float k2 = static_cast<float>(kLog2eD / t2);
-  a.kap1[i] = k1; a.bet1[i] = -s_ii * k1; a.coef1[i] = static_cast<float>(c1);
-  a.kap2[i] = k2; a.bet2[i] = -s_ii * k2; a.coef2[i] = static_cast<float>(c2);
-  atomicMax(reinterpret_cast<int*>(a.bounds) + 2, __float_as_int(fmaxf(k1, k2)));
+  AnchorParams p;
+  p.t1 = t1;
+  p.t2 = t2;
+  p.c1 = w1 / t1;   // P1 coefficient: w1_a / t1_a  (engine.cpp:104,118)
+  p.c2 = w2 / t2;   // P2 coefficient: w2_a / t2_a
+  p.k1 = static_cast<float>(kLog2eD / t1);
+  p.k2 = static_cast<float>(kLog2eD / t2);
+  return p;
+}
 
-  if (k == a.rank) {
-    // ---- local anchor: r_i, tau-gradient terms, loss term ----
-    a.rcoef[r] = static_cast<float>(c1 * a.sum1[r] + c2 * a.sum2[r]);
-    const double inv = 1.0 / static_cast<double>(a.B - 1);
-    const double ds1 = (-(a.dx1[r] / (t1 * t1))) * inv;   // engine.cpp:198-205
-    const double ds2 = (-(a.dx2[r] / (t2 * t2))) * inv;
-    const double g1 = a.g1[r], g2 = a.g2[r];
-    if (a.variant == 0) {
-      const double c = inv;
-      ta = ds1 / (c + g1) + ds2 / (c + g2);                 // grad_tau_mbcl (engine.cpp:261-266)
-      tl = log(c + g1) + log(c + g2);                       // eval_mbcl (losses.cpp:168-180)
-    } else if (a.individual) {
-      const double inv_n = 1.0 / static_cast<double>(a.n_train);   // engine.cpp:240-259
-      a.gt1[r] = inv_n * (log(eps + u1) + a.rho + t1 * ds1 / (eps + u1));
-      a.gt2[r] = inv_n * (log(eps + u2) + a.rho + t2 * ds2 / (eps + u2));
-      tl = t1 * (log(eps + g1) + a.rho) + t2 * (log(eps + g2) + a.rho);  // eval_rgcl
-    } else {
-      ta = ds1 / (eps + u1) + ds2 / (eps + u2);             // grad_tau_unscaled (engine.cpp:208-224)
-      tb = log(eps + u1) + log(eps + u2);                   // grad_tau_margin logs (engine.cpp:226-238)
-      tl = log(eps + g1) + log(eps + g2);                   // eval_gcl (losses.cpp:126-138)
+__device__ __forceinline__ void store_params(const StepArgs& a, int i, const AnchorParams& p, float s_ii) {
+  a.kap1[i] = p.k1; a.bet1[i] = -s_ii * p.k1; a.coef1[i] = static_cast<float>(p.c1);
+  a.kap2[i] = p.k2; a.bet2[i] = -s_ii * p.k2; a.coef2[i] = static_cast<float>(p.c2);
+}
+
+// Local anchor: tau-gradient and loss terms (engine.cpp:198-266, losses.cpp:126-180); v2 writes
+// its per-anchor tau gradients.
+__device__ __forceinline__ void local_terms(const StepArgs& a, int r, const AnchorParams& p, double u1, double u2,
+                                            double g1, double g2, double dx1, double dx2, double eps, double& ta,
+                                            double& tb, double& tl) {
+  const double t1 = p.t1, t2 = p.t2;
+  const double inv = 1.0 / static_cast<double>(a.B - 1);
+  const double ds1 = (-(dx1 / (t1 * t1))) * inv;   // engine.cpp:198-205
+  const double ds2 = (-(dx2 / (t2 * t2))) * inv;
+  if (a.variant == 0) {
+    const double c = inv;
+    ta = ds1 / (c + g1) + ds2 / (c + g2);                 // grad_tau_mbcl (engine.cpp:261-266)
+    tl = log(c + g1) + log(c + g2);                       // eval_mbcl (losses.cpp:168-180)
+  } else if (a.individual) {
+    const double inv_n = 1.0 / static_cast<double>(a.n_train);   // engine.cpp:240-259
+    a.gt1[r] = inv_n * (log(eps + u1) + a.rho + t1 * ds1 / (eps + u1));
+    a.gt2[r] = inv_n * (log(eps + u2) + a.rho + t2 * ds2 / (eps + u2));
+    tl = t1 * (log(eps + g1) + a.rho) + t2 * (log(eps + g2) + a.rho);  // eval_rgcl
+  } else {
+    ta = ds1 / (eps + u1) + ds2 / (eps + u2);             // grad_tau_unscaled (engine.cpp:208-224)
+    tb = log(eps + u1) + log(eps + u2);                   // grad_tau_margin logs (engine.cpp:226-238)
+    tl = log(eps + g1) + log(eps + g2);                   // eval_gcl (losses.cpp:126-138)
+  }
+}
+
+__device__ __forceinline__ void store_payload(const StepArgs& a, int r, int id, const TableVals& v, double t1,
+                                              double t2) {
+  if (a.track_u) {   // state.cpp:52-53 EMA, then the snapshot (state.cpp:57-71)
+    a.u1_tab[id] = v.u1;
+    a.u2_tab[id] = v.u2;
+  }
+  a.g1[r] = v.g1; a.g2[r] = v.g2;
+  a.u1[r] = v.u1; a.u2[r] = v.u2;
+  // packed payload [u1 | u2 | t1 | t2 | id] (trainer.cpp:459-487 "u-gather" + "tau-gather")
+  double* snd = a.send;
+  snd[r] = v.u1;
+  snd[a.Bl + r] = v.u2;
+  snd[2 * a.Bl + r] = t1;
+  snd[3 * a.Bl + r] = t2;
+  snd[4 * a.Bl + r] = static_cast<double>(id);
+}
+
+__device__ void block_partials(const StepArgs& a, double ta, double tb, double tl, float kmax);
+
+// K > 1, before the payload all-gather: lane group per local anchor -> g, u update, payload.
+__global__ void fc_table_kernel(StepArgs a) {
+  const int r = (blockIdx.x * blockDim.x + threadIdx.x) / kGroup;
+  const int sub = threadIdx.x % kGroup;
+  const bool valid = r < a.Bl;
+  const int rr = valid ? r : 0;
+  const double gamma = a.scal[0];
+  const int id = a.ids[rr];
+  const float kr = a.rowstat_R[rr].x, kc = a.rowstat_C[rr].x;
+  const double uo1 = a.track_u ? a.uold1[rr] : 0.0, uo2 = a.track_u ? a.uold2[rr] : 0.0;
+  const double t1 = a.t_loc1[rr], t2 = a.t_loc2[rr];
+  double s1, x1, s2, x2;
+  reduce_partials(a, rr, valid, sub, s1, x1, s2, x2);
+  if (sub != 0 || !valid) return;
+  const TableVals v = table_math(a, s1, x1, s2, x2, kr, kc, uo1, uo2, gamma);
+  a.sum1[r] = s1; a.dx1[r] = v.dx1; a.sum2[r] = s2; a.dx2[r] = v.dx2;
+  store_payload(a, r, id, v, t1, t2);
+}
+
+// K > 1, after the all-gather: thread per anchor of the global batch.
+__global__ void fc_weights_kernel(StepArgs a) {
+  const double eps = a.scal[1];     // eps_t of this step
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  double ta = 0.0, tb = 0.0, tl = 0.0;
+  float kmax = 0.f;
+  // every thread reaches the block reduction from the same place (warp-synchronous shuffles)
+  if (i < a.B) {
+    const int k = i / a.Bl;
+    const int r = i % a.Bl;
+    const double* blk = a.recv + static_cast<size_t>(k) * 5 * a.Bl;
+    const double u1 = blk[r], u2 = blk[a.Bl + r];
+    const double t1 = blk[2 * a.Bl + r], t2 = blk[3 * a.Bl + r];
+    const float s_ii = a.diag[i];
+    const AnchorParams p = anchor_params(a, u1, u2, t1, t2, a.tau_state->tau, eps);
+    store_params(a, i, p, s_ii);
+    kmax = fmaxf(p.k1, p.k2);
+    if (k == a.rank) {
+      const double s1 = a.sum1[r], s2 = a.sum2[r];
+      a.rcoef[r] = static_cast<float>(p.c1 * s1 + p.c2 * s2);
+      local_terms(a, r, p, u1, u2, a.g1[r], a.g2[r], a.dx1[r], a.dx2[r], eps, ta, tb, tl);
     }
   }
+  block_partials(a, ta, tb, tl, kmax);
+}
+
+// K = 1: no collective separates the u update from the weights, so a lane group per anchor does
+// the partial reduction, and its leader the table update, weights and local terms from
+// registers; then the per-block partial sums (reduced off the critical path by fc_reduce_kernel).
+__global__ void __launch_bounds__(128) fc_anchor_kernel(StepArgs a) {
+  const int r = (blockIdx.x * blockDim.x + threadIdx.x) / kGroup;
+  const int sub = threadIdx.x % kGroup;
+  const bool valid = r < a.Bl;
+  const int rr = valid ? r : 0;
+  double ta = 0.0, tb = 0.0, tl = 0.0;
+  float kmax = 0.f;
+  {
+    // every load of the anchor first (independent, overlapping the partial loads)
+    const double gamma = a.scal[0], eps = a.scal[1];
+    const double tau = a.tau_state->tau;
+    const int id = a.ids[rr];
+    const float kr = a.rowstat_R[rr].x, kc = a.rowstat_C[rr].x;
+    const double uo1 = a.track_u ? a.uold1[rr] : 0.0, uo2 = a.track_u ? a.uold2[rr] : 0.0;
+    const double t1 = a.t_loc1[rr], t2 = a.t_loc2[rr];
+    const float s_ii = a.diag[rr];
+    double s1, x1, s2, x2;
+    reduce_partials(a, rr, valid, sub, s1, x1, s2, x2);
+    if (sub == 0 && valid) {
+      const TableVals v = table_math(a, s1, x1, s2, x2, kr, kc, uo1, uo2, gamma);
+      const AnchorParams p = anchor_params(a, v.u1, v.u2, t1, t2, tau, eps);
+      kmax = fmaxf(p.k1, p.k2);
+      local_terms(a, r, p, v.u1, v.u2, v.g1, v.g2, v.dx1, v.dx2, eps, ta, tb, tl);
+      a.rcoef[r] = static_cast<float>(p.c1 * s1 + p.c2 * s2);
+      store_params(a, r, p, s_ii);
+      a.sum1[r] = s1; a.dx1[r] = v.dx1; a.sum2[r] = s2; a.dx2[r] = v.dx2;
+      store_payload(a, r, id, v, t1, t2);
+    }
+  }
+  block_partials(a, ta, tb, tl, kmax);
 }
 
 
@@ -246,40 +350,54 @@ __device__ void finalize_step(const StepArgs& a) {
   res->err = *a.err;
 }
 
-// Deterministic two-level reduction of the local tau-gradient / loss terms: fixed warp
-// trees into per-block partials, then the LAST block to finish (threadfence + ticket) sums
-// the partials in block order, forms G_tau,k (engine.cpp:208-238) and, when no all-reduce
-// separates them (K = 1), runs the temperature step.
-__device__ void block_reduce_and_finish(const StepArgs& a, double ta, double tb, double tl) {
+// Deterministic two-level reduction of the local tau-gradient / loss terms: fixed warp trees
+// into per-block partials here (+ the block max of kappa for the pass-2 fast path) ...
+__device__ void block_partials(const StepArgs& a, double ta, double tb, double tl, float kmax) {
   __shared__ double sh[3][32];
-  __shared__ bool last;
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  __shared__ float shk[32];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
     ta += __shfl_xor_sync(0xffffffffu, ta, o);
     tb += __shfl_xor_sync(0xffffffffu, tb, o);
     tl += __shfl_xor_sync(0xffffffffu, tl, o);
+    kmax = fmaxf(kmax, __shfl_xor_sync(0xffffffffu, kmax, o));
   }
-  if (lane == 0) { sh[0][wid] = ta; sh[1][wid] = tb; sh[2][wid] = tl; }
+  if (lane == 0) { sh[0][wid] = ta; sh[1][wid] = tb; sh[2][wid] = tl; shk[wid] = kmax; }
   __syncthreads();
   if (threadIdx.x == 0) {
     double b0 = 0.0, b1 = 0.0, b2 = 0.0;
-    for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) { b0 += sh[0][w]; b1 += sh[1][w]; b2 += sh[2][w]; }
+    float km = 0.f;
+    for (int w = 0; w < nw; ++w) { b0 += sh[0][w]; b1 += sh[1][w]; b2 += sh[2][w]; km = fmaxf(km, shk[w]); }
+    atomicMax(reinterpret_cast<int*>(a.bounds) + 2, __float_as_int(km));   // max kappa (pass-2 fast path)
     double* bp = a.blockpart + 3 * blockIdx.x;
     bp[0] = b0; bp[1] = b1; bp[2] = b2;
-    __threadfence();
-    const unsigned ticket = atomicAdd(a.counter, 1u);
-    last = ticket == gridDim.x - 1;
   }
-  __syncthreads();
-  if (!last || threadIdx.x != 0) return;
-  __threadfence();
+}
+
+// ... and the sum of the block partials in a fixed order by one block (thread t takes blocks
+// t, t + blockDim, ... then a fixed shuffle / shared-memory tree) in a separate kernel: it
+// forms G_tau,k (engine.cpp:208-238) and, when no all-reduce separates them (K = 1), runs the
+// temperature step. Nothing on the gradient path waits for it.
+__global__ void fc_reduce_kernel(StepArgs a) {
+  __shared__ double sh[3][32];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
   double s0 = 0.0, s1 = 0.0, s2 = 0.0;
-  for (unsigned b = 0; b < gridDim.x; ++b) {
-    const volatile double* bp = a.blockpart + 3 * b;
+  for (int b = threadIdx.x; b < a.n_blockpart; b += blockDim.x) {
+    const double* bp = a.blockpart + 3 * b;
     s0 += bp[0]; s1 += bp[1]; s2 += bp[2];
   }
-  *a.counter = 0u;   // re-arm for the next step
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    s0 += __shfl_xor_sync(0xffffffffu, s0, o);
+    s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+    s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+  }
+  if (lane == 0) { sh[0][wid] = s0; sh[1][wid] = s1; sh[2][wid] = s2; }
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  s0 = 0.0; s1 = 0.0; s2 = 0.0;
+  for (int w = 0; w < nw; ++w) { s0 += sh[0][w]; s1 += sh[1][w]; s2 += sh[2][w]; }
   const double bl = static_cast<double>(a.Bl);
   const double unscaled = s0 / bl;
   double gtl = unscaled;                                                   // v0 / MBCL

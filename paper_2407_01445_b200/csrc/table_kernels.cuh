@@ -53,6 +53,7 @@ struct StepArgs {
   double* g1; double* g2; double* u1; double* u2;
   double* term_a; double* term_b; double* term_loss;
   double* gt1; double* gt2;              // v2 tau gradients, contiguous [gt1 | gt2] (send)
+  double* uold1; double* uold2;          // u^{t-1} of the local ids, gathered by the prep kernel
   double* send;                          // [5][Bl] packed payload
   const double* recv;                    // [K][5][Bl] (== send when K == 1)
   const double* gt_recv;                 // [K][2][Bl] (== gt1 when K == 1)
@@ -63,8 +64,8 @@ struct StepArgs {
   float* rcoef;                          // [Bl]
   double* red;                           // [2] local G_tau, loss numerator (all-reduced)
   double* blockpart;                     // [grid][3] per-block partial sums (weights kernel)
-  unsigned* counter;                     // last-block ticket
-  int fuse_finalize;                     // K == 1: temperature step in the weights kernel
+  int n_blockpart;                       // blocks of the kernel that wrote blockpart
+  int fuse_finalize;                     // K == 1: temperature step in the reduce kernel
   int* err;
   StepResult* result;
 };
@@ -73,6 +74,8 @@ __global__ void fc_prep_kernel(const __nv_bfloat16* __restrict__ e1, const __nv_
                                StepArgs a);
 __global__ void fc_table_kernel(StepArgs a);
 __global__ void fc_weights_kernel(StepArgs a);
+__global__ void fc_anchor_kernel(StepArgs a);
+__global__ void fc_reduce_kernel(StepArgs a);
 __global__ void fc_finalize_kernel(StepArgs a);
 __global__ void fc_indiv_update_kernel(StepArgs a);
 

@@ -26,3 +26,18 @@ for k, name in enumerate(('pass1', 'pass2')):
     reg = out[k * 1664:(k + 1) * 1664]
     e = reg[:1024].reshape(128, 8)[80:80 + 48]
     print(name, 'epilogue warp cycles: total', e[:, 0].mean(), 'wait tfull', e[:, 1].mean(), 'tmem ld', e[:, 2].mean(), 'math', e[:, 3].mean())
+for k, name in enumerate(('pass1', 'pass2')):
+    reg = out[k * 1664:(k + 1) * 1664]
+    tl = reg[1024:].reshape(160, 4)[:148]
+    print('zero-entry CTAs', np.nonzero(tl[:, 0] == 0)[0][:10], 'nonzero', (tl[:, 0] != 0).sum())
+    tl = tl[(tl[:, 0] > 10**17) & (tl[:, 1] > 10**17)]   # rows 0-25 overlap the epilogue-counter region
+    e0 = tl[:, 0].min()
+    tl = (tl - e0).astype(np.float64)
+    e0 = 0
+    ent = np.sort((tl[:, 0] - e0) / 1e3); we = np.sort((tl[:, 1] - e0) / 1e3)
+    print(name, 'entry pct', np.round(ent[np.linspace(0, len(ent) - 1, 5).astype(int)], 2), 'work_end pct', np.round(we[np.linspace(0, len(we) - 1, 5).astype(int)], 2))
+st.enable_phase_timing(5)
+for _ in range(5): st.step(e1, e2, ids, 0.6, 1e-14)
+torch.cuda.synchronize()
+print('phases (debug9 build)', {k: round(v * 1e3, 1) for k, v in st.phase_times(4).items()})
+
