@@ -25,8 +25,8 @@ constexpr int kSimStagesQ = 3;       // B ring depth, Q pass (smem goes to the Q
 constexpr int kSimStageOutQ = 32 * 64;   // per epilogue warp: 32 rows x 32 bf16 (64-byte swizzled rows)
 constexpr int kSimEpiWarps = 16;   // 4 per TMEM lane quarter, 64 columns each
 constexpr int kSimThreads = (2 + kSimEpiWarps) * 32;
-constexpr int kSimPSlots = 3;      // column-parameter slots (Q pass): kappa, beta, coef x 256
-constexpr int kSimPSlotBytes = 3 * kPairN * 4;
+constexpr int kSimPSlots = 3;      // column-parameter slots (Q pass): kappa, beta, coef, fac x 256
+constexpr int kSimPSlotBytes = 4 * kPairN * 4;   // kappa, beta, coef, fac
 constexpr int kSimSmemStats = kSimASlots * kStageBytesA + kSimStagesStats * kStageBytesB + kSimPSlots * kSimPSlotBytes;
 constexpr int kSimSmemQ = kSimASlots * kStageBytesA + kSimStagesQ * kStageBytesB + kSimPSlots * kSimPSlotBytes +
                           kSimEpiWarps * kSimStageOutQ;
@@ -50,6 +50,8 @@ struct SimSeg {
   // Q: exponent y = s*kappa + beta (= (s - S_aa) log2(e)/t_a), weight coef (SoA, fp32)
   const float* row_kappa; const float* row_beta; const float* row_coef;   // [rows]
   const float* col_kappa; const float* col_beta; const float* col_coef;   // [n_jt*256], zero padded
+  // Q, global temperature: fac_a = coef_a 2^beta_a, so Q'_ij = 2^(s kappa) (fac_i + fac_j)
+  const float* row_fac; const float* col_fac;
   __nv_bfloat16* q;         // Q: [rows][ldq]
 };
 struct SimParams {
@@ -62,6 +64,7 @@ struct SimParams {
   int n_items;
   unsigned long long* clamps;  // STATS: exponent clamps (safe_exp, losses.cpp:22-28)
   const float* bounds;         // {max |E1_i|^2, max |E2_j|^2, max kappa over G}: clamp-free fast paths
+  int q_factor;                // Q: one shared temperature -> factorized single-exponential fast path
   int debug;                   // perf experiments: 1 = skip epilogue math, 2 = also skip B loads
   long long* dbg_out;          // debug == 9: per-pair MMA-warp cycle counters [pair][8]
 };

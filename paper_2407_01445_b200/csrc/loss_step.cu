@@ -126,6 +126,7 @@ struct LossStep {
   bool use_graph = true;
   bool shared_q = true;          // K == 1: one Q pass, Q^T read by the dE2 GEMM
   int sim_debug = 0, gemm_debug = 0;
+  bool q_factor = true;          // FC_Q_FACTOR=0 forces the two-exponential Q path (A/B checks)
   long long* dbg_buf = nullptr;   // FC_SIM_DEBUG=9 MMA-warp counters: [launch 0: pass 1, 1: pass 2][pair][8]             // FC_SIM_DEBUG perf experiments (results invalid when set)
   struct GraphEntry {
     const void* key[5];
@@ -219,8 +220,8 @@ struct LossStep {
     red = dalloc<double>(2);
     blockpart = dalloc<double>(3 * static_cast<size_t>(std::max((B + kWeightsBlock - 1) / kWeightsBlock,
                                                                  (Bl * 8 + kAnchorBlock - 1) / kAnchorBlock)));
-    par = dalloc<float>(6 * static_cast<size_t>(n_jt) * fc::kPairN);
-    FC_CUDA(cudaMemset(par, 0, 6 * static_cast<size_t>(n_jt) * fc::kPairN * 4));
+    par = dalloc<float>(8 * static_cast<size_t>(n_jt) * fc::kPairN);
+    FC_CUDA(cudaMemset(par, 0, 8 * static_cast<size_t>(n_jt) * fc::kPairN * 4));
     rcoef = dalloc<float>(Bl);
     q = dalloc<__nv_bfloat16>(2 * static_cast<size_t>(Bl) * ldq);
     err = dalloc<int>(1);
@@ -239,7 +240,8 @@ struct LossStep {
     shared_q = K == 1;
     if (const char* e = std::getenv("FC_DEBUG_SYNC")) debug_sync = atoi(e) != 0;
     if (const char* e = std::getenv("FC_SIM_DEBUG")) sim_debug = atoi(e);
-    if (sim_debug == 9) dbg_buf = dalloc<long long>(2 * 1664);
+    if (const char* e = std::getenv("FC_Q_FACTOR")) q_factor = atoi(e) != 0;
+    if (sim_debug == 9) dbg_buf = dalloc<long long>(2 * 2688);
     if (const char* e = std::getenv("FC_GEMM_DEBUG")) gemm_debug = atoi(e);
     if (debug_sync) use_graph = false;
     if (const char* e = std::getenv("FC_SHARED_Q")) shared_q = shared_q && atoi(e) != 0;
@@ -281,6 +283,7 @@ struct LossStep {
     const size_t np = static_cast<size_t>(n_jt) * fc::kPairN;
     a.kap1 = par; a.bet1 = par + np; a.coef1 = par + 2 * np;
     a.kap2 = par + 3 * np; a.bet2 = par + 4 * np; a.coef2 = par + 5 * np;
+    a.fac1 = par + 6 * np; a.fac2 = par + 7 * np;
     a.rcoef = rcoef;
     a.blockpart = blockpart;
     a.fuse_finalize = K == 1 ? 1 : 0; a.red = red; a.err = err; a.result = result_d;
@@ -406,7 +409,7 @@ struct LossStep {
       FC_CUDA(cudaGetLastError());
       FC_CUDA(cudaEventRecord(side_fork, st));
       FC_CUDA(cudaStreamWaitEvent(ws2, side_fork, 0));
-      fc::fc_reduce_kernel<<<1, 256, 0, ws2>>>(a);
+      fc::fc_reduce_kernel<<<1, 32, 0, ws2>>>(a);
       if (indiv) fc::fc_indiv_update_kernel<<<(B + 255) / 256, 256, 0, ws2>>>(a);
       FC_CUDA(cudaGetLastError());
       FC_CUDA(cudaEventRecord(side_join, ws2));
@@ -416,7 +419,7 @@ struct LossStep {
       FC_NCCL(ncclAllGather(send, recv, 5 * static_cast<size_t>(Bl), ncclFloat64, comm, st));
       a.n_blockpart = (B + kWeightsBlock - 1) / kWeightsBlock;
       fc::fc_weights_kernel<<<a.n_blockpart, kWeightsBlock, 0, st>>>(a);
-      fc::fc_reduce_kernel<<<1, 256, 0, st>>>(a);
+      fc::fc_reduce_kernel<<<1, 32, 0, st>>>(a);
       FC_CUDA(cudaGetLastError());
       FC_NCCL(ncclAllReduce(red, red, 2, ncclFloat64, ncclSum, comm, st));
       if (indiv) {
@@ -439,6 +442,8 @@ struct LossStep {
       g.col_kappa = s ? a.kap1 : a.kap2;
       g.col_beta = s ? a.bet1 : a.bet2;
       g.col_coef = s ? a.coef1 : a.coef2;
+      g.row_fac = (s ? a.fac2 : a.fac1) + off;
+      g.col_fac = s ? a.fac1 : a.fac2;
       g.q = q + static_cast<size_t>(s) * Bl * ldq;
     }
     mark(4, st);
@@ -447,7 +452,8 @@ struct LossStep {
       sp.n_rb[1] = 0;
       sp.n_items = sp.n_rb[0] * n_jt;
     }
-    if (sim_debug == 9) sp.dbg_out = dbg_buf + 1664;   // pass-2 counters / timelines
+    if (sim_debug == 9) sp.dbg_out = dbg_buf + 2688;
+    sp.q_factor = (!indiv && q_factor) ? 1 : 0;   // one shared temperature: single-exponential Q   // pass-2 counters / timelines
     FC_CUDA(fc::launch_sim(fc::kSimQ, sp, mA, mB, mQo, pair_grid(sp.n_items), st, nullptr));
 
     // ---- pass 2b: dE = c (Q' E - r o E_local) ----
@@ -766,7 +772,7 @@ int fc_debug_counters(void* ctx, long long* out /* host [2*128*8] */) {
   auto* s = static_cast<LossStep*>(ctx);
   return guarded([&] {
     FC_CUDA(cudaDeviceSynchronize());
-    if (s->dbg_buf) FC_CUDA(cudaMemcpy(out, s->dbg_buf, 2 * 1664 * 8, cudaMemcpyDeviceToHost));
+    if (s->dbg_buf) FC_CUDA(cudaMemcpy(out, s->dbg_buf, 2 * 2688 * 8, cudaMemcpyDeviceToHost));
   });
 }
 

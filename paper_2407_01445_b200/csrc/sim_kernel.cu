@@ -26,7 +26,7 @@ constexpr float kClampLog2 = 60.0f * 1.4426950408889634f;  // kExpClampMax in th
 struct SmemLayout {
   uint8_t* a;          // kSimASlots x 16 KB: resident anchor rows (one K block per slot)
   uint8_t* b;          // kStagesB x 16 KB: streamed contrast rows
-  float* par;          // kSimPSlots x {kappa[256], beta[256], coef[256]} (Q pass)
+  float* par;          // kSimPSlots x {kappa[256], beta[256], coef[256], fac[256]} (Q pass)
   uint8_t* qout;       // kSimEpiWarps x 2 KB: Q store staging (Q pass)
   uint64_t* full;      // B ring
   uint64_t* empty;
@@ -118,6 +118,28 @@ __device__ __forceinline__ void stats_masked(const uint32_t (&r)[32], float kap,
     se += ok ? e : 0.f;
     sye += ok ? y * e : 0.f;
     ncl += (ok && y > kClampLog2) ? 1u : 0u;
+  }
+}
+
+// Q with one temperature for every anchor (kappa_i = kappa_j): the two exponentials share
+// 2^(s kappa), so Q'_ij = 2^(s kappa) (fac_i + fac_j) with fac_a = coef_a 2^beta_a -- one
+// MUFU ex2 per element instead of two (pass 2 is otherwise SFU-bound at the MMA rate).
+constexpr float kFactMaxLog2 = 63.0f;
+__device__ __forceinline__ void q_chunk_fact(const uint32_t (&r)[32], float rk, float rf, const float* fc,
+                                             uint32_t (&packed)[16]) {
+  const float2 rk2 = f2(rk, rk), rf2 = f2(rf, rf);
+#pragma unroll
+  for (int k = 0; k < 32; k += 4) {
+    const float4 ff = *reinterpret_cast<const float4*>(fc + k);
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const float2 s = f2(__uint_as_float(r[k + 2 * h]), __uint_as_float(r[k + 2 * h + 1]));
+      const float2 y = __fmul2_rn(s, rk2);
+      const float2 e = f2(ex2_approx(y.x), ex2_approx(y.y));
+      const float2 q = __fmul2_rn(e, __fadd2_rn(rf2, h ? f2(ff.z, ff.w) : f2(ff.x, ff.y)));
+      __nv_bfloat162 hq = __floats2bfloat162_rn(q.x, q.y);
+      packed[k / 2 + h] = *reinterpret_cast<uint32_t*>(&hq);
+    }
   }
 }
 
@@ -229,7 +251,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kSimThreads, 1)
     {
       const bool issuer = lane == 0;
       uint32_t stage = 0, phase = 0;
-      uint32_t sgen[kSimASlots] = {};   // per-slot load generation (phase parity of afull/aempty)
+      uint32_t spar = 0;   // bit per A slot: parity of its load generation (afull/aempty phase), kept in a register
       int cur_key = -1;
       int it = 0;
       for (int item = it_lo; item < it_hi; ++item, ++it) {
@@ -250,6 +272,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kSimThreads, 1)
             bulk_load(dst, sg.col_kappa + jt * kPairN, kPairN * 4, &L.pfull[ps]);
             bulk_load(dst + kPairN, sg.col_beta + jt * kPairN, kPairN * 4, &L.pfull[ps]);
             bulk_load(dst + 2 * kPairN, sg.col_coef + jt * kPairN, kPairN * 4, &L.pfull[ps]);
+            bulk_load(dst + 3 * kPairN, sg.col_fac + jt * kPairN, kPairN * 4, &L.pfull[ps]);
           }
           __syncwarp();
         }
@@ -260,8 +283,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kSimThreads, 1)
           if (key != cur_key) {
             for (int kb = kb_lo; kb < kb_hi; ++kb) {
               const int slot = kb - kb_lo;
-              mbar_wait(&L.aempty[slot], (sgen[slot] & 1) ^ 1);
-              ++sgen[slot];
+              mbar_wait(&L.aempty[slot], ((spar >> slot) & 1) ^ 1);
+              spar ^= 1u << slot;
               if (issuer) {
                 if (rank == 0) mbar_arrive_expect_tx(&L.afull[slot], 2 * kStageBytesA);
                 else mbar_arrive_cluster(&L.afull[slot], 0);
@@ -299,7 +322,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kSimThreads, 1)
       const uint64_t a_desc0 = make_sdesc_sw128(smem_u32(L.a), 0, 1024);
       const uint64_t b_desc0 = make_sdesc_sw128(smem_u32(L.b), 0, 1024);
       uint32_t stage = 0, phase = 0;
-      uint32_t sgen[kSimASlots] = {};
+      uint32_t spar = 0;   // bit per A slot: parity of the generation being consumed + 1
       uint32_t ready = 0;   // bit per A slot: afull of the current generation observed
       int cur_key = -1;
       int it = 0;
@@ -320,7 +343,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kSimThreads, 1)
           if (key != cur_key) {
             cur_key = key;
             ready = 0;
-            for (int kb = kb_lo; kb < kb_hi; ++kb) ++sgen[kb - kb_lo];
+            spar ^= (1u << (kb_hi - kb_lo)) - 1u;
           }
           // last use of this A generation: release each slot right after its MMAs
           int nxt_key = -2;
@@ -332,7 +355,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kSimThreads, 1)
             const int slot = kb - kb_lo;
             if (!(ready & (1u << slot))) {
               long long t1 = prof ? clock64() : 0;
-              mbar_wait(&L.afull[slot], (sgen[slot] - 1) & 1);
+              mbar_wait(&L.afull[slot], ((spar >> slot) & 1) ^ 1);
               if (prof) c_afull += clock64() - t1;
               ready |= 1u << slot;
             }
@@ -364,13 +387,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kSimThreads, 1)
         long long* o = p.dbg_out + pair * 8;
         o[0] = clock64() - c_start; o[1] = c_tempty; o[2] = c_afull; o[3] = c_full; o[4] = c_first; o[5] = n_mma;
         o[6] = it_hi - it_lo;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(o[7]));   // MMA loop end (ns)
       }
     }
   } else {
     // ===================== epilogue (both CTAs) =====================
     const uint32_t q4 = warp & 3;               // TMEM lane quarter accessible to this warp
-    long long e_wait = 0, e_ld = 0, e_math = 0, e_t0 = clock64();
+    long long e_wait = 0, e_ld = 0, e_math = 0, e_t0 = clock64(), e_g0 = 0;
     const bool eprof = p.debug == 9 && warp == 5;
+    if (eprof) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(e_g0));
     const uint32_t cq = warp >> 2;        // 64-column quarter of the 256-wide tile
     int it = 0;
     for (int item = it_lo; item < it_hi; ++item, ++it) {
@@ -388,13 +413,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kSimThreads, 1)
       const int colq = jt * kPairN + static_cast<int>(cq) * 64;
 
       float2 rstat = make_float2(0.f, 0.f);
-      float rk = 0.f, rbeta = 0.f, rc = 0.f;
+      float rk = 0.f, rbeta = 0.f, rc = 0.f, rf = 0.f;
       if (row_ok) {
         if constexpr (kMode == kSimStats) rstat = sg.row_stat[r_loc];
         if constexpr (kMode == kSimQ) {
           rk = sg.row_kappa[r_loc];
           rbeta = sg.row_beta[r_loc];
           rc = sg.row_coef[r_loc];
+          rf = sg.row_fac[r_loc];
         }
       }
 
@@ -411,12 +437,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kSimThreads, 1)
       uint32_t ncl = 0;
       int ps = 0;
       const float* par = nullptr;
-      bool q_col_safe = false;
+      bool q_col_safe = false, q_fact = false;
       if constexpr (kMode == kSimQ) {
         ps = it % kSimPSlots;
         mbar_wait(&L.pfull[ps], (it / kSimPSlots) & 1);
         par = L.par + ps * (kSimPSlotBytes / 4) + cq * 64;
         q_col_safe = 2.f * smax * p.bounds[2] <= kClampLog2;
+        // factorized form: 2^(s kappa) stays within [2^-63, 2^63] and fac within fp32 range
+        q_fact = p.q_factor && __all_sync(0xffffffffu, rk * smax <= kFactMaxLog2);
       }
       const float row_kap = kMode == kSimQ ? rk : rstat.x;
       const float row_beta = kMode == kSimQ ? rbeta : rstat.y;
@@ -451,7 +479,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kSimThreads, 1)
         } else {  // kSimQ
           uint32_t packed[16];
           const float* kc = par + 32 * h;
-          if (interior && row_safe && q_col_safe)
+          if (interior && row_safe && q_col_safe && q_fact)
+            q_chunk_fact(rr, rk, rf, kc + 3 * kPairN, packed);
+          else if (interior && row_safe && q_col_safe)
             q_chunk<false>(rr, rk, rbeta, rc, kc, kc + kPairN, kc + 2 * kPairN, col0, sg.cols, gi, packed);
           else
             q_chunk<true>(rr, rk, rbeta, rc, kc, kc + kPairN, kc + 2 * kPairN, col0, sg.cols, gi, packed);
@@ -492,8 +522,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kSimThreads, 1)
       if (eprof) e_math += clock64() - tc;
     }
     if (eprof && lane == 0 && rank == 0) {   // epilogue counters of one warp per pair
-      long long* o = p.dbg_out + (pair + 80) * 8;
+      long long* o = p.dbg_out + 1024 + pair * 8;
       o[0] = clock64() - e_t0; o[1] = e_wait; o[2] = e_ld; o[3] = e_math;
+      o[4] = e_g0;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(o[5]));   // epilogue loop end (ns)
     }
   }
 
@@ -509,7 +541,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kSimThreads, 1)
   if (p.debug == 9 && threadIdx.x == 0) {
     long long g_exit;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_exit));
-    long long* o = p.dbg_out + 1024 + blockIdx.x * 4;   // per-CTA timeline (ns)
+    long long* o = p.dbg_out + 2048 + blockIdx.x * 4;   // per-CTA timeline (ns)
     o[0] = g_entry; o[1] = g_work_end; o[2] = g_exit;
   }
 }

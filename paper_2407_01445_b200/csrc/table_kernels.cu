@@ -180,8 +180,10 @@ __device__ __forceinline__ AnchorParams anchor_params(const StepArgs& a, double 
 }
 
 __device__ __forceinline__ void store_params(const StepArgs& a, int i, const AnchorParams& p, float s_ii) {
-  a.kap1[i] = p.k1; a.bet1[i] = -s_ii * p.k1; a.coef1[i] = static_cast<float>(p.c1);
-  a.kap2[i] = p.k2; a.bet2[i] = -s_ii * p.k2; a.coef2[i] = static_cast<float>(p.c2);
+  const float b1 = -s_ii * p.k1, b2 = -s_ii * p.k2;
+  const float c1 = static_cast<float>(p.c1), c2 = static_cast<float>(p.c2);
+  a.kap1[i] = p.k1; a.bet1[i] = b1; a.coef1[i] = c1; a.fac1[i] = c1 * exp2f(b1);
+  a.kap2[i] = p.k2; a.bet2[i] = b2; a.coef2[i] = c2; a.fac2[i] = c2 * exp2f(b2);
 }
 
 // Local anchor: tau-gradient and loss terms (engine.cpp:198-266, losses.cpp:126-180); v2 writes
@@ -375,15 +377,14 @@ __device__ void block_partials(const StepArgs& a, double ta, double tb, double t
   }
 }
 
-// ... and the sum of the block partials in a fixed order by one block (thread t takes blocks
-// t, t + blockDim, ... then a fixed shuffle / shared-memory tree) in a separate kernel: it
-// forms G_tau,k (engine.cpp:208-238) and, when no all-reduce separates them (K = 1), runs the
-// temperature step. Nothing on the gradient path waits for it.
-__global__ void fc_reduce_kernel(StepArgs a) {
-  __shared__ double sh[3][32];
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+// ... and the sum of the block partials in a fixed order by ONE WARP (lane t takes blocks
+// t, t + 32, ... then a fixed xor tree) in a separate kernel: it forms G_tau,k
+// (engine.cpp:208-238) and, when no all-reduce separates them (K = 1), runs the temperature
+// step. Nothing on the gradient path waits for it; a single warp without shared memory fits
+// beside a persistent similarity CTA, so it never delays the pass-2 launch.
+__global__ void __launch_bounds__(32) fc_reduce_kernel(StepArgs a) {
   double s0 = 0.0, s1 = 0.0, s2 = 0.0;
-  for (int b = threadIdx.x; b < a.n_blockpart; b += blockDim.x) {
+  for (int b = threadIdx.x; b < a.n_blockpart; b += 32) {
     const double* bp = a.blockpart + 3 * b;
     s0 += bp[0]; s1 += bp[1]; s2 += bp[2];
   }
@@ -393,11 +394,7 @@ __global__ void fc_reduce_kernel(StepArgs a) {
     s1 += __shfl_xor_sync(0xffffffffu, s1, o);
     s2 += __shfl_xor_sync(0xffffffffu, s2, o);
   }
-  if (lane == 0) { sh[0][wid] = s0; sh[1][wid] = s1; sh[2][wid] = s2; }
-  __syncthreads();
   if (threadIdx.x != 0) return;
-  s0 = 0.0; s1 = 0.0; s2 = 0.0;
-  for (int w = 0; w < nw; ++w) { s0 += sh[0][w]; s1 += sh[1][w]; s2 += sh[2][w]; }
   const double bl = static_cast<double>(a.Bl);
   const double unscaled = s0 / bl;
   double gtl = unscaled;                                                   // v0 / MBCL

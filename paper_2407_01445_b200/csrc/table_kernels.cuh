@@ -61,6 +61,7 @@ struct StepArgs {
   // per-anchor exponent parameters y = s*kappa + beta and weights coef (SoA, [n_jt*256])
   float* kap1; float* bet1; float* coef1;   // track 1: kappa = log2e/t1, coef = w1/t1
   float* kap2; float* bet2; float* coef2;   // track 2: kappa = log2e/t2, coef = w2/t2
+  float* fac1; float* fac2;                 // coef * 2^beta (factorized pass 2, one shared temperature)
   float* rcoef;                          // [Bl]
   double* red;                           // [2] local G_tau, loss numerator (all-reduced)
   double* blockpart;                     // [grid][3] per-block partial sums (weights kernel)

@@ -1,3 +1,4 @@
+"""FC_SIM_DEBUG=9 counters of the similarity kernels (diagnostics; results of the step are valid)."""
 import ctypes as C, os, sys, numpy as np, torch
 sys.path.insert(0, '.')
 os.environ['FC_SIM_DEBUG'] = '9'
@@ -13,31 +14,21 @@ e2 = torch.from_numpy(b2.view(np.int16)).cuda().view(torch.bfloat16)
 ids = torch.from_numpy(S.ids(B, N, 0)).cuda()
 for _ in range(3): st.step(e1, e2, ids, 0.6, 1e-14)
 torch.cuda.synchronize()
-out = np.zeros(2 * 1664, dtype=np.int64)
+R = 2688
+out = np.zeros(2 * R, dtype=np.int64)
 P.lib().fc_debug_counters(st._h, out.ctypes.data_as(C.POINTER(C.c_longlong)))
 for k, name in enumerate(('pass1', 'pass2')):
-    reg = out[k * 1664:(k + 1) * 1664]
+    reg = out[k * R:(k + 1) * R]
     o = reg[:1024].reshape(128, 8)[:74]
-    tl = reg[1024:].reshape(160, 4)[:148]
-    print(name, 'MMA-warp cycles: total', o[:, 0].mean(), 'max', o[:, 0].max(), 'tempty', o[:, 1].mean(), 'afull', o[:, 2].mean(), 'full', o[:, 3].mean(), 'first', o[:, 4].mean())
-    e0 = tl[:, 0].min()
-    print('   timeline us: entry spread', (tl[:, 0].max() - e0) / 1e3, 'work_end min/max', (tl[:, 1].min() - e0) / 1e3, (tl[:, 1].max() - e0) / 1e3, 'exit max', (tl[:, 2].max() - e0) / 1e3)
-for k, name in enumerate(('pass1', 'pass2')):
-    reg = out[k * 1664:(k + 1) * 1664]
-    e = reg[:1024].reshape(128, 8)[80:80 + 48]
-    print(name, 'epilogue warp cycles: total', e[:, 0].mean(), 'wait tfull', e[:, 1].mean(), 'tmem ld', e[:, 2].mean(), 'math', e[:, 3].mean())
-for k, name in enumerate(('pass1', 'pass2')):
-    reg = out[k * 1664:(k + 1) * 1664]
-    tl = reg[1024:].reshape(160, 4)[:148]
-    print('zero-entry CTAs', np.nonzero(tl[:, 0] == 0)[0][:10], 'nonzero', (tl[:, 0] != 0).sum())
-    tl = tl[(tl[:, 0] > 10**17) & (tl[:, 1] > 10**17)]   # rows 0-25 overlap the epilogue-counter region
-    e0 = tl[:, 0].min()
-    tl = (tl - e0).astype(np.float64)
-    e0 = 0
-    ent = np.sort((tl[:, 0] - e0) / 1e3); we = np.sort((tl[:, 1] - e0) / 1e3)
-    print(name, 'entry pct', np.round(ent[np.linspace(0, len(ent) - 1, 5).astype(int)], 2), 'work_end pct', np.round(we[np.linspace(0, len(we) - 1, 5).astype(int)], 2))
+    e = reg[1024:2048].reshape(128, 8)[:74]
+    tl = reg[2048:].reshape(160, 4)[:148]
+    t0 = tl[:, 0].min()
+    us = lambda x: np.round(np.percentile((x - t0) / 1e3, [0, 50, 100]), 2)
+    print(f'{name}: MMA-warp cycles total {o[:, 0].mean():.0f} (max {o[:, 0].max()}) waits: tempty {o[:, 1].mean():.0f} afull {o[:, 2].mean():.0f} full {o[:, 3].mean():.0f} first-MMA {o[:, 4].mean():.0f}; items {o[:, 6].min()}-{o[:, 6].max()}')
+    print(f'   epilogue warp cycles total {e[:, 0].mean():.0f} wait tfull {e[:, 1].mean():.0f} math {e[:, 3].mean():.0f}')
+    print('   timeline us [min, median, max] from first CTA entry: entry', us(tl[:, 0]), 'epi start', us(e[:, 4]),
+          'MMA end', us(o[:, 7]), 'epi end', us(e[:, 5]), 'work end', us(tl[:, 1]), 'exit', us(tl[:, 2]))
 st.enable_phase_timing(5)
 for _ in range(5): st.step(e1, e2, ids, 0.6, 1e-14)
 torch.cuda.synchronize()
 print('phases (debug9 build)', {k: round(v * 1e3, 1) for k, v in st.phase_times(4).items()})
-
