@@ -4,13 +4,20 @@
 // (engine.cpp:77-121 regrouped: Q[i,j] = P1[i,j] + P2[j,i], r_i = a_i S1_i + b_i S2_i,
 //  c = 1/(Bl (B-1))). A = Q' (bf16, K-major, written by the Q pass; at K = 1 the dE2 GEMM
 // reads Q^T through an MN-major A operand), B = E (bf16, N = d contiguous => MN-major UMMA
-// operand), fp32 accumulation in TMEM, CTA pairs (cta_group::2, 256 x 256 pair tiles).
+// operand), fp32 accumulation in TMEM.
 //
-// Schedule (hybrid data-parallel + stream-K): the first floor(T/P)*P tiles are processed
-// whole, one tile per pair per round, and stored directly; the k-blocks of the remaining
-// T mod P tiles are split evenly over all P pairs (contiguous k ranges) and reduced with
-// vector fp32 atomics into a pre-zeroed output. Every pair therefore runs the same number
-// of k-blocks (+-1) whatever T is.
+// The GEMM is skinny (N = d = 512, K = B = 5120) and both operands stream, so its limit is
+// the L2 -> SM operand bandwidth, not the tensor pipe: a 256 x 256 pair tile moves 64 KB per
+// 512 MMA cycles, ~1.5x what the L2 slices deliver chip-wide. This kernel therefore
+//   * gives each CTA pair (cta_group::2) a 256 x 512 tile: two N = 256 accumulators that
+//     fill TMEM, sharing every A k-block (48 KB per 1024 MMA cycles per CTA), and
+//   * (kPairs = 2) runs two pairs as a cluster of 4 on row blocks that share the B operand:
+//     each B slab is fetched once and multicast into both pairs (32 KB of L2 reads per CTA
+//     per 1024 MMA cycles, half the original per-MMA traffic).
+// Schedule: stream-K over (cluster tile, k-block) -- every cluster runs the same number of
+// k-blocks (+-1); partial tiles are reduced with TMA reduce-add into the gradient rows,
+// which the pass-1 kernel zeroed earlier in the step; the unit holding k-block 0 of a tile
+// also adds the local term -c r o E_L.
 #include "kernels.cuh"
 #include "sm100.cuh"
 
@@ -19,9 +26,9 @@ namespace fc {
 namespace {
 
 struct GSmem {
-  uint8_t* a;
-  uint8_t* b;
-  uint8_t* out;   // kEpiWarps x 4 KB epilogue staging (TMA store / reduce-add source)
+  uint8_t* a;     // kGemmStages x 16 KB (own 128 rows x 64 k)
+  uint8_t* b;     // kGemmStages x 32 KB (own 128 columns of each N half x 64 k)
+  uint8_t* out;   // kGemmEpiWarps x 4 KB epilogue staging (TMA reduce-add source)
   uint64_t* full;
   uint64_t* empty;
   uint64_t* tfull;
@@ -33,19 +40,18 @@ __device__ __forceinline__ GSmem gcarve(uint8_t* base) {
   GSmem L;
   uint8_t* p = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(base) + 1023) & ~uintptr_t(1023));
   L.a = p;
-  L.b = p + kStages * kStageBytesA;
-  L.out = L.b + kStages * kStageBytesB;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(L.out + kEpiWarps * kGemmStageOut);
+  L.b = p + kGemmStages * kStageBytesA;
+  L.out = L.b + kGemmStages * kGemmStageBytesB;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(L.out + kGemmEpiWarps * kGemmStageOut);
   L.full = bars;
-  L.empty = bars + kStages;
-  L.tfull = bars + 2 * kStages;
-  L.tempty = bars + 2 * kStages + 2;
-  L.tmem_ptr = reinterpret_cast<uint32_t*>(bars + 2 * kStages + 4);
+  L.empty = bars + kGemmStages;
+  L.tfull = bars + 2 * kGemmStages;
+  L.tempty = bars + 2 * kGemmStages + 1;
+  L.tmem_ptr = reinterpret_cast<uint32_t*>(bars + 2 * kGemmStages + 2);
   return L;
 }
 
-// tile -> (segment, row block, column block); column block fastest so that pairs running
-// side by side read the same Q' rows (the second read of each Q' tile hits L2).
+// cluster tile -> (segment, row block of 256 * kPairs rows, column block of 512)
 __device__ __forceinline__ void tile_decode(const GemmParams& p, int t, int& s, int& mb, int& nb) {
   const int per_seg0 = p.n_mb[0] * p.n_nb;
   s = t < per_seg0 ? 0 : 1;
@@ -54,36 +60,21 @@ __device__ __forceinline__ void tile_decode(const GemmParams& p, int t, int& s, 
   mb = local / p.n_nb;
 }
 
-// The pair's sequence of (tile, k-block range, atomic?) work segments.
-struct SegIter {
-  int pair, n_pairs, T, KB, dp_tiles;   // dp_tiles = floor(T / P) * P
-  int t;                                // next data-parallel tile
-  long long u, u1;                      // stream-K unit range (units = remainder tile k-blocks)
-  __device__ SegIter(const GemmParams& p, int pair_, int n_pairs_) {
-    pair = pair_;
-    n_pairs = n_pairs_;
-    T = p.n_tiles;
+// The cluster's stream-K work: contiguous range of (tile, k-block) units.
+struct UnitIter {
+  int KB;
+  long long u, u1;
+  __device__ UnitIter(const GemmParams& p, int cluster, int n_clusters) {
     KB = p.kb_total;
-    dp_tiles = (T / n_pairs) * n_pairs;
-    t = pair;
-    const long long U = static_cast<long long>(T - dp_tiles) * KB;
-    u = U * pair / n_pairs;
-    u1 = U * (pair + 1) / n_pairs;
+    const long long U = static_cast<long long>(p.n_tiles) * KB;
+    u = U * cluster / n_clusters;
+    u1 = U * (cluster + 1) / n_clusters;
   }
-  __device__ bool next(int& tile, int& kb0, int& kb1, bool& atomic) {
-    if (t < dp_tiles) {
-      tile = t;
-      kb0 = 0;
-      kb1 = KB;
-      atomic = false;
-      t += n_pairs;
-      return true;
-    }
+  __device__ bool next(int& tile, int& kb0, int& kb1) {
     if (u >= u1) return false;
-    tile = dp_tiles + static_cast<int>(u / KB);
+    tile = static_cast<int>(u / KB);
     kb0 = static_cast<int>(u % KB);
     kb1 = static_cast<int>(min(static_cast<long long>(KB), kb0 + (u1 - u)));
-    atomic = true;
     u += kb1 - kb0;
     return true;
   }
@@ -91,23 +82,27 @@ struct SegIter {
 
 }  // namespace
 
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+template <int kPairs>
+__global__ void __launch_bounds__(kGemmThreads, 1)
     grad_gemm_kernel(const __grid_constant__ GemmParams p, const __grid_constant__ CUtensorMap mapQ0,
                      const __grid_constant__ CUtensorMap mapX0, const __grid_constant__ CUtensorMap mapQ1,
                      const __grid_constant__ CUtensorMap mapX1, const __grid_constant__ CUtensorMap mapO0,
                      const __grid_constant__ CUtensorMap mapO1) {
   extern __shared__ uint8_t smem_raw[];
+  long long g_entry = 0;
+  if (p.debug >= 9) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_entry));
   const GSmem L = gcarve(smem_raw);
   const uint32_t warp = threadIdx.x / 32;
   const uint32_t lane = lane_id();
-  const uint32_t rank = cluster_ctarank();
-  const int pair = blockIdx.x / 2;
-  const int n_pairs = gridDim.x / 2;
+  const uint32_t crank = cluster_ctarank();          // 0 .. 2*kPairs-1
+  const uint32_t prank = crank & 1;                  // rank inside the CTA pair
+  const uint32_t pc = crank >> 1;                    // pair index inside the cluster
+  const int cluster = blockIdx.x / (2 * kPairs);
+  const int n_clusters = gridDim.x / (2 * kPairs);
+  constexpr uint16_t kAllCtas = static_cast<uint16_t>((1u << (2 * kPairs)) - 1);
+  const uint16_t pair_mask = static_cast<uint16_t>(0x3u << (2 * pc));
 
-  // warp roles: epilogue warps first, producer and MMA issuer LAST -- the SMSP arbiter
-  // favours the highest warp id, so the single-thread TMA/MMA issue never waits behind
-  // the epilogue math.
-  constexpr uint32_t kProdWarp = kEpiWarps, kMmaWarp = kEpiWarps + 1;
+  constexpr uint32_t kProdWarp = kGemmEpiWarps, kMmaWarp = kGemmEpiWarps + 1;
   if (warp == kProdWarp && lane == 0) {
     tma_prefetch(&mapQ0);
     tma_prefetch(&mapX0);
@@ -117,14 +112,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     }
   }
   if (warp == kMmaWarp && lane == 0) {
-    for (int i = 0; i < kStages; ++i) {
-      mbar_init(&L.full[i], 2);
-      mbar_init(&L.empty[i], 1);
+    for (int i = 0; i < kGemmStages; ++i) {
+      mbar_init(&L.full[i], 2);          // both producers of the pair (leader's barrier is used)
+      mbar_init(&L.empty[i], kPairs);    // one MMA commit per pair of the cluster (multicast B)
     }
-    for (int i = 0; i < 2; ++i) {
-      mbar_init(&L.tfull[i], 1);
-      mbar_init(&L.tempty[i], 2 * kEpiWarps);
-    }
+    mbar_init(&L.tfull[0], 1);
+    mbar_init(&L.tempty[0], 2 * kGemmEpiWarps);
     fence_barrier_init();
   }
   if (warp == 0) tmem_alloc<2>(L.tmem_ptr, 512);
@@ -134,157 +127,192 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   const uint32_t tmem_base = *L.tmem_ptr;
 
   if (warp == kProdWarp) {
-    // ===================== TMA producer =====================
-    {   // whole warp walks the loop, lane 0 issues
-      const bool issuer = lane == 0;
-      uint32_t stage = 0, phase = 0;
-      SegIter iter(p, pair, n_pairs);
-      int tile, kb0, kb1;
-      bool atomic;
-      while (iter.next(tile, kb0, kb1, atomic)) {
-        int s, mb, nb;
-        tile_decode(p, tile, s, mb, nb);
-        const CUtensorMap* mq = s ? &mapQ1 : &mapQ0;
-        const CUtensorMap* mx = s ? &mapX1 : &mapX0;
-        const int a_row = mb * kPairM + static_cast<int>(rank) * kCtaM;
-        const int n0 = nb * kPairN + static_cast<int>(rank) * (kPairN / 2);
-        const bool a_mn = p.seg[s].a_mn_major != 0;
-        for (int kb = kb0; kb < kb1; ++kb) {
-          mbar_wait(&L.empty[stage], phase ^ 1);
-          if (p.debug == 2 && kb > kb0 + kStages) {
-            if (issuer) {
-              if (rank == 0) mbar_arrive(&L.full[stage]);
-              else mbar_arrive_cluster(&L.full[stage], 0);
-            }
-            __syncwarp();
-            if (++stage == kStages) { stage = 0; phase ^= 1; }
-            continue;
-          }
-          if (!issuer) {
-            __syncwarp();
-            if (++stage == kStages) { stage = 0; phase ^= 1; }
-            continue;
-          }
-          if (rank == 0)
-            mbar_arrive_expect_tx(&L.full[stage], 2 * (kStageBytesA + kStageBytesB));
-          else
-            mbar_arrive_cluster(&L.full[stage], 0);
+    // ===================== TMA producer (whole warp walks, lane 0 issues) =====================
+    const bool issuer = lane == 0;
+    uint32_t stage = 0, phase = 0;
+    UnitIter iter(p, cluster, n_clusters);
+    int tile, kb0, kb1;
+    while (iter.next(tile, kb0, kb1)) {
+      int s, mb, nb;
+      tile_decode(p, tile, s, mb, nb);
+      const CUtensorMap* mq = s ? &mapQ1 : &mapQ0;
+      const CUtensorMap* mx = s ? &mapX1 : &mapX0;
+      const int a_row = (mb * kPairs + static_cast<int>(pc)) * kPairM + static_cast<int>(prank) * kCtaM;
+      const int n_blk = nb * kGemmN;
+      const bool a_mn = p.seg[s].a_mn_major != 0;
+      const bool half1 = n_blk + kPairN < p.d;   // this block's second N half has columns
+      const uint32_t bytes = 2 * (kStageBytesA + (half1 ? 2 : 1) * kStageBytesB);
+      for (int kb = kb0; kb < kb1; ++kb) {
+        mbar_wait(&L.empty[stage], phase ^ 1);
+        if (issuer) {
+          if (prank == 0) mbar_arrive_expect_tx(&L.full[stage], bytes);
+          else mbar_arrive_cluster(&L.full[stage], crank & ~1u);
           uint8_t* sa = L.a + stage * kStageBytesA;
-          uint8_t* sb = L.b + stage * kStageBytesB;
+          uint8_t* sb = L.b + stage * kGemmStageBytesB;
+          const int k0 = kb * kBlockK;
           if (a_mn) {
             // A = Q^T: two 64(M) x 64(K) swizzle atoms of the row-major Q (K = rows of Q)
-            tma_load_2d_pair(mq, &L.full[stage], sa, a_row, kb * kBlockK);
-            tma_load_2d_pair(mq, &L.full[stage], sa + kStageBytesA / 2, a_row + 64, kb * kBlockK);
+            tma_load_2d_pair(mq, &L.full[stage], sa, a_row, k0);
+            tma_load_2d_pair(mq, &L.full[stage], sa + kStageBytesA / 2, a_row + 64, k0);
           } else {
-            tma_load_2d_pair(mq, &L.full[stage], sa, kb * kBlockK, a_row);
+            tma_load_2d_pair(mq, &L.full[stage], sa, k0, a_row);
           }
-          // MN-major B: two 64(N) x 64(K) swizzle atoms for this CTA's 128 columns of N.
-          tma_load_2d_pair(mx, &L.full[stage], sb, n0, kb * kBlockK);
-          tma_load_2d_pair(mx, &L.full[stage], sb + kStageBytesB / 2, n0 + 64, kb * kBlockK);
-          __syncwarp();
-          if (++stage == kStages) { stage = 0; phase ^= 1; }
+          // B slab h of this CTA: columns n_blk + h*256 + prank*128 .. +128 (two 64-wide atoms)
+          if constexpr (kPairs == 1) {
+            for (int h = 0; h < (half1 ? 2 : 1); ++h) {
+              const int n0 = n_blk + h * kPairN + static_cast<int>(prank) * (kPairN / 2);
+              uint8_t* dst = sb + h * kStageBytesB;
+              tma_load_2d_pair(mx, &L.full[stage], dst, n0, k0);
+              tma_load_2d_pair(mx, &L.full[stage], dst + kStageBytesB / 2, n0 + 64, k0);
+            }
+          } else {
+            // pair pc fetches half h = pc once and multicasts it into the same-rank CTA of
+            // both pairs (the other pair fetches the other half)
+            const int h = static_cast<int>(pc);
+            if (h == 0 || half1) {
+              const uint16_t mask = static_cast<uint16_t>((1u << prank) | (1u << (prank + 2)));
+              const int n0 = n_blk + h * kPairN + static_cast<int>(prank) * (kPairN / 2);
+              uint8_t* dst = sb + h * kStageBytesB;
+              tma_load_2d_pair_mc(mx, &L.full[stage], dst, n0, k0, mask);
+              tma_load_2d_pair_mc(mx, &L.full[stage], dst + kStageBytesB / 2, n0 + 64, k0, mask);
+            }
+          }
         }
+        __syncwarp();
+        if (++stage == kGemmStages) { stage = 0; phase ^= 1; }
       }
     }
   } else if (warp == kMmaWarp) {
-    // ===================== MMA issuer (leader CTA, one thread; lean issue loop) =====================
-    if (rank == 0) {
+    // ===================== MMA issuer (pair leader; whole warp in the loop, one lane issues) =====================
+    if (prank == 0) {
       constexpr uint32_t idesc_k = make_idesc_bf16(kPairM, kPairN, 0, 1);
       constexpr uint32_t idesc_mn = make_idesc_bf16(kPairM, kPairN, 1, 1);
       const uint64_t a_desc_k = make_sdesc_sw128(smem_u32(L.a), 0, 1024);
       const uint64_t a_desc_mn = make_sdesc_sw128(smem_u32(L.a), kStageBytesA / 2, 1024);
       // MN-major SW128 B: 16 K rows of 128 B per UMMA_K; LBO = next 64-wide N atom.
       const uint64_t b_desc0 = make_sdesc_sw128(smem_u32(L.b), kStageBytesB / 2, 1024);
+      constexpr uint32_t kBHalf = kStageBytesB >> 4;   // descriptor offset of N half 1
       uint32_t stage = 0, phase = 0;
       int it = 0;
-      SegIter iter(p, pair, n_pairs);
+      const bool prof = p.debug >= 9;
+      long long c0 = clock64(), c_tempty = 0, c_full = 0, c_first = -1;
+      UnitIter iter(p, cluster, n_clusters);
       int tile, kb0, kb1;
-      bool atomic;
-      while (iter.next(tile, kb0, kb1, atomic)) {
+      while (iter.next(tile, kb0, kb1)) {
         int s, mb, nb;
         tile_decode(p, tile, s, mb, nb);
         const bool a_mn = p.seg[s].a_mn_major != 0;
+        const bool half1 = nb * kGemmN + kPairN < p.d;
         const uint32_t idesc = a_mn ? idesc_mn : idesc_k;
         const uint64_t a_desc0 = a_mn ? a_desc_mn : a_desc_k;
         const uint32_t a_kstep = a_mn ? (2048 >> 4) : (32 >> 4);   // descriptor units per UMMA_K
-        const uint32_t acc = it & 1;
-        const uint32_t acc_phase = (it >> 1) & 1;
-        mbar_wait(&L.tempty[acc], acc_phase ^ 1);
+        long long t0 = prof ? clock64() : 0;
+        mbar_wait(&L.tempty[0], (it & 1) ^ 1);   // the epilogue drained the previous unit
+        if (prof) c_tempty += clock64() - t0;
         tc_fence_after();
-        const uint32_t d_tmem = tmem_base + acc * kPairN;
         for (int kb = kb0; kb < kb1; ++kb) {
+          long long t1 = prof ? clock64() : 0;
           mbar_wait(&L.full[stage], phase);
+          if (prof) {
+            c_full += clock64() - t1;
+            if (c_first < 0) c_first = clock64() - c0;
+          }
           tc_fence_after();
           if (elect_one()) {
             const uint64_t ad = a_desc0 + static_cast<uint64_t>((stage * kStageBytesA) >> 4);
-            const uint64_t bd = b_desc0 + static_cast<uint64_t>((stage * kStageBytesB) >> 4);
-            mma_bf16_pair(d_tmem, ad, bd, idesc, kb != kb0);
-            mma_bf16_pair(d_tmem, ad + a_kstep, bd + 128, idesc, 1);
-            mma_bf16_pair(d_tmem, ad + 2 * a_kstep, bd + 256, idesc, 1);
-            mma_bf16_pair(d_tmem, ad + 3 * a_kstep, bd + 384, idesc, 1);
-            mma_commit_pair(&L.empty[stage], 0x3);
-            if (kb == kb1 - 1) mma_commit_pair(&L.tfull[acc], 0x3);
+            const uint64_t bd = b_desc0 + static_cast<uint64_t>((stage * kGemmStageBytesB) >> 4);
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              const uint32_t accum = (kb != kb0 || k != 0) ? 1u : 0u;
+              mma_bf16_pair(tmem_base, ad + k * a_kstep, bd + 128 * k, idesc, accum);
+              if (half1) mma_bf16_pair(tmem_base + kPairN, ad + k * a_kstep, bd + kBHalf + 128 * k, idesc, accum);
+            }
+            mma_commit_pair(&L.empty[stage], kPairs == 1 ? pair_mask : kAllCtas);
+            if (kb == kb1 - 1) mma_commit_pair(&L.tfull[0], pair_mask);
           }
           __syncwarp();
-          if (++stage == kStages) { stage = 0; phase ^= 1; }
+          if (++stage == kGemmStages) { stage = 0; phase ^= 1; }
         }
         ++it;
+      }
+      if (prof && lane == 0) {
+        long long* o = p.dbg_out + blockIdx.x * 16;
+        o[0] = clock64() - c0; o[1] = c_tempty; o[2] = c_full; o[3] = c_first; o[4] = it;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(o[5]));
       }
     }
   } else {
     // ===================== epilogue =====================
-    // Each warp owns 32 rows (its TMEM lane quarter) x 128 columns (its half of N), handled
-    // as 4 chunks of 32 columns: TMEM -> registers -> c (acc - r o X_local) -> swizzled smem
-    // -> one TMA tile store (whole tiles) or TMA reduce-add (stream-K partial tiles).
+    // Warp w owns 32 rows (TMEM lane quarter w & 3) x 256 columns (N half w >> 2) of the
+    // pair's 256 x 512 accumulator: 8 chunks of 32 columns, TMEM -> registers ->
+    // c (acc - r o X_L) -> swizzled smem -> TMA reduce-add into the zeroed gradient rows.
+    constexpr int kEpiCols = kGemmN / (kGemmEpiWarps / 4);   // columns per warp
+    constexpr int kChunks = kEpiCols / 32;
     const uint32_t q4 = warp & 3;
-    const uint32_t half = warp >> 2;
+    const uint32_t cg = warp >> 2;
     uint8_t* stage_out = L.out + warp * kGemmStageOut;
+    const uint32_t leader = crank & ~1u;
+    const bool eprof = p.debug >= 9 && warp == 0;
+    long long e0 = clock64(), e_wait = 0;
     int it = 0;
-    SegIter iter(p, pair, n_pairs);
+    UnitIter iter(p, cluster, n_clusters);
     int tile, kb0, kb1;
-    bool atomic;
-    while (iter.next(tile, kb0, kb1, atomic)) {
+    while (iter.next(tile, kb0, kb1)) {
       int s, mb, nb;
       tile_decode(p, tile, s, mb, nb);
       const GemmSeg& sg = p.seg[s];
       const CUtensorMap* mo = s ? &mapO1 : &mapO0;
-      const uint32_t acc = it & 1;
-      const uint32_t acc_phase = (it >> 1) & 1;
-      const int row0 = mb * kPairM + static_cast<int>(rank) * kCtaM + static_cast<int>(q4) * 32;
+      const int row0 = (mb * kPairs + static_cast<int>(pc)) * kPairM + static_cast<int>(prank) * kCtaM +
+                       static_cast<int>(q4) * 32;
       const int r_loc = row0 + static_cast<int>(lane);
       const bool row_ok = r_loc < sg.rows;
-      const bool with_r = kb0 == 0;   // the -r o X_local term is added exactly once per tile
-      const float rr = (row_ok && with_r) ? sg.r[r_loc] : 0.f;
-      const __nv_bfloat16* xrow = sg.x + static_cast<size_t>(sg.x_row0 + (row_ok ? r_loc : 0)) * p.d;
-      mbar_wait(&L.tfull[acc], acc_phase);
+      // the unit holding k-block 0 adds the local term -c r o X_L exactly once per tile; its X
+      // loads are software-pipelined one chunk ahead (the first before the accumulator wait)
+      const bool with_r = kb0 == 0;
+      const float cr = (row_ok && with_r) ? p.scale * sg.r[r_loc] : 0.f;
+      const uint4* xrow = reinterpret_cast<const uint4*>(sg.x + static_cast<size_t>(sg.x_row0 + (row_ok ? r_loc : 0)) * p.d);
+      uint4 xn[4];
+      auto load_x = [&](int c) {
+        const int col0 = nb * kGemmN + static_cast<int>(cg) * kEpiCols + c * 32;
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          xn[q] = (with_r && row_ok && col0 + 8 * q < p.d) ? __ldg(xrow + col0 / 8 + q) : make_uint4(0u, 0u, 0u, 0u);
+      };
+      load_x(0);
+      long long t0 = eprof ? clock64() : 0;
+      mbar_wait(&L.tfull[0], it & 1);
+      if (eprof) e_wait += clock64() - t0;
       tc_fence_after();
 #pragma unroll 1
-      for (int c = 0; c < 4; ++c) {
-        const int col0 = nb * kPairN + static_cast<int>(half) * 128 + c * 32;
-        const uint32_t taddr = tmem_base + ((q4 * 32u) << 16) + acc * kPairN + half * 128u + c * 32u;
+      for (int c = 0; c < kChunks; ++c) {
+        const int tcol = static_cast<int>(cg) * kEpiCols + c * 32;   // column inside the 512-wide block
+        const int col0 = nb * kGemmN + tcol;
+        const bool live = col0 < p.d && row0 < sg.rows;          // warp-uniform
         uint32_t r[32];
-        tmem_ld_32x32b_x32(taddr, r);
-        tmem_ld_wait();
-        if (c == 3) {   // whole accumulator slice read: release it to the MMA warp
+        if (live || c == kChunks - 1) {
+          tmem_ld_32x32b_x32(tmem_base + ((q4 * 32u) << 16) + static_cast<uint32_t>(tcol), r);
+          tmem_ld_wait();
+        }
+        if (c == kChunks - 1) {   // this warp's accumulator slice is in registers: release it
           tc_fence_before();
           __syncwarp();
           if (lane == 0) {
-            if (rank == 0) mbar_arrive(&L.tempty[acc]);
-            else mbar_arrive_cluster(&L.tempty[acc], 0);
+            if (prank == 0) mbar_arrive(&L.tempty[0]);
+            else mbar_arrive_cluster(&L.tempty[0], leader);
           }
         }
-        if (col0 >= p.d || p.debug != 0) continue;   // warp-uniform
+        if (!live || (p.debug != 0 && p.debug < 3)) continue;
         float v[32];
 #pragma unroll
         for (int k = 0; k < 32; ++k) v[k] = p.scale * __uint_as_float(r[k]);
-        if (with_r && row_ok) {
-          const float cr = p.scale * rr;
-          const uint4* xs = reinterpret_cast<const uint4*>(xrow + col0);
+        if (with_r) {
+          uint4 xc[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) xc[q] = xn[q];
+          if (c + 1 < kChunks) load_x(c + 1);
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
-            if (col0 + 8 * q >= p.d) break;  // d % 8 == 0: groups of 8 are all-in or all-out
-            const uint4 w = __ldg(xs + q);
-            const uint32_t ww[4] = {w.x, w.y, w.z, w.w};
+            const uint32_t ww[4] = {xc[q].x, xc[q].y, xc[q].z, xc[q].w};
 #pragma unroll
             for (int t = 0; t < 4; ++t) {
               const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&ww[t]));
@@ -293,7 +321,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             }
           }
         }
-        // the previous chunk's bulk store must have finished reading the staging buffer
+        // the previous chunk's bulk reduce must have finished reading the staging buffer
         if (lane == 0) bulk_wait_read0();
         __syncwarp();
         uint8_t* rowp = stage_out + lane * 128;
@@ -304,35 +332,78 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) {
-          if (atomic) tma_reduce_add_2d(mo, stage_out, col0, row0);
-          else tma_store_2d(mo, stage_out, col0, row0);
+          if (p.debug == 3 || p.debug == 10) tma_store_2d(mo, stage_out, col0, row0);   // experiment: plain store
+          else tma_reduce_add_2d(mo, stage_out, col0, row0);
           bulk_commit();
         }
       }
       ++it;
     }
     if (lane == 0) bulk_wait0();
+    if (eprof && lane == 0) {
+      long long* o = p.dbg_out + blockIdx.x * 16 + 8;
+      o[0] = clock64() - e0; o[1] = e_wait;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(o[2]));
+      o[3] = g_entry;
+    }
   }
 
-  __syncwarp();   // single-thread producer / MMA roles reconverge before the aligned cluster barrier
+  __syncwarp();   // single-lane producer / MMA roles reconverge before the aligned cluster barrier
   tc_fence_before();
   cluster_sync();
   if (warp == 0) tmem_dealloc<2>(tmem_base, 512);
 }
 
+namespace {
+template <int kPairs>
+cudaError_t launch_gemm_t(const GemmParams& p, const CUtensorMap* mapQ, const CUtensorMap* mapX,
+                          const CUtensorMap* mapOut, int grid, cudaStream_t s) {
+  const CUtensorMap& q1 = p.nseg > 1 ? mapQ[1] : mapQ[0];
+  const CUtensorMap& x1 = p.nseg > 1 ? mapX[1] : mapX[0];
+  const CUtensorMap& o1 = p.nseg > 1 ? mapOut[1] : mapOut[0];
+  cudaLaunchConfig_t cfg{};
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2 * kPairs;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.gridDim = dim3(grid, 1, 1);
+  cfg.blockDim = dim3(kGemmThreads, 1, 1);
+  cfg.dynamicSmemBytes = kGemmSmemBytes;
+  cfg.stream = s;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, grad_gemm_kernel<kPairs>, p, mapQ[0], mapX[0], q1, x1, mapOut[0], o1);
+}
+}  // namespace
+
+cudaError_t gemm_max_active_clusters(int pairs_per_cluster, int* n) {
+  cudaLaunchConfig_t cfg{};
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2 * pairs_per_cluster;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.gridDim = dim3(148, 1, 1);
+  cfg.blockDim = dim3(kGemmThreads, 1, 1);
+  cfg.dynamicSmemBytes = kGemmSmemBytes;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  if (pairs_per_cluster == 2) return cudaOccupancyMaxActiveClusters(n, grad_gemm_kernel<2>, &cfg);
+  return cudaOccupancyMaxActiveClusters(n, grad_gemm_kernel<1>, &cfg);
+}
+
 cudaError_t gemm_set_smem() {
-  return cudaFuncSetAttribute(grad_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
+  cudaError_t e = cudaFuncSetAttribute(grad_gemm_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kGemmSmemBytes);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(grad_gemm_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, kGemmSmemBytes);
+  return e;
 }
 
 cudaError_t launch_gemm(const GemmParams& p, const CUtensorMap* mapQ, const CUtensorMap* mapX,
                         const CUtensorMap* mapOut, int grid, cudaStream_t s) {
-  const CUtensorMap& q1 = p.nseg > 1 ? mapQ[1] : mapQ[0];
-  const CUtensorMap& x1 = p.nseg > 1 ? mapX[1] : mapX[0];
-  const CUtensorMap& o1 = p.nseg > 1 ? mapOut[1] : mapOut[0];
-  if (grid < 2) grid = 2;
-  grid &= ~1;
-  grad_gemm_kernel<<<grid, kThreads, kSmemBytes, s>>>(p, mapQ[0], mapX[0], q1, x1, mapOut[0], o1);
-  return cudaGetLastError();
+  if (p.pairs_per_cluster == 2) return launch_gemm_t<2>(p, mapQ, mapX, mapOut, grid, s);
+  return launch_gemm_t<1>(p, mapQ, mapX, mapOut, grid, s);
 }
 
 }  // namespace fc

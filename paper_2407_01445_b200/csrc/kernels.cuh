@@ -13,8 +13,6 @@ constexpr int kPairM = 256;      // rows per pair tile (128 per CTA)
 constexpr int kCtaM = 128;       // TMEM lanes / rows per CTA
 constexpr int kPairN = 256;      // columns per pair tile (UMMA N)
 constexpr int kBlockK = 64;      // bf16 per 128-byte swizzle atom
-constexpr int kEpiWarps = 8;     // 2 per TMEM lane quarter (column halves)
-constexpr int kThreads = (2 + kEpiWarps) * 32;
 constexpr int kStageBytesA = kCtaM * kBlockK * 2;        // 16 KB
 constexpr int kStageBytesB = (kPairN / 2) * kBlockK * 2;  // 16 KB (own half of N)
 // similarity kernel: A (the anchor rows) stays resident for up to 8 K blocks (d <= 512;
@@ -31,11 +29,15 @@ constexpr int kSimSmemStats = kSimASlots * kStageBytesA + kSimStagesStats * kSta
 constexpr int kSimSmemQ = kSimASlots * kStageBytesA + kSimStagesQ * kStageBytesB + kSimPSlots * kSimPSlotBytes +
                           kSimEpiWarps * kSimStageOutQ;
 constexpr int kSimSmemBytes = (kSimSmemStats > kSimSmemQ ? kSimSmemStats : kSimSmemQ) + 1024 + 512;
-// gradient GEMM: A (Q') and B (E) both stream.
-constexpr int kStages = 6;
+// gradient GEMM: A (Q') and B (E) both stream; pair tile 256 x 512 (two N = 256 accumulators).
+constexpr int kGemmN = 2 * kPairN;
+constexpr int kGemmStages = 4;
+constexpr int kGemmStageBytesB = 2 * kStageBytesB;   // own 128 columns of both N halves
+constexpr int kGemmEpiWarps = 8;                     // 2 per TMEM lane quarter, 256 columns each
+constexpr int kGemmThreads = (2 + kGemmEpiWarps) * 32;
 constexpr int kGemmStageOut = 32 * 32 * 4;   // per epilogue warp: 32 rows x 32 fp32 (128-byte swizzled rows)
-constexpr int kSmemBytes = kStages * (kStageBytesA + kStageBytesB) + kEpiWarps * kGemmStageOut + 1024 /*align*/ +
-                           256 /*barriers*/;
+constexpr int kGemmSmemBytes = kGemmStages * (kStageBytesA + kGemmStageBytesB) + kGemmEpiWarps * kGemmStageOut +
+                               1024 /*align*/ + 256 /*barriers*/;
 
 // ---- similarity-tile kernel (pass 1: row statistics; pass 2: Q tiles) ----
 // One "segment" is an S block S' = A B^T with A = E_rows[a_row0 .. a_row0+rows) and
@@ -46,6 +48,7 @@ struct SimSeg {
   int a_row0;               // global index of local row 0 (diagonal masking)
   int cols;                 // contrast set size (global batch B)
   const float2* row_stat;   // STATS: [rows] {kappa_i = log2(e)/t_i, beta_i = -S_ii kappa_i}
+  const float2* col_stat;   // FUSED: [cols] {kappa_j, beta_j} of the column anchors (segment C)
   float2* partial;          // STATS: [rows][n_jt*4] {sum e, sum y e} per column quarter
   // Q: exponent y = s*kappa + beta (= (s - S_aa) log2(e)/t_a), weight coef (SoA, fp32)
   const float* row_kappa; const float* row_beta; const float* row_coef;   // [rows]
@@ -65,6 +68,15 @@ struct SimParams {
   unsigned long long* clamps;  // STATS: exponent clamps (safe_exp, losses.cpp:22-28)
   const float* bounds;         // {max |E1_i|^2, max |E2_j|^2, max kappa over G}: clamp-free fast paths
   int q_factor;                // Q: one shared temperature -> factorized single-exponential fast path
+  // STATS pass prologue (idle epilogue warps): zero the step's gradient outputs, which the
+  // gradient GEMM later accumulates into with TMA reduce-add
+  float4* zero_a; float4* zero_b;          // nullptr: nothing to zero
+  long long zero_n4;                       // float4 count of each
+  // FUSED: column statistics {sum e, sum y e} per (row slot = 32-row quarter of a pair tile,
+  // column): [n_slots][cols]; fuse_fast enables the one-exponential path (one temperature)
+  float2* col_partial;
+  int n_slots;
+  int fuse_fast;
   int debug;                   // perf experiments: 1 = skip epilogue math, 2 = also skip B loads
   long long* dbg_out;          // debug == 9: per-pair MMA-warp cycle counters [pair][8]
 };
@@ -76,7 +88,7 @@ struct GemmSeg {
   int x_row0;                // global index of local row 0 (for the r o X_local term)
   const float* r;            // [rows]
   const __nv_bfloat16* x;    // [B][d] row-major (the B operand, read for the r term)
-  float* out;                // [rows][d]
+  float* out;                // [rows][d], zeroed before the GEMM (reduce-add target)
 };
 struct GemmParams {
   GemmSeg seg[2];
@@ -84,13 +96,17 @@ struct GemmParams {
   int d;
   int n_mb[2];
   int n_nb;
-  int n_tiles;       // sum over segments of n_mb * n_nb
+  int n_tiles;       // sum over segments of n_mb * n_nb (cluster tiles: 256*pairs_per_cluster x 512)
+  int pairs_per_cluster;   // 1, or 2: two pairs share (multicast) the B operand
   int kb_total;      // K blocks of 64 over ldq
   float scale;       // 1 / (Bl (B-1)), engine.cpp:84-85
-  int debug;         // perf experiments: 1 = skip epilogue stores, 2 = also skip loads after the first stage
+  int debug;         // perf experiments: 1 = skip epilogue stores; 9 = counters / timelines into dbg_out
+  long long* dbg_out;   // debug == 9: [cta][8] MMA / epilogue counters, globaltimer stamps
 };
 
-enum SimMode { kSimStats = 0, kSimQ = 1, kSimRaw = 2 };
+// kSimFused (K = 1): one S tile gives both the row statistics (segment R) and the column
+// statistics (segment C = S^T), so pass 1 multiplies S once instead of twice.
+enum SimMode { kSimStats = 0, kSimQ = 1, kSimRaw = 2, kSimFused = 3 };
 
 cudaError_t launch_sim(int mode, const SimParams& p, const CUtensorMap* mapA, const CUtensorMap* mapB,
                        const CUtensorMap* mapQout, int grid, cudaStream_t s, float* raw_out);
@@ -98,6 +114,7 @@ cudaError_t sim_set_smem();
 cudaError_t launch_ring_probe(int n_pairs, int n_kb, int tile_kb, int epi, long long* cycles, cudaStream_t s);
 cudaError_t launch_mma_probe(int n_pairs, int n_mma, int commit_every, long long* cycles, cudaStream_t s);
 cudaError_t gemm_set_smem();
+cudaError_t gemm_max_active_clusters(int pairs_per_cluster, int* n);
 cudaError_t launch_gemm(const GemmParams& p, const CUtensorMap* mapQ, const CUtensorMap* mapX,
                         const CUtensorMap* mapOut, int grid, cudaStream_t s);
 

@@ -108,7 +108,7 @@ struct LossStep {
   // workspaces
   __nv_bfloat16 *e1g = nullptr, *e2g = nullptr;   // gathered embeddings (K > 1)
   float* diag = nullptr;
-  float2 *rowstat = nullptr, *partial = nullptr;
+  float2 *rowstat = nullptr, *partial = nullptr, *col_partial = nullptr;
   unsigned long long* clamps = nullptr;
   float* bounds = nullptr;
   double* f64 = nullptr;   // per-local-anchor fp64 arrays
@@ -119,7 +119,7 @@ struct LossStep {
   int* err = nullptr;
   fc::StepResult* result_d = nullptr;
   fc::StepResult* result_h = nullptr;   // pinned
-  cudaEvent_t done{}, fork{}, side_fork{}, side_join{};
+  cudaEvent_t done{}, fork{}, side_fork{}, side_join{}, zero_fork{}, zero_join{};
   cudaStream_t ws = nullptr;     // context stream (capturable), joined to the caller's stream
   cudaStream_t ws2 = nullptr;    // side branch: reductions / tau updates off the critical path
   double* scal = nullptr;        // device {gamma_t, eps_t}
@@ -127,6 +127,8 @@ struct LossStep {
   bool shared_q = true;          // K == 1: one Q pass, Q^T read by the dE2 GEMM
   int sim_debug = 0, gemm_debug = 0;
   bool q_factor = true;          // FC_Q_FACTOR=0 forces the two-exponential Q path (A/B checks)
+  bool gemm_mc = false;          // FC_GEMM_MC=1: clusters of two pairs multicast the GEMM B operand
+  bool fused_p1 = false;         // K == 1: row + column statistics from one S pass (FC_FUSED_P1=0: two passes)
   long long* dbg_buf = nullptr;   // FC_SIM_DEBUG=9 MMA-warp counters: [launch 0: pass 1, 1: pass 2][pair][8]             // FC_SIM_DEBUG perf experiments (results invalid when set)
   struct GraphEntry {
     const void* key[5];
@@ -211,6 +213,7 @@ struct LossStep {
     diag = dalloc<float>(B);
     rowstat = dalloc<float2>(2 * static_cast<size_t>(Bl));
     partial = dalloc<float2>(2 * static_cast<size_t>(Bl) * n_jt * 4);
+    if (K == 1) col_partial = dalloc<float2>(static_cast<size_t>((Bl + fc::kPairM - 1) / fc::kPairM) * 8 * B);
     clamps = dalloc<unsigned long long>(1);
     bounds = dalloc<float>(4);
     f64 = dalloc<double>(static_cast<size_t>(Bl) * 18);
@@ -235,18 +238,31 @@ struct LossStep {
     FC_CUDA(cudaStreamCreateWithFlags(&ws2, cudaStreamNonBlocking));
     FC_CUDA(cudaEventCreateWithFlags(&side_fork, cudaEventDisableTiming));
     FC_CUDA(cudaEventCreateWithFlags(&side_join, cudaEventDisableTiming));
+    FC_CUDA(cudaEventCreateWithFlags(&zero_fork, cudaEventDisableTiming));
+    FC_CUDA(cudaEventCreateWithFlags(&zero_join, cudaEventDisableTiming));
     scal = dalloc<double>(2);
     if (const char* e = std::getenv("FC_GRAPH")) use_graph = atoi(e) != 0;
     shared_q = K == 1;
     if (const char* e = std::getenv("FC_DEBUG_SYNC")) debug_sync = atoi(e) != 0;
     if (const char* e = std::getenv("FC_SIM_DEBUG")) sim_debug = atoi(e);
     if (const char* e = std::getenv("FC_Q_FACTOR")) q_factor = atoi(e) != 0;
-    if (sim_debug == 9) dbg_buf = dalloc<long long>(2 * 2688);
+    if (const char* e = std::getenv("FC_GEMM_MC")) gemm_mc = atoi(e) != 0;
+    fused_p1 = K == 1;
+    if (const char* e = std::getenv("FC_FUSED_P1")) fused_p1 = fused_p1 && atoi(e) != 0;
     if (const char* e = std::getenv("FC_GEMM_DEBUG")) gemm_debug = atoi(e);
+    if (sim_debug == 9 || gemm_debug >= 9) dbg_buf = dalloc<long long>(2 * 2688 + 160 * 16);
     if (debug_sync) use_graph = false;
     if (const char* e = std::getenv("FC_SHARED_Q")) shared_q = shared_q && atoi(e) != 0;
     FC_CUDA(fc::sim_set_smem());
     FC_CUDA(fc::gemm_set_smem());
+    // side-branch kernels run beside persistent similarity CTAs: ask for the max-shared
+    // carveout so the SM configuration they land on never has to change for a pass-2 CTA
+    FC_CUDA(cudaFuncSetAttribute(fc::fc_reduce_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                 cudaSharedmemCarveoutMaxShared));
+    FC_CUDA(cudaFuncSetAttribute(fc::fc_zero_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                 cudaSharedmemCarveoutMaxShared));
+    FC_CUDA(cudaFuncSetAttribute(fc::fc_indiv_update_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                 cudaSharedmemCarveoutMaxShared));
     mQ[0] = make_map(q, ldq, Bl, static_cast<uint64_t>(ldq) * 2, 64, 128);
     mQ[1] = make_map(q + static_cast<size_t>(Bl) * ldq, ldq, Bl, static_cast<uint64_t>(ldq) * 2, 64, 128);
     mQt = make_map(q, ldq, Bl, static_cast<uint64_t>(ldq) * 2, 64, 64);   // Q^T as MN-major A (K = 1)
@@ -368,11 +384,19 @@ struct LossStep {
     ensure_maps(E1, E2);
     fc::StepArgs a = args;
     a.ids = in->ids;
+    a.gscale = static_cast<float>(1.0 / (static_cast<double>(Bl) * static_cast<double>(B - 1)));
     a.scal = scal;
 
     mark(1, st);
+    // side branch: zero dE (the GEMM's reduce-add target) while prep and pass 1 run
+    FC_CUDA(cudaEventRecord(zero_fork, st));
+    FC_CUDA(cudaStreamWaitEvent(ws2, zero_fork, 0));
+    fc::fc_zero_kernel<<<n_sm, 256, 0, ws2>>>(reinterpret_cast<float4*>(out->de1), reinterpret_cast<float4*>(out->de2),
+                                              static_cast<long long>(Bl) * d / 4);
+    FC_CUDA(cudaGetLastError());
+    FC_CUDA(cudaEventRecord(zero_join, ws2));
     FC_CUDA(cudaMemsetAsync(bounds, 0, 4 * sizeof(float), st));
-    fc::fc_prep_kernel<<<(B * 32 + 511) / 512, 512, 0, st>>>(E1, E2, a);
+    fc::fc_prep_kernel<<<(B * 32 + 127) / 128, 128, 0, st>>>(E1, E2, a);   // one wave: <= 9 blocks/SM
     FC_CUDA(cudaGetLastError());
 
     // ---- pass 1: row statistics of S[L,G] (segment R) and S^T[L,G] (segment C) ----
@@ -394,10 +418,27 @@ struct LossStep {
     sp.clamps = clamps;
     sp.bounds = bounds;
     sp.debug = sim_debug;
+    sp.zero_a = sp.zero_b = nullptr;
     if (sim_debug == 9) sp.dbg_out = dbg_buf;
     CUtensorMap mA[2] = {mE1k, mE2k}, mB[2] = {mE2k, mE1k};
     mark(2, st);
-    FC_CUDA(fc::launch_sim(fc::kSimStats, sp, mA, mB, nullptr, pair_grid(sp.n_items), st, nullptr));
+    if (fused_p1) {
+      // K = 1: segment C is S^T -- its row statistics are the column statistics of the
+      // segment-R tiles, collected in the same epilogue (S is multiplied once)
+      sp.nseg = 1;
+      sp.n_rb[1] = 0;
+      sp.n_items = sp.n_rb[0] * n_jt;
+      sp.seg[0].col_stat = a.rowstat_C;
+      sp.col_partial = col_partial;
+      sp.n_slots = sp.n_rb[0] * 8;
+      sp.fuse_fast = indiv ? 0 : 1;
+      a.col_partial = col_partial;
+      a.col_slots = sp.n_slots;
+      FC_CUDA(fc::launch_sim(fc::kSimFused, sp, mA, mB, nullptr, pair_grid(sp.n_items), st, nullptr));
+    } else {
+      a.col_slots = 0;
+      FC_CUDA(fc::launch_sim(fc::kSimStats, sp, mA, mB, nullptr, pair_grid(sp.n_items), st, nullptr));
+    }
 
     // ---- u table, payload, (all-gather), weights, reductions, tau update ----
     mark(3, st);
@@ -453,7 +494,8 @@ struct LossStep {
       sp.n_items = sp.n_rb[0] * n_jt;
     }
     if (sim_debug == 9) sp.dbg_out = dbg_buf + 2688;
-    sp.q_factor = (!indiv && q_factor) ? 1 : 0;   // one shared temperature: single-exponential Q   // pass-2 counters / timelines
+    sp.q_factor = (!indiv && q_factor) ? 1 : 0;   // one shared temperature: single-exponential Q
+    sp.zero_a = sp.zero_b = nullptr;
     FC_CUDA(fc::launch_sim(fc::kSimQ, sp, mA, mB, mQo, pair_grid(sp.n_items), st, nullptr));
 
     // ---- pass 2b: dE = c (Q' E - r o E_local) ----
@@ -461,10 +503,12 @@ struct LossStep {
     fc::GemmParams gp{};
     gp.nseg = 2;
     gp.d = d;
-    gp.n_nb = (d + fc::kPairN - 1) / fc::kPairN;
+    gp.n_nb = (d + fc::kGemmN - 1) / fc::kGemmN;
+    gp.pairs_per_cluster = gemm_mc ? 2 : 1;
     gp.kb_total = ldq / fc::kBlockK;
     gp.scale = static_cast<float>(1.0 / (static_cast<double>(Bl) * static_cast<double>(B - 1)));
     gp.debug = gemm_debug;
+    if (gemm_debug >= 9) gp.dbg_out = dbg_buf + 2 * 2688;
     for (int s = 0; s < 2; ++s) {
       fc::GemmSeg& g = gp.seg[s];
       g.a_mn_major = (shared_q && s == 1) ? 1 : 0;
@@ -473,25 +517,12 @@ struct LossStep {
       g.r = rcoef;
       g.x = s ? E1 : E2;
       g.out = s ? out->de2 : out->de1;
-      gp.n_mb[s] = (Bl + fc::kPairM - 1) / fc::kPairM;
+      const int rows_per_tile = fc::kPairM * gp.pairs_per_cluster;
+      gp.n_mb[s] = (Bl + rows_per_tile - 1) / rows_per_tile;
     }
     gp.n_tiles = (gp.n_mb[0] + gp.n_mb[1]) * gp.n_nb;
-    const int gemm_pairs = n_sm / 2;
-    {
-      // tiles past the data-parallel rounds are split over all pairs and reduced with
-      // atomics: zero their row blocks first (they form the tail in (segment, row block) order)
-      const int dp = (gp.n_tiles / gemm_pairs) * gemm_pairs;
-      if (dp < gp.n_tiles) {
-        const int per0 = gp.n_mb[0] * gp.n_nb;
-        const int s0 = dp < per0 ? 0 : 1;
-        const int mb0 = (dp - (s0 ? per0 : 0)) / gp.n_nb;
-        for (int s = s0; s < 2; ++s) {
-          const size_t r0 = s == s0 ? static_cast<size_t>(mb0) * fc::kPairM : 0;
-          if (r0 < static_cast<size_t>(Bl))
-            FC_CUDA(cudaMemsetAsync(gp.seg[s].out + r0 * d, 0, (Bl - r0) * d * 4, st));
-        }
-      }
-    }
+    // every unit reduce-adds into dE (zeroed by the per-anchor kernel of this step)
+    const int gemm_ctas = (n_sm / (2 * gp.pairs_per_cluster)) * 2 * gp.pairs_per_cluster;
     CUtensorMap mX[2] = {mE2n, mE1n};
     CUtensorMap mQs[2] = {mQ[0], shared_q ? mQt : mQ[1]};
     if (out->de1 != map_o1 || out->de2 != map_o2) {
@@ -501,7 +532,8 @@ struct LossStep {
       map_o1 = out->de1;
       map_o2 = out->de2;
     }
-    FC_CUDA(fc::launch_gemm(gp, mQs, mX, mO, gemm_pairs * 2, st));
+    FC_CUDA(cudaStreamWaitEvent(st, zero_join, 0));
+    FC_CUDA(fc::launch_gemm(gp, mQs, mX, mO, gemm_ctas, st));
     mark(6, st);
 
     if (K == 1) FC_CUDA(cudaStreamWaitEvent(st, side_join, 0));
@@ -510,14 +542,14 @@ struct LossStep {
 
   int kernels_per_step() const {
     return 1 /*prep*/ + 1 /*pass1*/ + (K > 1 ? 2 : 1) /*table (+weights)*/ + 1 /*reduce*/ + (indiv ? 1 : 0) +
-           (K > 1 ? 1 : 0) /*finalize*/ + 1 /*pass2*/ + 1 /*gemm*/;
+           (K > 1 ? 1 : 0) /*finalize*/ + 1 /*zero dE*/ + 1 /*pass2*/ + 1 /*gemm*/;
   }
 
   void destroy() {
     if (comm) ncclCommDestroy(comm);
     for (void* p : {(void*)u1, (void*)u2, (void*)tau1, (void*)tau2, (void*)m1, (void*)v1, (void*)m2, (void*)v2,
                     (void*)s1, (void*)s2, (void*)tau_state, (void*)e1g, (void*)e2g, (void*)diag, (void*)rowstat,
-                    (void*)partial, (void*)clamps, (void*)bounds, (void*)f64, (void*)red, (void*)par, (void*)rcoef, (void*)blockpart,
+                    (void*)partial, (void*)col_partial, (void*)clamps, (void*)bounds, (void*)f64, (void*)red, (void*)par, (void*)rcoef, (void*)blockpart,
                     (void*)q, (void*)err, (void*)result_d, (void*)gt_recv})
       if (p) cudaFree(p);
     if (recv && recv != send) cudaFree(recv);
@@ -530,6 +562,8 @@ struct LossStep {
     if (ws2) cudaStreamDestroy(ws2);
     cudaEventDestroy(side_fork);
     cudaEventDestroy(side_join);
+    cudaEventDestroy(zero_fork);
+    cudaEventDestroy(zero_join);
     cudaEventDestroy(done);
     cudaEventDestroy(fork);
     for (auto& e : ev) cudaEventDestroy(e);
@@ -562,6 +596,10 @@ int fc_debug_ring_probe(int32_t n_pairs, int32_t n_kb, int32_t tile_kb, int32_t 
   return guarded([&] {
     FC_CUDA(fc::launch_ring_probe(n_pairs, n_kb, tile_kb, epi, cycles_dev, static_cast<cudaStream_t>(stream)));
   });
+}
+
+int fc_debug_gemm_clusters(int32_t pairs_per_cluster, int32_t* max_clusters) {
+  return guarded([&] { FC_CUDA(fc::gemm_max_active_clusters(pairs_per_cluster, max_clusters)); });
 }
 
 int fc_debug_mma_probe(int32_t n_pairs, int32_t n_mma, int32_t commit_every, long long* cycles_dev, void* stream) {
@@ -772,7 +810,7 @@ int fc_debug_counters(void* ctx, long long* out /* host [2*128*8] */) {
   auto* s = static_cast<LossStep*>(ctx);
   return guarded([&] {
     FC_CUDA(cudaDeviceSynchronize());
-    if (s->dbg_buf) FC_CUDA(cudaMemcpy(out, s->dbg_buf, 2 * 2688 * 8, cudaMemcpyDeviceToHost));
+    if (s->dbg_buf) FC_CUDA(cudaMemcpy(out, s->dbg_buf, (2 * 2688 + 160 * 16) * 8, cudaMemcpyDeviceToHost));
   });
 }
 

@@ -47,15 +47,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128, 1)
         }
       } else {
         // realistic k-block loop: 4 MMAs per block with precomputed descriptors;
-        // commit_every bit0: try_wait on a completed barrier, bit1: fence, bit2: commit
-        const uint64_t ad0 = make_sdesc_sw128(a0, 0, 1024), bd0 = make_sdesc_sw128(b0, 0, 1024);
+        // commit_every bit0: try_wait on a completed barrier, bit1: fence, bit2: commit,
+        // bit3: MN-major B operand, bit4: MN-major A operand (operand-major rate check)
+        const bool bmn = commit_every & 8, amn = commit_every & 16;
+        const uint32_t idesc2 = amn ? (bmn ? make_idesc_bf16(kPairM, kPairN, 1, 1) : make_idesc_bf16(kPairM, kPairN, 1, 0))
+                                    : (bmn ? make_idesc_bf16(kPairM, kPairN, 0, 1) : idesc);
+        const uint64_t ad0 = make_sdesc_sw128(a0, amn ? 8192 : 0, 1024), bd0 = make_sdesc_sw128(b0, bmn ? 8192 : 0, 1024);
+        const uint32_t ak = amn ? 128 : 2, bk = bmn ? 128 : 2;
         mbar_arrive(&bar[0]);   // complete phase 0 so waits on parity 0 return at once
         for (int i = 0; i < n_mma / 4; ++i) {
           if (commit_every & 1) mbar_wait(&bar[0], 0);
           if (commit_every & 2) tc_fence_after();
 #pragma unroll
           for (int k = 0; k < 4; ++k)
-            mma_bf16_pair(tmem + (i & 1) * 256, ad0 + 2 * k, bd0 + 2 * k, idesc, 1);
+            mma_bf16_pair(tmem + (i & 1) * 256, ad0 + ak * k, bd0 + bk * k, idesc2, 1);
           if (commit_every & 4) mma_commit_pair(&bar[0] + 0, 0x1);
         }
       }

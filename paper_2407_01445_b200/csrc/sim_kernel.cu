@@ -121,6 +121,99 @@ __device__ __forceinline__ void stats_masked(const uint32_t (&r)[32], float kap,
   }
 }
 
+// Column sums of a warp's 32-row x N-column piece (N = 32 or 8): lane l holds row l's N
+// values; the rows are folded pairwise (xor 16 .. N), then log2(N) xor-halving steps leave the
+// sum of column (l % N) in lane l (31 shuffles per array for N = 32).
+template <int N>
+__device__ __forceinline__ float transpose_reduce(float (&v)[N], uint32_t lane) {
+#pragma unroll
+  for (int w = 16; w >= N; w >>= 1)
+#pragma unroll
+    for (int k = 0; k < N; ++k) v[k] += __shfl_xor_sync(0xffffffffu, v[k], w);
+#pragma unroll
+  for (int w = N / 2; w >= 1; w >>= 1) {
+    const bool upper = (lane & w) != 0;
+#pragma unroll
+    for (int k = 0; k < w; ++k) {
+      const float send = upper ? v[k] : v[k + w];
+      const float keep = upper ? v[k + w] : v[k];
+      v[k] = keep + __shfl_xor_sync(0xffffffffu, send, w);
+    }
+  }
+  return v[0];
+}
+
+// Two arrays reduced in lock-step (twice the independent shuffles per halving step).
+__device__ __forceinline__ void transpose_reduce2(float (&v)[32], float (&u)[32], uint32_t lane, float& sv, float& su) {
+#pragma unroll
+  for (int w = 16; w >= 1; w >>= 1) {
+    const bool upper = (lane & w) != 0;
+#pragma unroll
+    for (int k = 0; k < w; ++k) {
+      const float sv_ = upper ? v[k] : v[k + w];
+      const float kv = upper ? v[k + w] : v[k];
+      const float su_ = upper ? u[k] : u[k + w];
+      const float ku = upper ? u[k + w] : u[k];
+      v[k] = kv + __shfl_xor_sync(0xffffffffu, sv_, w);
+      u[k] = ku + __shfl_xor_sync(0xffffffffu, su_, w);
+    }
+  }
+  sv = v[0];
+  su = u[0];
+}
+
+// FUSED fast path (one temperature, no clamp possible, no diagonal / ragged element in the
+// chunk): x = 2^(s kappa) once per element serves the row (R) and the column (C) statistics,
+// e_row = 2^beta_i x, e_col = 2^beta_j x. Row raw sums {sum x, sum z x} (z = s kappa)
+// accumulate per thread; lane c gets column c's raw sums from the transposed reductions.
+__device__ __forceinline__ void fused_fast(const uint32_t (&r)[32], float kap, float2& rx, float2& rzx, uint32_t lane,
+                                           float& cx, float& czx) {
+  const float2 k2 = f2(kap, kap);
+  float x[32], zx[32];
+#pragma unroll
+  for (int k = 0; k < 32; k += 2) {
+    const float2 z = __fmul2_rn(f2(__uint_as_float(r[k]), __uint_as_float(r[k + 1])), k2);
+    const float2 e = f2(ex2_approx(z.x), ex2_approx(z.y));
+    const float2 ze = __fmul2_rn(z, e);
+    rx = __fadd2_rn(rx, e);
+    rzx = __fadd2_rn(rzx, ze);
+    x[k] = e.x; x[k + 1] = e.y;
+    zx[k] = ze.x; zx[k + 1] = ze.y;
+  }
+  transpose_reduce2(x, zx, lane, cx, czx);
+}
+
+// FUSED exact path for one 8-column piece (rare: diagonal / ragged / clamp-capable chunks):
+// both exponentials with the safe_exp clamp, masks and clamp counts; the lanes of quarter q of
+// the warp get their column's exact {sum e, sum y e}.
+__device__ __forceinline__ void fused_masked(const uint32_t (&r)[8], float2 rs, const float2* __restrict__ cs, int c0,
+                                             int cols, int gi, bool row_ok, uint32_t lane, int q, float& se,
+                                             float& sye, uint32_t& ncl, float& ce, float& cye) {
+  float x[8], yx[8];
+  // lane l loads column (c0 + l % 8)'s parameters once; element k reads them by shuffle
+  const int jl = c0 + static_cast<int>(lane & 7);
+  const float2 cl = jl < cols ? cs[jl] : f2(0.f, 0.f);
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const int j = c0 + k;
+    const bool ok = row_ok && (j < cols) && (j != gi);
+    const float s = __uint_as_float(r[k]);
+    const float yr = fmaf(s, rs.x, rs.y);
+    const float yc = fmaf(s, __shfl_sync(0xffffffffu, cl.x, k), __shfl_sync(0xffffffffu, cl.y, k));
+    const float er = ex2_approx(fminf(yr, kClampLog2));
+    const float ec = ex2_approx(fminf(yc, kClampLog2));
+    se += ok ? er : 0.f;
+    sye += ok ? yr * er : 0.f;
+    ncl += (ok && yr > kClampLog2) ? 1u : 0u;
+    ncl += (ok && yc > kClampLog2) ? 1u : 0u;
+    x[k] = ok ? ec : 0.f;
+    yx[k] = ok ? yc * ec : 0.f;
+  }
+  const float a = transpose_reduce<8>(x, lane);
+  const float b = transpose_reduce<8>(yx, lane);
+  if ((lane >> 3) == static_cast<uint32_t>(q)) { ce = a; cye = b; }
+}
+
 // Q with one temperature for every anchor (kappa_i = kappa_j): the two exponentials share
 // 2^(s kappa), so Q'_ij = 2^(s kappa) (fac_i + fac_j) with fac_a = coef_a 2^beta_a -- one
 // MUFU ex2 per element instead of two (pass 2 is otherwise SFU-bound at the MMA rate).
@@ -182,13 +275,24 @@ __device__ __forceinline__ void q_chunk(const uint32_t (&r)[32], float rk, float
 
 }  // namespace
 
+// Epilogue width per mode: FUSED runs 8 epilogue warps (128 columns each) so that its wider
+// per-chunk working set (two 32-column transposes) fits the register file; the others run 16.
 template <int kMode>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kSimThreads, 1)
+struct SimCfg {
+  static constexpr int kEpi = kMode == kSimFused ? 8 : kSimEpiWarps;
+  static constexpr int kThreads = (kEpi + 2) * 32;
+  static constexpr int kColsW = kPairN / (kEpi / 4);   // columns per epilogue warp
+  static constexpr int kChunksW = kColsW / 32;
+};
+
+template <int kMode>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(SimCfg<kMode>::kThreads, 1)
     sim_tile_kernel(const __grid_constant__ SimParams p, const __grid_constant__ CUtensorMap mapA0,
                     const __grid_constant__ CUtensorMap mapB0, const __grid_constant__ CUtensorMap mapA1,
                     const __grid_constant__ CUtensorMap mapB1, const __grid_constant__ CUtensorMap mapQo0,
                     const __grid_constant__ CUtensorMap mapQo1, float* __restrict__ raw_out) {
   constexpr int kStagesB = kMode == kSimQ ? kSimStagesQ : kSimStagesStats;
+  constexpr bool kStatsLike = kMode == kSimStats || kMode == kSimFused;
   extern __shared__ uint8_t smem_raw[];
   long long g_entry = 0;
   if (p.debug == 9) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_entry));
@@ -203,7 +307,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kSimThreads, 1)
   // warp roles: epilogue warps first, producer and MMA issuer LAST -- the SMSP arbiter
   // favours the highest warp id, so the single-thread TMA/MMA issue never waits behind
   // the epilogue math.
-  constexpr uint32_t kProdWarp = kSimEpiWarps, kMmaWarp = kSimEpiWarps + 1;
+  constexpr int kEpi = SimCfg<kMode>::kEpi;
+  constexpr int kColsW = SimCfg<kMode>::kColsW;
+  constexpr int kChunksW = SimCfg<kMode>::kChunksW;
+  constexpr uint32_t kProdWarp = kEpi, kMmaWarp = kEpi + 1;
   if (warp == kProdWarp && lane == 0) {
     tma_prefetch(&mapA0);
     tma_prefetch(&mapB0);
@@ -223,11 +330,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kSimThreads, 1)
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&L.tfull[i], 1);                    // MMA commit (multicast)
-      mbar_init(&L.tempty[i], 2 * kSimEpiWarps);    // one arrive per epilogue warp of the pair
+      mbar_init(&L.tempty[i], 2 * kEpi);            // one arrive per epilogue warp of the pair
     }
     for (int i = 0; i < kSimPSlots; ++i) {
       mbar_init(&L.pfull[i], 1);                    // local producer + bulk-copy bytes
-      mbar_init(&L.pempty[i], kSimEpiWarps);        // local epilogue warps
+      mbar_init(&L.pempty[i], kEpi);                // local epilogue warps
     }
     fence_barrier_init();
   }
@@ -392,11 +499,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kSimThreads, 1)
     }
   } else {
     // ===================== epilogue (both CTAs) =====================
+    if constexpr (kStatsLike) {
+      // While the first tiles load and multiply (two TMEM buffers of slack), the epilogue
+      // warps zero this CTA's slice of the gradient outputs for the GEMM of this step.
+      if (p.zero_a) {
+        const long long nthr = static_cast<long long>(gridDim.x) * kEpi * 32;
+        const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+        for (long long g = blockIdx.x * (kEpi * 32) + threadIdx.x; g < p.zero_n4; g += nthr) {
+          p.zero_a[g] = z;
+          p.zero_b[g] = z;
+        }
+      }
+    }
     const uint32_t q4 = warp & 3;               // TMEM lane quarter accessible to this warp
     long long e_wait = 0, e_ld = 0, e_math = 0, e_t0 = clock64(), e_g0 = 0;
     const bool eprof = p.debug == 9 && warp == 5;
     if (eprof) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(e_g0));
-    const uint32_t cq = warp >> 2;        // 64-column quarter of the 256-wide tile
+    const uint32_t cq = warp >> 2;        // column group (kColsW wide) of the 256-wide tile
     int it = 0;
     for (int item = it_lo; item < it_hi; ++item, ++it) {
       int s, rb, jt;
@@ -410,12 +529,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kSimThreads, 1)
       const bool warp_rows_ok = warp_row0 + 32 <= sg.rows;
       const int g0 = sg.a_row0 + warp_row0;     // global index of lane 0's anchor
       const int gi = g0 + static_cast<int>(lane);
-      const int colq = jt * kPairN + static_cast<int>(cq) * 64;
+      const int colq = jt * kPairN + static_cast<int>(cq) * kColsW;
 
       float2 rstat = make_float2(0.f, 0.f);
       float rk = 0.f, rbeta = 0.f, rc = 0.f, rf = 0.f;
       if (row_ok) {
-        if constexpr (kMode == kSimStats) rstat = sg.row_stat[r_loc];
+        if constexpr (kStatsLike) rstat = sg.row_stat[r_loc];
         if constexpr (kMode == kSimQ) {
           rk = sg.row_kappa[r_loc];
           rbeta = sg.row_beta[r_loc];
@@ -424,14 +543,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kSimThreads, 1)
         }
       }
 
+      // every global load of the tile is issued before the accumulator wait (latency hidden)
+      const float bnd0 = p.bounds[0], bnd1 = p.bounds[1];
+      float2 cst_all[kMode == kSimFused ? kChunksW : 1];
+      if constexpr (kMode == kSimFused) {
+#pragma unroll
+        for (int h = 0; h < kChunksW; ++h) {
+          const int jc = colq + 32 * h + static_cast<int>(lane);
+          cst_all[h] = jc < sg.cols ? sg.col_stat[jc] : f2(0.f, 0.f);
+        }
+      }
       long long ta = eprof ? clock64() : 0;
       mbar_wait(&L.tfull[acc], acc_phase);
       long long tb = eprof ? clock64() : 0;
       if (eprof) e_wait += tb - ta;
       tc_fence_after();
       // safe_exp can only clamp if some exponent may exceed 60: |s| <= |E1|max |E2|max bounds it
-      const float smax = sqrtf(p.bounds[0] * p.bounds[1]) * 1.0001f;
-      const uint32_t taddr = tmem_base + ((q4 * 32u) << 16) + acc * kPairN + cq * 64u;
+      const float smax = sqrtf(bnd0 * bnd1) * 1.0001f;
+      const uint32_t taddr = tmem_base + ((q4 * 32u) << 16) + acc * kPairN + cq * kColsW;
       float2 se2 = f2(0.f, 0.f), sye2 = f2(0.f, 0.f);
       float se = 0.f, sye = 0.f;
       uint32_t ncl = 0;
@@ -441,7 +570,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kSimThreads, 1)
       if constexpr (kMode == kSimQ) {
         ps = it % kSimPSlots;
         mbar_wait(&L.pfull[ps], (it / kSimPSlots) & 1);
-        par = L.par + ps * (kSimPSlotBytes / 4) + cq * 64;
+        par = L.par + ps * (kSimPSlotBytes / 4) + cq * kColsW;
         q_col_safe = 2.f * smax * p.bounds[2] <= kClampLog2;
         // factorized form: 2^(s kappa) stays within [2^-63, 2^63] and fac within fp32 range
         q_fact = p.q_factor && __all_sync(0xffffffffu, rk * smax <= kFactMaxLog2);
@@ -449,12 +578,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kSimThreads, 1)
       const float row_kap = kMode == kSimQ ? rk : rstat.x;
       const float row_beta = kMode == kSimQ ? rbeta : rstat.y;
       const bool row_safe = !__any_sync(0xffffffffu, row_ok && fmaf(smax, row_kap, row_beta) > kClampLog2);
+      // FUSED one-exponential form: 2^(s kappa) and 2^beta stay inside [2^-63, 2^63]
+      const bool fused_ok = kMode == kSimFused && __all_sync(0xffffffffu, row_kap * smax <= kFactMaxLog2);
 #pragma unroll 1
-      for (int h = 0; h < 2; ++h) {
-        uint32_t rr[32];
-        tmem_ld_32x32b_x32(taddr + 32 * h, rr);
-        tmem_ld_wait();
-        if (h == 1) {   // the tile is in registers: hand the TMEM buffer back to the MMA warp
+      for (int h = 0; h < kChunksW; ++h) {
+        uint32_t rr[kMode == kSimFused ? 1 : 32];
+        if constexpr (kMode != kSimFused) {
+          tmem_ld_32x32b_x32(taddr + 32 * h, rr);
+          tmem_ld_wait();
+        }
+        if (kMode != kSimFused && h == kChunksW - 1) {   // the tile is in registers: hand the TMEM buffer back
           tc_fence_before();
           __syncwarp();
           if (lane == 0) {
@@ -476,6 +609,55 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kSimThreads, 1)
         } else if constexpr (kMode == kSimStats) {
           if (interior && warp_rows_ok && row_safe) stats_fast(rr, rstat.x, rstat.y, se2, sye2);
           else stats_masked(rr, rstat.x, rstat.y, col0, sg.cols, gi, row_ok, se, sye, ncl);
+        } else if constexpr (kMode == kSimFused) {
+          // column anchor of this lane (the statistics it collects) and its parameters
+          const int jc = col0 + static_cast<int>(lane);
+          float2 cst = cst_all[0];
+#pragma unroll
+          for (int q = 1; q < kChunksW; ++q)
+            if (h == q) cst = cst_all[q];
+          const bool col_safe = !__any_sync(0xffffffffu, jc < sg.cols && fmaf(smax, cst.x, cst.y) > kClampLog2);
+          const bool fast = p.fuse_fast && interior && warp_rows_ok && row_safe && col_safe && fused_ok;
+          uint32_t r32[32];
+          tmem_ld_32x32b_x32(taddr + 32 * h, r32);
+          tmem_ld_wait();
+          if (h == kChunksW - 1) {   // the tile is in registers: release the TMEM buffer
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) {
+              if (rank == 0) mbar_arrive(&L.tempty[acc]);
+              else mbar_arrive_cluster(&L.tempty[acc], 0);
+            }
+          }
+          float ce = 0.f, cye = 0.f;
+          if (fast) {
+            fused_fast(r32, rstat.x, se2, sye2, lane, ce, cye);
+          } else {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              uint32_t r8[8];
+#pragma unroll
+              for (int k = 0; k < 8; ++k) r8[k] = r32[8 * q + k];
+              fused_masked(r8, rstat, sg.col_stat, col0 + 8 * q, sg.cols, gi, row_ok, lane, q, se, sye, ncl, ce, cye);
+            }
+          }
+          if (fast) {   // raw {sum x, sum z x} -> {sum e, sum y e} with 2^beta_j (|beta_j| <= 63)
+            const float sc = ex2_approx(cst.y);
+            cye = sc * fmaf(cst.y, ce, cye);
+            ce = sc * ce;
+          }
+          if (jc < sg.cols)
+            p.col_partial[static_cast<size_t>(rb * 8 + rank * 4 + q4) * sg.cols + jc] = f2(ce, cye);
+          if (h & 1) {   // 64 columns done: one row partial per (row, column quarter)
+            // fast-path row raw sums {sum x, sum z x} -> e = 2^beta_i x, y e = (z + beta_i) e
+            const float sc = ex2_approx(rstat.y);
+            const float rx = se2.x + se2.y, rzx = sye2.x + sye2.y;
+            const float sxe = sc * fmaf(rstat.y, rx, rzx) + sye;
+            const int quarter = (static_cast<int>(cq) * kColsW + 32 * h) / 64;
+            if (row_ok)
+              sg.partial[static_cast<size_t>(r_loc) * (p.n_jt * 4) + jt * 4 + quarter] = make_float2(se + sc * rx, sxe);
+            se2 = f2(0.f, 0.f); sye2 = f2(0.f, 0.f); se = 0.f; sye = 0.f;
+          }
         } else {  // kSimQ
           uint32_t packed[16];
           const float* kc = par + 32 * h;
@@ -507,6 +689,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kSimThreads, 1)
         }
       }
       long long tc = eprof ? clock64() : 0;
+      if constexpr (kMode == kSimFused) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) ncl += __shfl_xor_sync(0xffffffffu, ncl, o);
+        if (lane == 0 && ncl) atomicAdd(p.clamps, static_cast<unsigned long long>(ncl));
+      }
       if constexpr (kMode == kSimStats) {
         const float sxe = sye2.x + sye2.y + sye;   // sum y e; the table kernel divides by kappa
         se += se2.x + se2.y;
@@ -550,6 +737,7 @@ cudaError_t sim_set_smem() {
   cudaError_t e = cudaFuncSetAttribute(sim_tile_kernel<kSimStats>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSimSmemBytes);
   if (e == cudaSuccess) e = cudaFuncSetAttribute(sim_tile_kernel<kSimQ>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSimSmemBytes);
   if (e == cudaSuccess) e = cudaFuncSetAttribute(sim_tile_kernel<kSimRaw>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSimSmemBytes);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(sim_tile_kernel<kSimFused>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSimSmemBytes);
   return e;
 }
 
@@ -563,13 +751,16 @@ cudaError_t launch_sim(int mode, const SimParams& p, const CUtensorMap* mapA, co
   grid &= ~1;
   switch (mode) {
     case kSimStats:
-      sim_tile_kernel<kSimStats><<<grid, kSimThreads, kSimSmemBytes, s>>>(p, mapA[0], mapB[0], a1, b1, q0, q1, raw_out);
+      sim_tile_kernel<kSimStats><<<grid, SimCfg<kSimStats>::kThreads, kSimSmemBytes, s>>>(p, mapA[0], mapB[0], a1, b1, q0, q1, raw_out);
+      break;
+    case kSimFused:
+      sim_tile_kernel<kSimFused><<<grid, SimCfg<kSimFused>::kThreads, kSimSmemBytes, s>>>(p, mapA[0], mapB[0], a1, b1, q0, q1, raw_out);
       break;
     case kSimQ:
-      sim_tile_kernel<kSimQ><<<grid, kSimThreads, kSimSmemBytes, s>>>(p, mapA[0], mapB[0], a1, b1, q0, q1, raw_out);
+      sim_tile_kernel<kSimQ><<<grid, SimCfg<kSimQ>::kThreads, kSimSmemBytes, s>>>(p, mapA[0], mapB[0], a1, b1, q0, q1, raw_out);
       break;
     default:
-      sim_tile_kernel<kSimRaw><<<grid, kSimThreads, kSimSmemBytes, s>>>(p, mapA[0], mapB[0], a1, b1, q0, q1, raw_out);
+      sim_tile_kernel<kSimRaw><<<grid, SimCfg<kSimRaw>::kThreads, kSimSmemBytes, s>>>(p, mapA[0], mapB[0], a1, b1, q0, q1, raw_out);
       break;
   }
   return cudaGetLastError();

@@ -34,25 +34,46 @@ __global__ void fc_prep_kernel(const __nv_bfloat16* __restrict__ e1, const __nv_
   const int w = (blockIdx.x * blockDim.x + threadIdx.x) / 32;
   const int lane = threadIdx.x & 31;
   if (w == 0 && lane == 0) *a.clamps = 0ull;
-  const uint4* x4 = reinterpret_cast<const uint4*>(e1 + static_cast<size_t>(w) * a.d);
-  const uint4* y4 = reinterpret_cast<const uint4*>(e2 + static_cast<size_t>(w) * a.d);
+  const bool valid = w < a.B;
+  const int r = w - a.row0;
+  const bool lead = valid && lane == 0 && r >= 0 && r < a.Bl;   // this rank's anchor, lane 0
+  const uint4* x4 = reinterpret_cast<const uint4*>(e1 + static_cast<size_t>(valid ? w : 0) * a.d);
+  const uint4* y4 = reinterpret_cast<const uint4*>(e2 + static_cast<size_t>(valid ? w : 0) * a.d);
+  const int nv = valid ? a.d / 8 : 0;
+  // the row loads (two per lane at d = 512) and the id load are all issued before any use
+  constexpr int kPre = 2;
+  uint4 xs[kPre], ys[kPre];
+#pragma unroll
+  for (int i = 0; i < kPre; ++i) {
+    const int v = lane + 32 * i;
+    xs[i] = v < nv ? __ldg(x4 + v) : make_uint4(0u, 0u, 0u, 0u);
+    ys[i] = v < nv ? __ldg(y4 + v) : make_uint4(0u, 0u, 0u, 0u);
+  }
+  const int id = lead ? a.ids[r] : 0;
   float acc = 0.f, n1 = 0.f, n2 = 0.f;
-#pragma unroll 4
-  for (int v = lane; w < a.B && v < a.d / 8; v += 32) {
-    const uint4 x = __ldg(x4 + v);
-    const uint4 y = __ldg(y4 + v);
-    const uint32_t xs[4] = {x.x, x.y, x.z, x.w};
-    const uint32_t ys[4] = {y.x, y.y, y.z, y.w};
+  auto accum = [&](const uint4& x, const uint4& y) {
+    const uint32_t xx[4] = {x.x, x.y, x.z, x.w};
+    const uint32_t yy[4] = {y.x, y.y, y.z, y.w};
 #pragma unroll
     for (int t = 0; t < 4; ++t) {
-      const float2 fx = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&xs[t]));
-      const float2 fy = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&ys[t]));
+      const float2 fx = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&xx[t]));
+      const float2 fy = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&yy[t]));
       acc = fmaf(fx.x, fy.x, acc);
       acc = fmaf(fx.y, fy.y, acc);
       n1 = fmaf(fx.x, fx.x, fmaf(fx.y, fx.y, n1));
       n2 = fmaf(fy.x, fy.x, fmaf(fy.y, fy.y, n2));
     }
+  };
+  // u^{t-1} / tau^t of the anchor's id: gathered here, off the table kernel's dependent chain
+  double uo1 = 0.0, uo2 = 0.0, t1 = 0.0, t2 = 0.0;
+  if (lead) {
+    if (a.track_u) { uo1 = a.u1_tab[id]; uo2 = a.u2_tab[id]; }
+    if (a.individual) { t1 = a.tau1_tab[id]; t2 = a.tau2_tab[id]; }
+    else { t1 = t2 = a.tau_state->tau; }
   }
+#pragma unroll
+  for (int i = 0; i < kPre; ++i) accum(xs[i], ys[i]);
+  for (int v = lane + 32 * kPre; v < nv; v += 32) accum(__ldg(x4 + v), __ldg(y4 + v));   // d > 512
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
     acc += __shfl_xor_sync(0xffffffffu, acc, o);
@@ -70,21 +91,12 @@ __global__ void fc_prep_kernel(const __nv_bfloat16* __restrict__ e1, const __nv_
     for (int k = 0; k < static_cast<int>(blockDim.x >> 5); ++k) m = fmaxf(m, bmax[threadIdx.x][k]);
     atomicMax(reinterpret_cast<int*>(a.bounds) + threadIdx.x, __float_as_int(m));
   }
-  if (lane != 0 || w >= a.B) return;
+  if (lane != 0 || !valid) return;
   a.diag[w] = acc;
-  const int r = w - a.row0;
-  if (r < 0 || r >= a.Bl) return;
-  double t1, t2;
-  const int id = a.ids[r];
-  if (a.track_u) {   // u^{t-1} for the table kernel, off its dependent-load chain
-    a.uold1[r] = a.u1_tab[id];
-    a.uold2[r] = a.u2_tab[id];
-  }
-  if (a.individual) {
-    t1 = a.tau1_tab[id];
-    t2 = a.tau2_tab[id];
-  } else {
-    t1 = t2 = a.tau_state->tau;
+  if (!lead) return;
+  if (a.track_u) {
+    a.uold1[r] = uo1;
+    a.uold2[r] = uo2;
   }
   a.t_loc1[r] = t1;
   a.t_loc2[r] = t2;
@@ -110,9 +122,19 @@ __device__ __forceinline__ void reduce_partials(const StepArgs& a, int r, bool v
   s1 = 0.0; x1 = 0.0; s2 = 0.0; x2 = 0.0;
   for (int q = sub; valid && q < nparts; q += kGroup) {
     const float2 u = __ldg(pr + q);
-    const float2 v = __ldg(pc + q);
     s1 += u.x; x1 += u.y;
-    s2 += v.x; x2 += v.y;
+  }
+  if (a.col_slots > 0) {   // fused pass 1: column statistics of S, slot-major
+    const float2* cp = a.col_partial + (a.row0 + r);
+    for (int q = sub; valid && q < a.col_slots; q += kGroup) {
+      const float2 v = __ldg(cp + static_cast<size_t>(q) * a.B);
+      s2 += v.x; x2 += v.y;
+    }
+  } else {
+    for (int q = sub; valid && q < nparts; q += kGroup) {
+      const float2 v = __ldg(pc + q);
+      s2 += v.x; x2 += v.y;
+    }
   }
 #pragma unroll
   for (int o = kGroup / 2; o > 0; o >>= 1) {
@@ -230,6 +252,17 @@ __device__ __forceinline__ void store_payload(const StepArgs& a, int r, int id, 
 
 __device__ void block_partials(const StepArgs& a, double ta, double tb, double tl, float kmax);
 
+// Zeroes the step's gradient outputs (the GEMM reduce-adds every stream-K unit into them).
+// Launched on the side branch while pass 1 runs: one small block per SM, no shared memory,
+// so it fits beside a persistent similarity CTA.
+__global__ void __launch_bounds__(256) fc_zero_kernel(float4* a0, float4* a1, long long n4) {
+  const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (long long g = blockIdx.x * blockDim.x + threadIdx.x; g < n4; g += static_cast<long long>(gridDim.x) * blockDim.x) {
+    a0[g] = z;
+    a1[g] = z;
+  }
+}
+
 // K > 1, before the payload all-gather: lane group per local anchor -> g, u update, payload.
 __global__ void fc_table_kernel(StepArgs a) {
   const int r = (blockIdx.x * blockDim.x + threadIdx.x) / kGroup;
@@ -268,7 +301,8 @@ __global__ void fc_weights_kernel(StepArgs a) {
     kmax = fmaxf(p.k1, p.k2);
     if (k == a.rank) {
       const double s1 = a.sum1[r], s2 = a.sum2[r];
-      a.rcoef[r] = static_cast<float>(p.c1 * s1 + p.c2 * s2);
+      const float rc = static_cast<float>(p.c1 * s1 + p.c2 * s2);
+      a.rcoef[r] = rc;
       local_terms(a, r, p, u1, u2, a.g1[r], a.g2[r], a.dx1[r], a.dx2[r], eps, ta, tb, tl);
     }
   }

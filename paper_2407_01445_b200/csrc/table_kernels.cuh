@@ -44,7 +44,9 @@ struct StepArgs {
   TauState* tau_state;
   // pass-1 products
   float2* rowstat_R; float2* rowstat_C;   // [Bl]
-  float2* partial_R; float2* partial_C;   // [Bl][n_jt*2]
+  float2* partial_R; float2* partial_C;   // [Bl][n_jt*4]
+  const float2* col_partial;             // fused pass 1 (K = 1): segment-C stats [col_slots][B]
+  int col_slots;                         // 0: segment-C stats are row partials in partial_C
   unsigned long long* clamps;
   float* bounds;                         // {max |E1|^2, max |E2|^2, max kappa} (atomicMax on float bits)
   // per-local-anchor fp64 state of the step
@@ -69,6 +71,7 @@ struct StepArgs {
   int fuse_finalize;                     // K == 1: temperature step in the reduce kernel
   int* err;
   StepResult* result;
+  float gscale;                          // c = 1 / (Bl (B-1)), engine.cpp:84-85
 };
 
 __global__ void fc_prep_kernel(const __nv_bfloat16* __restrict__ e1, const __nv_bfloat16* __restrict__ e2,
@@ -76,6 +79,7 @@ __global__ void fc_prep_kernel(const __nv_bfloat16* __restrict__ e1, const __nv_
 __global__ void fc_table_kernel(StepArgs a);
 __global__ void fc_weights_kernel(StepArgs a);
 __global__ void fc_anchor_kernel(StepArgs a);
+__global__ void fc_zero_kernel(float4* a0, float4* a1, long long n4);
 __global__ void fc_reduce_kernel(StepArgs a);
 __global__ void fc_finalize_kernel(StepArgs a);
 __global__ void fc_indiv_update_kernel(StepArgs a);

@@ -2,6 +2,7 @@
 import ctypes as C, os, sys, numpy as np, torch
 sys.path.insert(0, '.')
 os.environ['FC_SIM_DEBUG'] = '9'
+os.environ.setdefault('FC_GEMM_DEBUG', '9')
 os.environ['FC_GRAPH'] = '1'
 import paper_2407_01445_b200 as P
 from paper_2407_01445_b200 import synthetic as S
@@ -15,7 +16,7 @@ ids = torch.from_numpy(S.ids(B, N, 0)).cuda()
 for _ in range(3): st.step(e1, e2, ids, 0.6, 1e-14)
 torch.cuda.synchronize()
 R = 2688
-out = np.zeros(2 * R, dtype=np.int64)
+out = np.zeros(2 * R + 160 * 16, dtype=np.int64)
 P.lib().fc_debug_counters(st._h, out.ctypes.data_as(C.POINTER(C.c_longlong)))
 for k, name in enumerate(('pass1', 'pass2')):
     reg = out[k * R:(k + 1) * R]
@@ -32,3 +33,15 @@ st.enable_phase_timing(5)
 for _ in range(5): st.step(e1, e2, ids, 0.6, 1e-14)
 torch.cuda.synchronize()
 print('phases (debug9 build)', {k: round(v * 1e3, 1) for k, v in st.phase_times(4).items()})
+g = out[2 * R:2 * R + 160 * 16].reshape(160, 16)[:148]
+if os.environ.get('FC_GEMM_DEBUG') in ('9', '10'):
+    ld = g[0::2]   # pair leaders (MMA counters)
+    t0 = g[:, 11].min()
+    us = lambda x: np.round(np.percentile((x - t0) / 1e3, [0, 50, 100]), 2)
+    print(f'GEMM: MMA-warp cycles total {ld[:, 0].mean():.0f} (max {ld[:, 0].max()}) waits: tempty {ld[:, 1].mean():.0f} full {ld[:, 2].mean():.0f} first {ld[:, 3].mean():.0f}; units {ld[:, 4].min()}-{ld[:, 4].max()}')
+    print(f'   epilogue warp0 cycles total {g[:, 8].mean():.0f} wait tfull {g[:, 9].mean():.0f}')
+    print('   timeline us: entry', us(g[:, 11]), 'MMA end', us(ld[:, 5]), 'epi end', us(g[:, 10]))
+for pp in (1, 2):
+    n = C.c_int(0)
+    P.lib().fc_debug_gemm_clusters(pp, C.byref(n))
+    print(f'GEMM pairs/cluster {pp}: max active clusters {n.value}')
