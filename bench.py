@@ -204,6 +204,7 @@ def main():
     from paper_2407_01445_b200 import synthetic as S
 
     world, rank, local = dist_env()
+    os.environ.setdefault("NCCL_DEBUG", "WARN")   # keep rank 0's stdout to the one JSON line
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
@@ -238,11 +239,17 @@ def main():
         if world > 1:
             tdist.barrier()
 
+    def note(msg):
+        if os.environ.get("FC_BENCH_TRACE"):
+            print(f"[bench rank {rank}] {msg}", file=sys.stderr, flush=True)
+
+    note("init done")
     for i in range(args.warmup):
         e1, e2, ids = dev_sets[i % n_sets]
         step.step(e1, e2, ids, gamma, eps, de1, de2, stream)
     torch.cuda.synchronize()
     sc = step.scalars()
+    note("warmup done")
 
     # ---------------- device-timed steps (CUDA-graph replay, no host sync inside) ----------------
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
@@ -269,6 +276,7 @@ def main():
         total_ms = float(t.item())
     ms_per_step = total_ms / args.steps
     value = 1e3 / ms_per_step
+    note("timed steps done")
 
     # ---------------- per-kernel durations: CUDA events between the step's phases ----------------
     # (event-record nodes inside the replayed graph, same stream, same inputs; K more steps)
@@ -289,6 +297,7 @@ def main():
             phase_sum[k] += v
     phases = {k: v / args.steps for k, v in phase_sum.items()}
     step.disable_phase_timing()
+    note("phase timing done")
 
     # ---------------- end to end through the public API (host buffers) ----------------
     e2e = None
@@ -372,9 +381,12 @@ def main():
             "phases_ms": phases, "clocks": clk, "cpu_baseline": cpu,
             "last_step": {"loss": sc.loss, "gtau": sc.gtau, "tau": sc.tau, "exp_clamps": sc.exp_clamps}}
     print(json.dumps(line), flush=True)
-    if world > 1:
+    if world > 1:   # torch's process group first, then the loss step's own communicator
         tdist.barrier()
         tdist.destroy_process_group()
+        note("process group destroyed")
+    step.close()
+    note("loss step closed")
     return 0
 
 

@@ -546,7 +546,14 @@ struct LossStep {
   }
 
   void destroy() {
-    if (comm) ncclCommDestroy(comm);
+    // graphs first: NCCL keeps the communicator alive while a graph holds captured collectives
+    cudaDeviceSynchronize();
+    for (auto& g : graphs) cudaGraphExecDestroy(g.exec);
+    graphs.clear();
+    if (comm) {
+      cudaDeviceSynchronize();
+      ncclCommDestroy(comm);
+    }
     for (void* p : {(void*)u1, (void*)u2, (void*)tau1, (void*)tau2, (void*)m1, (void*)v1, (void*)m2, (void*)v2,
                     (void*)s1, (void*)s2, (void*)tau_state, (void*)e1g, (void*)e2g, (void*)diag, (void*)rowstat,
                     (void*)partial, (void*)col_partial, (void*)clamps, (void*)bounds, (void*)f64, (void*)red, (void*)par, (void*)rcoef, (void*)blockpart,
@@ -555,8 +562,6 @@ struct LossStep {
     if (recv && recv != send) cudaFree(recv);
     if (send) cudaFree(send);
     if (result_h) cudaFreeHost(result_h);
-    for (auto& g : graphs) cudaGraphExecDestroy(g.exec);
-    graphs.clear();
     if (scal) cudaFree(scal);
     if (ws) cudaStreamDestroy(ws);
     if (ws2) cudaStreamDestroy(ws2);

@@ -295,6 +295,11 @@ __global__ void fc_weights_kernel(StepArgs a) {
     const double* blk = a.recv + static_cast<size_t>(k) * 5 * a.Bl;
     const double u1 = blk[r], u2 = blk[a.Bl + r];
     const double t1 = blk[2 * a.Bl + r], t2 = blk[3 * a.Bl + r];
+    if (a.track_u && k != a.rank) {   // keep this rank's full u replica equal to the shared UTable
+      const int id = static_cast<int>(blk[4 * a.Bl + r]);
+      a.u1_tab[id] = u1;
+      a.u2_tab[id] = u2;
+    }
     const float s_ii = a.diag[i];
     const AnchorParams p = anchor_params(a, u1, u2, t1, t2, a.tau_state->tau, eps);
     store_params(a, i, p, s_ii);
