@@ -172,6 +172,25 @@ def reference_arm(args):
     return 0
 
 
+def ncu_traffic(phase):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of the phase's kernel, from the
+    newest committed ncu --set full summary (profiles/<round>_traffic.json); None if absent."""
+    import glob
+    kern = {"pass1_stats": ("sim_tile_kernel<3>", "sim_tile_kernel<0>"), "pass2_q": ("sim_tile_kernel<1>",),
+            "grad_gemm": ("grad_gemm_kernel<1>", "grad_gemm_kernel<2>")}.get(phase, ())
+    files = sorted(glob.glob(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "*_traffic.json")))
+    if not files:
+        return None
+    try:
+        tab = json.load(open(files[-1]))["bytes_per_launch"]
+    except (OSError, ValueError, KeyError):
+        return None
+    for k in kern:
+        if k in tab:
+            return {"bytes": tab[k], "kernel": k, "source": os.path.relpath(files[-1], os.path.dirname(os.path.abspath(__file__)))}
+    return None
+
+
 def workload_config(args, world):
     return {"workload": f"{args.variant} loss+grad step, global B={args.batch}, d={args.dim}, "
                         f"N={args.n_train} u table (BASELINE.json metric config)",
@@ -357,7 +376,8 @@ def main():
     t_dom = phases[dom] * 1e-3
     ach = per_kernel_flops[dom] / t_dom / 1e12 if t_dom > 0 else 0.0
     roofline = {"bound": "tensor", "kernel": dom, "achieved": ach, "peak": peak, "unit": "TFLOP/s",
-                "frac": ach / peak, "traffic": None, "peak_kind": f"{peak_kind} bf16 burst",
+                "frac": ach / peak, "traffic": (ncu_traffic(dom) or {}).get("bytes"),
+                "traffic_source": ncu_traffic(dom), "peak_kind": f"{peak_kind} bf16 burst",
                 "executed_tflops": exec_flops[dom] / t_dom / 1e12 if t_dom > 0 else 0.0,
                 "algorithmic_flops_per_launch": per_kernel_flops[dom]}
     step_ach = step_flops / (ms_per_step * 1e-3) / 1e12
