@@ -112,7 +112,8 @@ struct LossStep {
   unsigned long long* clamps = nullptr;
   float* bounds = nullptr;
   double* f64 = nullptr;   // per-local-anchor fp64 arrays
-  double *send = nullptr, *recv = nullptr, *gt_recv = nullptr, *red = nullptr, *blockpart = nullptr;
+  double *send = nullptr, *recv = nullptr, *red = nullptr;
+  int nblk = 0, pstride = 0;   // payload: [u1|u2|t1|t2|id|gt1|gt2] x Bl + nblk x 3 block partials
   float* par = nullptr;   // 6 x [n_jt*256]: kap1, bet1, coef1, kap2, bet2, coef2
   float* rcoef = nullptr;
   __nv_bfloat16* q = nullptr;   // [2][Bl][ldq]
@@ -217,12 +218,11 @@ struct LossStep {
     clamps = dalloc<unsigned long long>(1);
     bounds = dalloc<float>(4);
     f64 = dalloc<double>(static_cast<size_t>(Bl) * 18);
-    send = dalloc<double>(5 * static_cast<size_t>(Bl));
-    recv = K > 1 ? dalloc<double>(5 * static_cast<size_t>(B)) : send;
-    gt_recv = K > 1 ? dalloc<double>(2 * static_cast<size_t>(B)) : nullptr;
+    nblk = (Bl * 8 + kAnchorBlock - 1) / kAnchorBlock;
+    pstride = 7 * Bl + 3 * nblk;
+    send = dalloc<double>(static_cast<size_t>(pstride));
+    recv = K > 1 ? dalloc<double>(static_cast<size_t>(K) * pstride) : send;
     red = dalloc<double>(2);
-    blockpart = dalloc<double>(3 * static_cast<size_t>(std::max((B + kWeightsBlock - 1) / kWeightsBlock,
-                                                                 (Bl * 8 + kAnchorBlock - 1) / kAnchorBlock)));
     par = dalloc<float>(8 * static_cast<size_t>(n_jt) * fc::kPairN);
     FC_CUDA(cudaMemset(par, 0, 8 * static_cast<size_t>(n_jt) * fc::kPairN * 4));
     rcoef = dalloc<float>(Bl);
@@ -292,17 +292,17 @@ struct LossStep {
     a.sum1 = F(2); a.dx1 = F(3); a.sum2 = F(4); a.dx2 = F(5);
     a.g1 = F(6); a.g2 = F(7); a.u1 = F(8); a.u2 = F(9);
     a.term_a = F(10); a.term_b = F(11); a.term_loss = F(12);
-    a.gt1 = F(13); a.gt2 = F(14);   // contiguous [gt1 | gt2]
+    a.gt1 = send + 5 * static_cast<size_t>(Bl); a.gt2 = send + 6 * static_cast<size_t>(Bl);   // payload columns
     a.uold1 = F(15); a.uold2 = F(16);
     a.send = send; a.recv = recv;
-    a.gt_recv = K > 1 ? gt_recv : F(13);
+    a.pstride = pstride; a.nblk = nblk;
     const size_t np = static_cast<size_t>(n_jt) * fc::kPairN;
     a.kap1 = par; a.bet1 = par + np; a.coef1 = par + 2 * np;
     a.kap2 = par + 3 * np; a.bet2 = par + 4 * np; a.coef2 = par + 5 * np;
     a.fac1 = par + 6 * np; a.fac2 = par + 7 * np;
     a.rcoef = rcoef;
-    a.blockpart = blockpart;
-    a.fuse_finalize = K == 1 ? 1 : 0; a.red = red; a.err = err; a.result = result_d;
+    a.blockpart = send + 7 * static_cast<size_t>(Bl);
+    a.red = red; a.err = err; a.result = result_d;
   }
 
   void ensure_maps(const void* e1, const void* e2) {
@@ -442,34 +442,25 @@ struct LossStep {
 
     // ---- u table, payload, (all-gather), weights, reductions, tau update ----
     mark(3, st);
-    if (K == 1) {
-      // table + weights in one kernel; the G_tau reduction, temperature step and IndividualTemp
-      // update only feed the next step and the step scalars: they run on the side branch
-      a.n_blockpart = (Bl * 8 + kAnchorBlock - 1) / kAnchorBlock;
-      fc::fc_anchor_kernel<<<a.n_blockpart, kAnchorBlock, 0, st>>>(a);
-      FC_CUDA(cudaGetLastError());
-      FC_CUDA(cudaEventRecord(side_fork, st));
-      FC_CUDA(cudaStreamWaitEvent(ws2, side_fork, 0));
-      fc::fc_reduce_kernel<<<1, 32, 0, ws2>>>(a);
-      if (indiv) fc::fc_indiv_update_kernel<<<(B + 255) / 256, 256, 0, ws2>>>(a);
-      FC_CUDA(cudaGetLastError());
-      FC_CUDA(cudaEventRecord(side_join, ws2));
-    } else {
-      fc::fc_table_kernel<<<(Bl * 8 + 255) / 256, 256, 0, st>>>(a);
-      FC_CUDA(cudaGetLastError());
-      FC_NCCL(ncclAllGather(send, recv, 5 * static_cast<size_t>(Bl), ncclFloat64, comm, st));
-      a.n_blockpart = (B + kWeightsBlock - 1) / kWeightsBlock;
-      fc::fc_weights_kernel<<<a.n_blockpart, kWeightsBlock, 0, st>>>(a);
-      fc::fc_reduce_kernel<<<1, 32, 0, st>>>(a);
-      FC_CUDA(cudaGetLastError());
-      FC_NCCL(ncclAllReduce(red, red, 2, ncclFloat64, ncclSum, comm, st));
-      if (indiv) {
-        FC_NCCL(ncclAllGather(a.gt1, gt_recv, 2 * static_cast<size_t>(Bl), ncclFloat64, comm, st));
-        fc::fc_indiv_update_kernel<<<(B + 255) / 256, 256, 0, st>>>(a);
-      }
-      fc::fc_finalize_kernel<<<1, 32, 0, st>>>(a);
+    // table update + weights + local G_tau / loss terms + payload, one lane group per anchor
+    a.n_blockpart = nblk;
+    fc::fc_anchor_kernel<<<nblk, kAnchorBlock, 0, st>>>(a);
+    FC_CUDA(cudaGetLastError());
+    if (K > 1) {
+      // ONE all-gather carries u/tau/id, the v2 per-index tau gradients and the G_tau / loss
+      // block partials of every rank (no scalar all-reduce, no second gather)
+      FC_NCCL(ncclAllGather(send, recv, static_cast<size_t>(pstride), ncclFloat64, comm, st));
+      fc::fc_weights_kernel<<<(B + kWeightsBlock - 1) / kWeightsBlock, kWeightsBlock, 0, st>>>(a);
       FC_CUDA(cudaGetLastError());
     }
+    // the G_tau reduction, temperature step and IndividualTemp update only feed the next step
+    // and the step scalars: they run on the side branch
+    FC_CUDA(cudaEventRecord(side_fork, st));
+    FC_CUDA(cudaStreamWaitEvent(ws2, side_fork, 0));
+    fc::fc_reduce_kernel<<<1, 32, 0, ws2>>>(a);
+    if (indiv) fc::fc_indiv_update_kernel<<<(B + 255) / 256, 256, 0, ws2>>>(a);
+    FC_CUDA(cudaGetLastError());
+    FC_CUDA(cudaEventRecord(side_join, ws2));
 
     // ---- pass 2: Q' tiles (bf16) for both segments ----
     for (int s = 0; s < 2; ++s) {
@@ -536,13 +527,13 @@ struct LossStep {
     FC_CUDA(fc::launch_gemm(gp, mQs, mX, mO, gemm_ctas, st));
     mark(6, st);
 
-    if (K == 1) FC_CUDA(cudaStreamWaitEvent(st, side_join, 0));
+    FC_CUDA(cudaStreamWaitEvent(st, side_join, 0));
     FC_CUDA(cudaMemcpyAsync(result_h, result_d, sizeof(fc::StepResult), cudaMemcpyDeviceToHost, st));
   }
 
   int kernels_per_step() const {
-    return 1 /*prep*/ + 1 /*pass1*/ + (K > 1 ? 2 : 1) /*table (+weights)*/ + 1 /*reduce*/ + (indiv ? 1 : 0) +
-           (K > 1 ? 1 : 0) /*finalize*/ + 1 /*zero dE*/ + 1 /*pass2*/ + 1 /*gemm*/;
+    return 1 /*prep*/ + 1 /*pass1*/ + 1 /*anchor*/ + (K > 1 ? 1 : 0) /*weights*/ + 1 /*reduce*/ + (indiv ? 1 : 0) +
+           1 /*zero dE*/ + 1 /*pass2*/ + 1 /*gemm*/;
   }
 
   void destroy() {
@@ -556,8 +547,8 @@ struct LossStep {
     }
     for (void* p : {(void*)u1, (void*)u2, (void*)tau1, (void*)tau2, (void*)m1, (void*)v1, (void*)m2, (void*)v2,
                     (void*)s1, (void*)s2, (void*)tau_state, (void*)e1g, (void*)e2g, (void*)diag, (void*)rowstat,
-                    (void*)partial, (void*)col_partial, (void*)clamps, (void*)bounds, (void*)f64, (void*)red, (void*)par, (void*)rcoef, (void*)blockpart,
-                    (void*)q, (void*)err, (void*)result_d, (void*)gt_recv})
+                    (void*)partial, (void*)col_partial, (void*)clamps, (void*)bounds, (void*)f64, (void*)red, (void*)par, (void*)rcoef,
+                    (void*)q, (void*)err, (void*)result_d})
       if (p) cudaFree(p);
     if (recv && recv != send) cudaFree(recv);
     if (send) cudaFree(send);

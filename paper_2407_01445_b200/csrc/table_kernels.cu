@@ -1,18 +1,20 @@
 // table_kernels.cu -- the per-anchor (O(B)) kernels of the FastCLIP loss step.
 //
-// These are HBM/latency-bound gather/scatter and scalar kernels (no tensor-core shape):
-//   fc_diag_kernel        S_ii = <E1_i, E2_i> for the global batch (fp32 from bf16)
-//   fc_rowpar_kernel      tau^t snapshot per local anchor (global tau or IndividualTemp
-//                         gather by id, state.cpp:112-122) -> pass-1 row parameters
-//   fc_table_kernel       fixed-order reduction of the pass-1 partials -> g (engine.cpp:151-176),
-//                         UTable EMA + snapshot (state.cpp:45-71), packed all-gather payload
-//   fc_weights_kernel     PairWeights for the whole batch (engine.cpp:37-75), pass-2 row/col
-//                         parameters, r_i, per-anchor tau-gradient and loss terms
-//   fc_reduce_kernel      fixed-order block reduction of the local terms (G_tau, loss)
-//   fc_finalize_kernel    all-reduced G_tau -> temperature_step (optimizers.cpp:65-83) with the
-//                         TauLrLatch (schedules.hpp:55-58); step scalars
+// These are latency-bound gather/scatter and scalar kernels (no tensor-core shape):
+//   fc_prep_kernel        S_ii = <E1_i, E2_i> and the row-norm bounds for the global batch;
+//                         tau^t snapshot (global tau or IndividualTemp by id, state.cpp:112-122)
+//                         and u^{t-1} gather for the local anchors -> pass-1 row parameters
+//   fc_anchor_kernel      per local anchor: fixed-order reduction of the pass-1 partials -> g
+//                         (engine.cpp:151-176), UTable EMA + snapshot (state.cpp:45-71),
+//                         PairWeights (engine.cpp:37-75), pass-2 parameters, r_i, the local
+//                         tau-gradient / loss terms and the packed payload (+ block partials)
+//   fc_weights_kernel     K > 1, after the payload all-gather: pass-2 parameters of every
+//                         anchor of G and the u replica update for the other ranks' ids
+//   fc_reduce_kernel      fixed-order sum of the (gathered) block partials -> G_tau, loss, and
+//                         temperature_step (optimizers.cpp:65-83) with the TauLrLatch
 //   fc_indiv_update_kernel  v2: IndividualTemp::update for every id of the global batch
 //                         (state.cpp:124-131), replicated identically on every rank
+//   fc_zero_kernel        zeroes dE (the GEMM's reduce-add target)
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
@@ -263,36 +265,17 @@ __global__ void __launch_bounds__(256) fc_zero_kernel(float4* a0, float4* a1, lo
   }
 }
 
-// K > 1, before the payload all-gather: lane group per local anchor -> g, u update, payload.
-__global__ void fc_table_kernel(StepArgs a) {
-  const int r = (blockIdx.x * blockDim.x + threadIdx.x) / kGroup;
-  const int sub = threadIdx.x % kGroup;
-  const bool valid = r < a.Bl;
-  const int rr = valid ? r : 0;
-  const double gamma = a.scal[0];
-  const int id = a.ids[rr];
-  const float kr = a.rowstat_R[rr].x, kc = a.rowstat_C[rr].x;
-  const double uo1 = a.track_u ? a.uold1[rr] : 0.0, uo2 = a.track_u ? a.uold2[rr] : 0.0;
-  const double t1 = a.t_loc1[rr], t2 = a.t_loc2[rr];
-  double s1, x1, s2, x2;
-  reduce_partials(a, rr, valid, sub, s1, x1, s2, x2);
-  if (sub != 0 || !valid) return;
-  const TableVals v = table_math(a, s1, x1, s2, x2, kr, kc, uo1, uo2, gamma);
-  a.sum1[r] = s1; a.dx1[r] = v.dx1; a.sum2[r] = s2; a.dx2[r] = v.dx2;
-  store_payload(a, r, id, v, t1, t2);
-}
-
-// K > 1, after the all-gather: thread per anchor of the global batch.
+// K > 1, after the payload all-gather: thread per anchor of the global batch -> pass-2
+// parameters of every anchor (the local ones were written by fc_anchor_kernel as well) and the
+// u replica update for the other ranks' ids.
 __global__ void fc_weights_kernel(StepArgs a) {
   const double eps = a.scal[1];     // eps_t of this step
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  double ta = 0.0, tb = 0.0, tl = 0.0;
   float kmax = 0.f;
-  // every thread reaches the block reduction from the same place (warp-synchronous shuffles)
   if (i < a.B) {
     const int k = i / a.Bl;
     const int r = i % a.Bl;
-    const double* blk = a.recv + static_cast<size_t>(k) * 5 * a.Bl;
+    const double* blk = a.recv + static_cast<size_t>(k) * a.pstride;
     const double u1 = blk[r], u2 = blk[a.Bl + r];
     const double t1 = blk[2 * a.Bl + r], t2 = blk[3 * a.Bl + r];
     if (a.track_u && k != a.rank) {   // keep this rank's full u replica equal to the shared UTable
@@ -304,14 +287,17 @@ __global__ void fc_weights_kernel(StepArgs a) {
     const AnchorParams p = anchor_params(a, u1, u2, t1, t2, a.tau_state->tau, eps);
     store_params(a, i, p, s_ii);
     kmax = fmaxf(p.k1, p.k2);
-    if (k == a.rank) {
-      const double s1 = a.sum1[r], s2 = a.sum2[r];
-      const float rc = static_cast<float>(p.c1 * s1 + p.c2 * s2);
-      a.rcoef[r] = rc;
-      local_terms(a, r, p, u1, u2, a.g1[r], a.g2[r], a.dx1[r], a.dx2[r], eps, ta, tb, tl);
-    }
   }
-  block_partials(a, ta, tb, tl, kmax);
+  __shared__ float shk[32];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) kmax = fmaxf(kmax, __shfl_xor_sync(0xffffffffu, kmax, o));
+  if ((threadIdx.x & 31) == 0) shk[threadIdx.x >> 5] = kmax;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float km = 0.f;
+    for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) km = fmaxf(km, shk[w]);
+    atomicMax(reinterpret_cast<int*>(a.bounds) + 2, __float_as_int(km));   // max kappa (pass-2 fast path)
+  }
 }
 
 // K = 1: no collective separates the u update from the weights, so a lane group per anchor does
@@ -332,7 +318,7 @@ __global__ void __launch_bounds__(128) fc_anchor_kernel(StepArgs a) {
     const float kr = a.rowstat_R[rr].x, kc = a.rowstat_C[rr].x;
     const double uo1 = a.track_u ? a.uold1[rr] : 0.0, uo2 = a.track_u ? a.uold2[rr] : 0.0;
     const double t1 = a.t_loc1[rr], t2 = a.t_loc2[rr];
-    const float s_ii = a.diag[rr];
+    const float s_ii = a.diag[a.row0 + rr];
     double s1, x1, s2, x2;
     reduce_partials(a, rr, valid, sub, s1, x1, s2, x2);
     if (sub == 0 && valid) {
@@ -341,7 +327,7 @@ __global__ void __launch_bounds__(128) fc_anchor_kernel(StepArgs a) {
       kmax = fmaxf(p.k1, p.k2);
       local_terms(a, r, p, v.u1, v.u2, v.g1, v.g2, v.dx1, v.dx2, eps, ta, tb, tl);
       a.rcoef[r] = static_cast<float>(p.c1 * s1 + p.c2 * s2);
-      store_params(a, r, p, s_ii);
+      store_params(a, a.row0 + r, p, s_ii);
       a.sum1[r] = s1; a.dx1[r] = v.dx1; a.sum2[r] = s2; a.dx2[r] = v.dx2;
       store_payload(a, r, id, v, t1, t2);
     }
@@ -422,29 +408,34 @@ __device__ void block_partials(const StepArgs& a, double ta, double tb, double t
 // step. Nothing on the gradient path waits for it; a single warp without shared memory fits
 // beside a persistent similarity CTA, so it never delays the pass-2 launch.
 __global__ void __launch_bounds__(32) fc_reduce_kernel(StepArgs a) {
-  double s0 = 0.0, s1 = 0.0, s2 = 0.0;
-  for (int b = threadIdx.x; b < a.n_blockpart; b += 32) {
-    const double* bp = a.blockpart + 3 * b;
-    s0 += bp[0]; s1 += bp[1]; s2 += bp[2];
-  }
+  // rank by rank in rank order (identical arithmetic on every rank, so the replicated tau
+  // stays bit-identical): G_tau,k from rank k's block partials (engine.cpp:208-238), summed
+  // over k -- the all_reduce_mean_scalar of trainer.cpp:572 without a collective
+  double gsum = 0.0, lsum = 0.0;
+  for (int k = 0; k < a.world; ++k) {
+    const double* bp0 = a.recv + static_cast<size_t>(k) * a.pstride + 7 * static_cast<size_t>(a.Bl);
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0;
+    for (int b = threadIdx.x; b < a.nblk; b += 32) {
+      const double* bp = bp0 + 3 * b;
+      s0 += bp[0]; s1 += bp[1]; s2 += bp[2];
+    }
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    s0 += __shfl_xor_sync(0xffffffffu, s0, o);
-    s1 += __shfl_xor_sync(0xffffffffu, s1, o);
-    s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+    for (int o = 16; o > 0; o >>= 1) {
+      s0 += __shfl_xor_sync(0xffffffffu, s0, o);
+      s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+      s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+    }
+    const double bl = static_cast<double>(a.Bl);
+    const double unscaled = s0 / bl;
+    double gtl = unscaled;                                                   // v0 / MBCL
+    if (a.variant == 6) gtl = s1 / bl + 2.0 * a.rho + a.tau_state->tau * unscaled;  // v3
+    gsum += gtl;
+    lsum += s2;
   }
   if (threadIdx.x != 0) return;
-  const double bl = static_cast<double>(a.Bl);
-  const double unscaled = s0 / bl;
-  double gtl = unscaled;                                                   // v0 / MBCL
-  if (a.variant == 6) gtl = s1 / bl + 2.0 * a.rho + a.tau_state->tau * unscaled;  // v3
-  a.red[0] = gtl;   // all-reduced (sum) across ranks, then * 1/K (fabric.cpp:73-83)
-  a.red[1] = s2;    // loss numerator, summed across ranks
-  if (a.fuse_finalize) finalize_step(a);
-}
-
-__global__ void fc_finalize_kernel(StepArgs a) {
-  if (threadIdx.x == 0 && blockIdx.x == 0) finalize_step(a);
+  a.red[0] = gsum;   // sum over ranks; finalize_step applies the 1/K of the mean (fabric.cpp:73-83)
+  a.red[1] = lsum;   // loss numerator over the global batch
+  finalize_step(a);
 }
 
 // v2 / iSogCLR: IndividualTemp::update for every id of the global batch (state.cpp:124-131);
@@ -454,9 +445,9 @@ __global__ void fc_indiv_update_kernel(StepArgs a) {
   if (i >= a.B) return;
   const int k = i / a.Bl;
   const int r = i % a.Bl;
-  const int id = static_cast<int>(a.recv[static_cast<size_t>(k) * 5 * a.Bl + 4 * a.Bl + r]);
-  const double gts[2] = {a.gt_recv[static_cast<size_t>(k) * 2 * a.Bl + r],
-                         a.gt_recv[static_cast<size_t>(k) * 2 * a.Bl + a.Bl + r]};
+  const double* blk = a.recv + static_cast<size_t>(k) * a.pstride;
+  const int id = static_cast<int>(blk[4 * a.Bl + r]);
+  const double gts[2] = {blk[5 * a.Bl + r], blk[6 * a.Bl + r]};
   double* taus[2] = {a.tau1_tab, a.tau2_tab};
   double* ms[2] = {a.m1_tab, a.m2_tab};
   double* vs[2] = {a.v1_tab, a.v2_tab};

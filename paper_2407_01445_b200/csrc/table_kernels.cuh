@@ -56,9 +56,13 @@ struct StepArgs {
   double* term_a; double* term_b; double* term_loss;
   double* gt1; double* gt2;              // v2 tau gradients, contiguous [gt1 | gt2] (send)
   double* uold1; double* uold2;          // u^{t-1} of the local ids, gathered by the prep kernel
-  double* send;                          // [5][Bl] packed payload
-  const double* recv;                    // [K][5][Bl] (== send when K == 1)
-  const double* gt_recv;                 // [K][2][Bl] (== gt1 when K == 1)
+  // packed per-rank payload (all-gathered at K > 1; recv == send at K == 1):
+  //   [u1 | u2 | t1 | t2 | id | gt1 | gt2] x Bl, then nblk x {G_tau term a, term b, loss}
+  // so one all-gather carries the per-sample scalars, the v2 per-index tau gradients and the
+  // per-block partial sums of G_tau and the loss (no separate all-reduce / gather)
+  double* send;                          // [pstride]
+  const double* recv;                    // [K][pstride]
+  int pstride, nblk;
   // pass-2 parameters
   // per-anchor exponent parameters y = s*kappa + beta and weights coef (SoA, [n_jt*256])
   float* kap1; float* bet1; float* coef1;   // track 1: kappa = log2e/t1, coef = w1/t1
@@ -66,9 +70,8 @@ struct StepArgs {
   float* fac1; float* fac2;                 // coef * 2^beta (factorized pass 2, one shared temperature)
   float* rcoef;                          // [Bl]
   double* red;                           // [2] local G_tau, loss numerator (all-reduced)
-  double* blockpart;                     // [grid][3] per-block partial sums (weights kernel)
+  double* blockpart;                     // [nblk][3] per-block partial sums (send + 7 Bl)
   int n_blockpart;                       // blocks of the kernel that wrote blockpart
-  int fuse_finalize;                     // K == 1: temperature step in the reduce kernel
   int* err;
   StepResult* result;
   float gscale;                          // c = 1 / (Bl (B-1)), engine.cpp:84-85
@@ -76,12 +79,10 @@ struct StepArgs {
 
 __global__ void fc_prep_kernel(const __nv_bfloat16* __restrict__ e1, const __nv_bfloat16* __restrict__ e2,
                                StepArgs a);
-__global__ void fc_table_kernel(StepArgs a);
 __global__ void fc_weights_kernel(StepArgs a);
 __global__ void fc_anchor_kernel(StepArgs a);
 __global__ void fc_zero_kernel(float4* a0, float4* a1, long long n4);
 __global__ void fc_reduce_kernel(StepArgs a);
-__global__ void fc_finalize_kernel(StepArgs a);
 __global__ void fc_indiv_update_kernel(StepArgs a);
 
 }  // namespace fc
