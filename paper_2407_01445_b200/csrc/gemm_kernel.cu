@@ -66,9 +66,8 @@ struct UnitIter {
   long long u, u1;
   __device__ UnitIter(const GemmParams& p, int cluster, int n_clusters) {
     KB = p.kb_total;
-    const long long U = static_cast<long long>(p.n_tiles) * KB;
-    u = U * cluster / n_clusters;
-    u1 = U * (cluster + 1) / n_clusters;
+    u = p.unit_lo[cluster];
+    u1 = p.unit_lo[cluster + 1];
   }
   __device__ bool next(int& tile, int& kb0, int& kb1) {
     if (u >= u1) return false;
@@ -92,6 +91,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   long long g_entry = 0;
   if (p.debug >= 9) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_entry));
   const GSmem L = gcarve(smem_raw);
+  griddep_launch_dependents();
   const uint32_t warp = threadIdx.x / 32;
   const uint32_t lane = lane_id();
   const uint32_t crank = cluster_ctarank();          // 0 .. 2*kPairs-1
@@ -130,6 +130,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     // ===================== TMA producer (whole warp walks, lane 0 issues) =====================
     const bool issuer = lane == 0;
     uint32_t stage = 0, phase = 0;
+    griddep_wait();   // Q' comes from the pass-2 kernel (barrier init / TMEM alloc overlapped it)
     UnitIter iter(p, cluster, n_clusters);
     int tile, kb0, kb1;
     while (iter.next(tile, kb0, kb1)) {
@@ -356,23 +357,25 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 
 namespace {
 template <int kPairs>
-cudaError_t launch_gemm_t(const GemmParams& p, const CUtensorMap* mapQ, const CUtensorMap* mapX,
+cudaError_t launch_gemm_t(bool pdl, const GemmParams& p, const CUtensorMap* mapQ, const CUtensorMap* mapX,
                           const CUtensorMap* mapOut, int grid, cudaStream_t s) {
   const CUtensorMap& q1 = p.nseg > 1 ? mapQ[1] : mapQ[0];
   const CUtensorMap& x1 = p.nseg > 1 ? mapX[1] : mapX[0];
   const CUtensorMap& o1 = p.nseg > 1 ? mapOut[1] : mapOut[0];
   cudaLaunchConfig_t cfg{};
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = 2 * kPairs;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
   cfg.gridDim = dim3(grid, 1, 1);
   cfg.blockDim = dim3(kGemmThreads, 1, 1);
   cfg.dynamicSmemBytes = kGemmSmemBytes;
   cfg.stream = s;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = 2;
   return cudaLaunchKernelEx(&cfg, grad_gemm_kernel<kPairs>, p, mapQ[0], mapX[0], q1, x1, mapOut[0], o1);
 }
 }  // namespace
@@ -400,10 +403,10 @@ cudaError_t gemm_set_smem() {
   return e;
 }
 
-cudaError_t launch_gemm(const GemmParams& p, const CUtensorMap* mapQ, const CUtensorMap* mapX,
+cudaError_t launch_gemm(bool pdl, const GemmParams& p, const CUtensorMap* mapQ, const CUtensorMap* mapX,
                         const CUtensorMap* mapOut, int grid, cudaStream_t s) {
-  if (p.pairs_per_cluster == 2) return launch_gemm_t<2>(p, mapQ, mapX, mapOut, grid, s);
-  return launch_gemm_t<1>(p, mapQ, mapX, mapOut, grid, s);
+  if (p.pairs_per_cluster == 2) return launch_gemm_t<2>(pdl, p, mapQ, mapX, mapOut, grid, s);
+  return launch_gemm_t<1>(pdl, p, mapQ, mapX, mapOut, grid, s);
 }
 
 }  // namespace fc

@@ -30,6 +30,7 @@ constexpr int kSimSmemQ = kSimASlots * kStageBytesA + kSimStagesQ * kStageBytesB
                           kSimEpiWarps * kSimStageOutQ;
 constexpr int kSimSmemBytes = (kSimSmemStats > kSimSmemQ ? kSimSmemStats : kSimSmemQ) + 1024 + 512;
 // gradient GEMM: A (Q') and B (E) both stream; pair tile 256 x 512 (two N = 256 accumulators).
+constexpr int kMaxGemmClusters = 160;
 constexpr int kGemmN = 2 * kPairN;
 constexpr int kGemmStages = 4;
 constexpr int kGemmStageBytesB = 2 * kStageBytesB;   // own 128 columns of both N halves
@@ -73,7 +74,7 @@ struct SimParams {
   float4* zero_a; float4* zero_b;          // nullptr: nothing to zero
   long long zero_n4;                       // float4 count of each
   // FUSED: column statistics {sum e, sum y e} per (row slot = 32-row quarter of a pair tile,
-  // column): [n_slots][cols]; fuse_fast enables the one-exponential path (one temperature)
+  // column), laid out [cols / 32][n_slots][32]; fuse_fast enables the one-exponential path
   float2* col_partial;
   int n_slots;
   int fuse_fast;
@@ -98,6 +99,10 @@ struct GemmParams {
   int n_nb;
   int n_tiles;       // sum over segments of n_mb * n_nb (cluster tiles: 256*pairs_per_cluster x 512)
   int pairs_per_cluster;   // 1, or 2: two pairs share (multicast) the B operand
+  // stream-K partition: cluster c runs units [unit_lo[c], unit_lo[c+1]) of the (tile, k-block)
+  // sequence; the host balances k-blocks + per-unit epilogue cost (a unit boundary costs one
+  // accumulator drain), so clusters with two units get fewer k-blocks
+  int unit_lo[kMaxGemmClusters + 1];
   int kb_total;      // K blocks of 64 over ldq
   float scale;       // 1 / (Bl (B-1)), engine.cpp:84-85
   int debug;         // perf experiments: 1 = skip epilogue stores; 9 = counters / timelines into dbg_out
@@ -109,13 +114,13 @@ struct GemmParams {
 enum SimMode { kSimStats = 0, kSimQ = 1, kSimRaw = 2, kSimFused = 3 };
 
 cudaError_t launch_sim(int mode, const SimParams& p, const CUtensorMap* mapA, const CUtensorMap* mapB,
-                       const CUtensorMap* mapQout, int grid, cudaStream_t s, float* raw_out);
+                       const CUtensorMap* mapQout, int grid, cudaStream_t s, float* raw_out, bool pdl = false);
 cudaError_t sim_set_smem();
 cudaError_t launch_ring_probe(int n_pairs, int n_kb, int tile_kb, int epi, long long* cycles, cudaStream_t s);
 cudaError_t launch_mma_probe(int n_pairs, int n_mma, int commit_every, long long* cycles, cudaStream_t s);
 cudaError_t gemm_set_smem();
 cudaError_t gemm_max_active_clusters(int pairs_per_cluster, int* n);
-cudaError_t launch_gemm(const GemmParams& p, const CUtensorMap* mapQ, const CUtensorMap* mapX,
+cudaError_t launch_gemm(bool pdl, const GemmParams& p, const CUtensorMap* mapQ, const CUtensorMap* mapX,
                         const CUtensorMap* mapOut, int grid, cudaStream_t s);
 
 }  // namespace fc

@@ -130,6 +130,8 @@ struct LossStep {
   bool q_factor = true;          // FC_Q_FACTOR=0 forces the two-exponential Q path (A/B checks)
   bool gemm_mc = false;          // FC_GEMM_MC=1: clusters of two pairs multicast the GEMM B operand
   bool fused_p1 = false;         // K == 1: row + column statistics from one S pass (FC_FUSED_P1=0: two passes)
+  bool pdl = true;               // programmatic dependent launch between the step's kernels (FC_PDL=0: off)
+  int gemm_drain = 0;            // FC_GEMM_DRAIN: stream-K unit-boundary cost in k-blocks (0: KB / 10)
   long long* dbg_buf = nullptr;   // FC_SIM_DEBUG=9 MMA-warp counters: [launch 0: pass 1, 1: pass 2][pair][8]             // FC_SIM_DEBUG perf experiments (results invalid when set)
   struct GraphEntry {
     const void* key[5];
@@ -214,7 +216,8 @@ struct LossStep {
     diag = dalloc<float>(B);
     rowstat = dalloc<float2>(2 * static_cast<size_t>(Bl));
     partial = dalloc<float2>(2 * static_cast<size_t>(Bl) * n_jt * 4);
-    if (K == 1) col_partial = dalloc<float2>(static_cast<size_t>((Bl + fc::kPairM - 1) / fc::kPairM) * 8 * B);
+    if (K == 1)   // [ceil(B/32)][n_slots][32]: 256-byte warp stores, 32-byte reads per 4 anchors
+      col_partial = dalloc<float2>(static_cast<size_t>((Bl + fc::kPairM - 1) / fc::kPairM) * 8 * ((B + 31) / 32 * 32));
     clamps = dalloc<unsigned long long>(1);
     bounds = dalloc<float>(4);
     f64 = dalloc<double>(static_cast<size_t>(Bl) * 18);
@@ -248,6 +251,8 @@ struct LossStep {
     if (const char* e = std::getenv("FC_Q_FACTOR")) q_factor = atoi(e) != 0;
     if (const char* e = std::getenv("FC_GEMM_MC")) gemm_mc = atoi(e) != 0;
     fused_p1 = K == 1;
+    if (const char* e = std::getenv("FC_PDL")) pdl = atoi(e) != 0;
+    if (const char* e = std::getenv("FC_GEMM_DRAIN")) gemm_drain = atoi(e);
     if (const char* e = std::getenv("FC_FUSED_P1")) fused_p1 = fused_p1 && atoi(e) != 0;
     if (const char* e = std::getenv("FC_GEMM_DEBUG")) gemm_debug = atoi(e);
     if (sim_debug == 9 || gemm_debug >= 9) dbg_buf = dalloc<long long>(2 * 2688 + 160 * 16);
@@ -314,6 +319,40 @@ struct LossStep {
     mE2n = make_map(e2, d, B, rb, 64, 64);
     map_e1 = e1;
     map_e2 = e2;
+  }
+
+  // Contiguous stream-K ranges over the (tile, k-block) sequence with equal estimated cost
+  // per cluster: k-blocks + kDrain per unit (each unit ends in a full-tile epilogue that the
+  // single TMEM accumulator cannot overlap). Greedy fill against a binary-searched budget.
+  void balance_units(fc::GemmParams& gp, int n_clusters) const {
+    const long long KB = gp.kb_total, U = static_cast<long long>(gp.n_tiles) * KB;
+    // cost of one unit boundary in k-blocks (measured best ~8 at K = 5120; FC_GEMM_DRAIN overrides)
+    const long long kDrain = gemm_drain > 0 ? gemm_drain : std::max<long long>(1, KB / 10);
+    auto fill = [&](long long budget, bool write) {
+      long long u = 0;
+      int c = 0;
+      for (; c < n_clusters && u < U; ++c) {
+        if (write) gp.unit_lo[c] = static_cast<int>(u);
+        long long left = budget;
+        while (u < U) {
+          const long long in_tile = KB - u % KB;
+          if (left <= kDrain) break;
+          const long long take = std::min(in_tile, left - kDrain);
+          u += take;
+          left -= take + kDrain;
+          if (take < in_tile) break;
+        }
+      }
+      if (write) for (int k = c; k <= n_clusters; ++k) gp.unit_lo[k] = static_cast<int>(U);
+      return u >= U;
+    };
+    long long lo = 1, hi = U + kDrain * (gp.n_tiles + 1);
+    while (lo < hi) {   // smallest budget that covers every unit with n_clusters clusters
+      const long long mid = (lo + hi) / 2;
+      if (fill(mid, false)) hi = mid; else lo = mid + 1;
+    }
+    fill(lo, true);
+    gp.unit_lo[n_clusters] = static_cast<int>(U);
   }
 
   int pair_grid(long items) const {
@@ -434,17 +473,28 @@ struct LossStep {
       sp.fuse_fast = indiv ? 0 : 1;
       a.col_partial = col_partial;
       a.col_slots = sp.n_slots;
-      FC_CUDA(fc::launch_sim(fc::kSimFused, sp, mA, mB, nullptr, pair_grid(sp.n_items), st, nullptr));
+      FC_CUDA(fc::launch_sim(fc::kSimFused, sp, mA, mB, nullptr, pair_grid(sp.n_items), st, nullptr, pdl && !timing));
     } else {
       a.col_slots = 0;
-      FC_CUDA(fc::launch_sim(fc::kSimStats, sp, mA, mB, nullptr, pair_grid(sp.n_items), st, nullptr));
+      FC_CUDA(fc::launch_sim(fc::kSimStats, sp, mA, mB, nullptr, pair_grid(sp.n_items), st, nullptr, pdl && !timing));
     }
 
     // ---- u table, payload, (all-gather), weights, reductions, tau update ----
     mark(3, st);
     // table update + weights + local G_tau / loss terms + payload, one lane group per anchor
     a.n_blockpart = nblk;
-    fc::fc_anchor_kernel<<<nblk, kAnchorBlock, 0, st>>>(a);
+    {
+      cudaLaunchConfig_t cfg{};
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      attr[0].val.programmaticStreamSerializationAllowed = (pdl && !timing) ? 1 : 0;
+      cfg.gridDim = dim3(nblk, 1, 1);
+      cfg.blockDim = dim3(kAnchorBlock, 1, 1);
+      cfg.stream = st;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+      FC_CUDA(cudaLaunchKernelEx(&cfg, fc::fc_anchor_kernel, a));
+    }
     FC_CUDA(cudaGetLastError());
     if (K > 1) {
       // ONE all-gather carries u/tau/id, the v2 per-index tau gradients and the G_tau / loss
@@ -487,7 +537,7 @@ struct LossStep {
     if (sim_debug == 9) sp.dbg_out = dbg_buf + 2688;
     sp.q_factor = (!indiv && q_factor) ? 1 : 0;   // one shared temperature: single-exponential Q
     sp.zero_a = sp.zero_b = nullptr;
-    FC_CUDA(fc::launch_sim(fc::kSimQ, sp, mA, mB, mQo, pair_grid(sp.n_items), st, nullptr));
+    FC_CUDA(fc::launch_sim(fc::kSimQ, sp, mA, mB, mQo, pair_grid(sp.n_items), st, nullptr, pdl && !timing));
 
     // ---- pass 2b: dE = c (Q' E - r o E_local) ----
     mark(5, st);
@@ -512,8 +562,9 @@ struct LossStep {
       gp.n_mb[s] = (Bl + rows_per_tile - 1) / rows_per_tile;
     }
     gp.n_tiles = (gp.n_mb[0] + gp.n_mb[1]) * gp.n_nb;
-    // every unit reduce-adds into dE (zeroed by the per-anchor kernel of this step)
+    // every unit reduce-adds into dE (zeroed on the side branch of this step)
     const int gemm_ctas = (n_sm / (2 * gp.pairs_per_cluster)) * 2 * gp.pairs_per_cluster;
+    balance_units(gp, gemm_ctas / (2 * gp.pairs_per_cluster));
     CUtensorMap mX[2] = {mE2n, mE1n};
     CUtensorMap mQs[2] = {mQ[0], shared_q ? mQt : mQ[1]};
     if (out->de1 != map_o1 || out->de2 != map_o2) {
@@ -524,7 +575,7 @@ struct LossStep {
       map_o2 = out->de2;
     }
     FC_CUDA(cudaStreamWaitEvent(st, zero_join, 0));
-    FC_CUDA(fc::launch_gemm(gp, mQs, mX, mO, gemm_ctas, st));
+    FC_CUDA(fc::launch_gemm(pdl && !timing, gp, mQs, mX, mO, gemm_ctas, st));
     mark(6, st);
 
     FC_CUDA(cudaStreamWaitEvent(st, side_join, 0));

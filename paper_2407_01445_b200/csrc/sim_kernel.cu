@@ -343,6 +343,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(SimCfg<kMode>::kThre
   cluster_sync();
   tc_fence_after();
   const uint32_t tmem_base = *L.tmem_ptr;
+  griddep_launch_dependents();   // the next kernel may take SMs as this grid's CTAs retire
 
   const int n_chunks = (nkb + kSimASlots - 1) / kSimASlots;
   int it_lo, it_hi;
@@ -369,7 +370,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(SimCfg<kMode>::kThre
         const int a_row = p.seg[s].a_row0 + rb * kPairM + static_cast<int>(rank) * kCtaM;
         const int b_row = jt * kPairN + static_cast<int>(rank) * (kPairN / 2);
         if constexpr (kMode == kSimQ) {
-          // this tile's column parameters (each CTA keeps its own copy)
+          // this tile's column parameters (each CTA keeps its own copy), written by the
+          // preceding per-anchor kernel: wait for it before the first parameter load (the A / B
+          // operand loads above do not depend on it)
+          if (it == 0) griddep_wait();
           const int ps = it % kSimPSlots;
           mbar_wait(&L.pempty[ps], ((it / kSimPSlots) & 1) ^ 1);
           if (issuer) {
@@ -499,6 +503,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(SimCfg<kMode>::kThre
     }
   } else {
     // ===================== epilogue (both CTAs) =====================
+    griddep_wait();   // row / column parameters and bounds come from the preceding kernel
     if constexpr (kStatsLike) {
       // While the first tiles load and multiply (two TMEM buffers of slack), the epilogue
       // warps zero this CTA's slice of the gradient outputs for the GEMM of this step.
@@ -647,7 +652,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(SimCfg<kMode>::kThre
             ce = sc * ce;
           }
           if (jc < sg.cols)
-            p.col_partial[static_cast<size_t>(rb * 8 + rank * 4 + q4) * sg.cols + jc] = f2(ce, cye);
+            p.col_partial[(static_cast<size_t>(col0 >> 5) * p.n_slots + (rb * 8 + rank * 4 + q4)) * 32 + lane] = f2(ce, cye);
           if (h & 1) {   // 64 columns done: one row partial per (row, column quarter)
             // fast-path row raw sums {sum x, sum z x} -> e = 2^beta_i x, y e = (z + beta_i) e
             const float sc = ex2_approx(rstat.y);
@@ -742,28 +747,36 @@ cudaError_t sim_set_smem() {
 }
 
 cudaError_t launch_sim(int mode, const SimParams& p, const CUtensorMap* mapA, const CUtensorMap* mapB,
-                       const CUtensorMap* mapQout, int grid, cudaStream_t s, float* raw_out) {
+                       const CUtensorMap* mapQout, int grid, cudaStream_t s, float* raw_out, bool pdl) {
   const CUtensorMap& a1 = p.nseg > 1 ? mapA[1] : mapA[0];
   const CUtensorMap& b1 = p.nseg > 1 ? mapB[1] : mapB[0];
   const CUtensorMap& q0 = mapQout ? mapQout[0] : mapA[0];
   const CUtensorMap& q1 = mapQout ? (p.nseg > 1 ? mapQout[1] : mapQout[0]) : mapA[0];
   if (grid < 2) grid = 2;
   grid &= ~1;
+  cudaLaunchConfig_t cfg{};
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
+  cfg.gridDim = dim3(grid, 1, 1);
+  cfg.dynamicSmemBytes = kSimSmemBytes;
+  cfg.stream = s;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
   switch (mode) {
     case kSimStats:
-      sim_tile_kernel<kSimStats><<<grid, SimCfg<kSimStats>::kThreads, kSimSmemBytes, s>>>(p, mapA[0], mapB[0], a1, b1, q0, q1, raw_out);
-      break;
+      cfg.blockDim = dim3(SimCfg<kSimStats>::kThreads, 1, 1);
+      return cudaLaunchKernelEx(&cfg, sim_tile_kernel<kSimStats>, p, mapA[0], mapB[0], a1, b1, q0, q1, raw_out);
     case kSimFused:
-      sim_tile_kernel<kSimFused><<<grid, SimCfg<kSimFused>::kThreads, kSimSmemBytes, s>>>(p, mapA[0], mapB[0], a1, b1, q0, q1, raw_out);
-      break;
+      cfg.blockDim = dim3(SimCfg<kSimFused>::kThreads, 1, 1);
+      return cudaLaunchKernelEx(&cfg, sim_tile_kernel<kSimFused>, p, mapA[0], mapB[0], a1, b1, q0, q1, raw_out);
     case kSimQ:
-      sim_tile_kernel<kSimQ><<<grid, SimCfg<kSimQ>::kThreads, kSimSmemBytes, s>>>(p, mapA[0], mapB[0], a1, b1, q0, q1, raw_out);
-      break;
+      cfg.blockDim = dim3(SimCfg<kSimQ>::kThreads, 1, 1);
+      return cudaLaunchKernelEx(&cfg, sim_tile_kernel<kSimQ>, p, mapA[0], mapB[0], a1, b1, q0, q1, raw_out);
     default:
-      sim_tile_kernel<kSimRaw><<<grid, SimCfg<kSimRaw>::kThreads, kSimSmemBytes, s>>>(p, mapA[0], mapB[0], a1, b1, q0, q1, raw_out);
-      break;
+      cfg.blockDim = dim3(SimCfg<kSimRaw>::kThreads, 1, 1);
+      return cudaLaunchKernelEx(&cfg, sim_tile_kernel<kSimRaw>, p, mapA[0], mapB[0], a1, b1, q0, q1, raw_out);
   }
-  return cudaGetLastError();
 }
 
 }  // namespace fc

@@ -116,26 +116,36 @@ constexpr int kGroup = 8;
 
 // Fixed-order (group-lane-strided + xor tree) reduction of one anchor's pass-1 partials; every
 // lane of the warp must call it (valid = false contributes nothing).
+// Sum of n strided float2 partials, lane `sub` of the group taking q = sub, sub + kGroup, ...
+// in ascending order; loads are issued eight at a time so their latencies overlap.
+__device__ __forceinline__ void sum_partials(const float2* __restrict__ base, size_t stride, int n, int sub,
+                                             double& s, double& x) {
+  for (int q0 = sub; q0 < n; q0 += 8 * kGroup) {
+    float2 v[8];
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+      const int q = q0 + t * kGroup;
+      v[t] = q < n ? __ldg(base + q * stride) : make_float2(0.f, 0.f);
+    }
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+      s += v[t].x;
+      x += v[t].y;
+    }
+  }
+}
+
 __device__ __forceinline__ void reduce_partials(const StepArgs& a, int r, bool valid, int sub, double& s1,
                                                 double& x1, double& s2, double& x2) {
   const int nparts = a.n_jt * 4;
-  const float2* pr = a.partial_R + static_cast<size_t>(r) * nparts;
-  const float2* pc = a.partial_C + static_cast<size_t>(r) * nparts;
   s1 = 0.0; x1 = 0.0; s2 = 0.0; x2 = 0.0;
-  for (int q = sub; valid && q < nparts; q += kGroup) {
-    const float2 u = __ldg(pr + q);
-    s1 += u.x; x1 += u.y;
-  }
-  if (a.col_slots > 0) {   // fused pass 1: column statistics of S, slot-major
-    const float2* cp = a.col_partial + (a.row0 + r);
-    for (int q = sub; valid && q < a.col_slots; q += kGroup) {
-      const float2 v = __ldg(cp + static_cast<size_t>(q) * a.B);
-      s2 += v.x; x2 += v.y;
-    }
-  } else {
-    for (int q = sub; valid && q < nparts; q += kGroup) {
-      const float2 v = __ldg(pc + q);
-      s2 += v.x; x2 += v.y;
+  if (valid) {
+    sum_partials(a.partial_R + static_cast<size_t>(r) * nparts, 1, nparts, sub, s1, x1);
+    if (a.col_slots > 0) {   // fused pass 1: column statistics of S, [B/32][slots][32]
+      const int j = a.row0 + r;
+      sum_partials(a.col_partial + static_cast<size_t>(j >> 5) * a.col_slots * 32 + (j & 31), 32, a.col_slots, sub, s2, x2);
+    } else {
+      sum_partials(a.partial_C + static_cast<size_t>(r) * nparts, 1, nparts, sub, s2, x2);
     }
   }
 #pragma unroll
@@ -304,6 +314,8 @@ __global__ void fc_weights_kernel(StepArgs a) {
 // the partial reduction, and its leader the table update, weights and local terms from
 // registers; then the per-block partial sums (reduced off the critical path by fc_reduce_kernel).
 __global__ void __launch_bounds__(128) fc_anchor_kernel(StepArgs a) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");   // pass-1 partials (programmatic launch)
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const int r = (blockIdx.x * blockDim.x + threadIdx.x) / kGroup;
   const int sub = threadIdx.x % kGroup;
   const bool valid = r < a.Bl;

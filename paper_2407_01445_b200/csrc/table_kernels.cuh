@@ -45,7 +45,7 @@ struct StepArgs {
   // pass-1 products
   float2* rowstat_R; float2* rowstat_C;   // [Bl]
   float2* partial_R; float2* partial_C;   // [Bl][n_jt*4]
-  const float2* col_partial;             // fused pass 1 (K = 1): segment-C stats [col_slots][B]
+  const float2* col_partial;             // fused pass 1 (K = 1): segment-C stats [B/32][col_slots][32]
   int col_slots;                         // 0: segment-C stats are row partials in partial_C
   unsigned long long* clamps;
   float* bounds;                         // {max |E1|^2, max |E2|^2, max kappa} (atomicMax on float bits)

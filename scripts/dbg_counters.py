@@ -45,3 +45,19 @@ for pp in (1, 2):
     n = C.c_int(0)
     P.lib().fc_debug_gemm_clusters(pp, C.byref(n))
     print(f'GEMM pairs/cluster {pp}: max active clusters {n.value}')
+# absolute step timeline from the per-CTA globaltimer stamps (ns): one graph replay
+for _ in range(2): st.step(e1, e2, ids, 0.6, 1e-14)
+st.disable_phase_timing()
+for _ in range(3): st.step(e1, e2, ids, 0.6, 1e-14)
+torch.cuda.synchronize()
+out[:] = 0
+P.lib().fc_debug_counters(st._h, out.ctypes.data_as(C.POINTER(C.c_longlong)))
+tls = [out[k * R + 2048:k * R + 2048 + 148 * 4].reshape(148, 4) for k in range(2)]
+g = out[2 * R:2 * R + 160 * 16].reshape(160, 16)[:148]
+t0 = tls[0][:, 0].min()
+f = lambda x: round((x - t0) / 1e3, 2)
+print('graph-step timeline (us from pass-1 first CTA entry):')
+print('  pass1: first entry', f(tls[0][:, 0].min()), 'last entry', f(tls[0][:, 0].max()), 'first exit', f(tls[0][:, 2].min()), 'last exit', f(tls[0][:, 2].max()))
+print('  pass2: first entry', f(tls[1][:, 0].min()), 'last entry', f(tls[1][:, 0].max()), 'first exit', f(tls[1][:, 2].min()), 'last exit', f(tls[1][:, 2].max()))
+if os.environ.get('FC_GEMM_DEBUG') in ('9', '10'):
+    print('  gemm : first entry', f(g[:, 11].min()), 'last entry', f(g[:, 11].max()), 'epi end min', f(g[:, 10].min()), 'epi end max', f(g[:, 10].max()))
