@@ -221,7 +221,7 @@ struct LossStep {
     clamps = dalloc<unsigned long long>(1);
     bounds = dalloc<float>(4);
     f64 = dalloc<double>(static_cast<size_t>(Bl) * 18);
-    nblk = (Bl * 8 + kAnchorBlock - 1) / kAnchorBlock;
+    nblk = (Bl * fc::kAnchorLanes + kAnchorBlock - 1) / kAnchorBlock;
     pstride = 7 * Bl + 3 * nblk;
     send = dalloc<double>(static_cast<size_t>(pstride));
     recv = K > 1 ? dalloc<double>(static_cast<size_t>(K) * pstride) : send;
@@ -255,7 +255,7 @@ struct LossStep {
     if (const char* e = std::getenv("FC_GEMM_DRAIN")) gemm_drain = atoi(e);
     if (const char* e = std::getenv("FC_FUSED_P1")) fused_p1 = fused_p1 && atoi(e) != 0;
     if (const char* e = std::getenv("FC_GEMM_DEBUG")) gemm_debug = atoi(e);
-    if (sim_debug == 9 || gemm_debug >= 9) dbg_buf = dalloc<long long>(2 * 2688 + 160 * 16);
+    if (sim_debug == 9 || gemm_debug >= 9) dbg_buf = dalloc<long long>(2 * 2688 + 160 * 16 + 8192);
     if (debug_sync) use_graph = false;
     if (const char* e = std::getenv("FC_SHARED_Q")) shared_q = shared_q && atoi(e) != 0;
     FC_CUDA(fc::sim_set_smem());
@@ -483,6 +483,7 @@ struct LossStep {
     mark(3, st);
     // table update + weights + local G_tau / loss terms + payload, one lane group per anchor
     a.n_blockpart = nblk;
+    if (sim_debug == 9) a.dbg = dbg_buf + 2 * 2688 + 160 * 16;
     {
       cudaLaunchConfig_t cfg{};
       cudaLaunchAttribute attr[1];
@@ -857,7 +858,7 @@ int fc_debug_counters(void* ctx, long long* out /* host [2*128*8] */) {
   auto* s = static_cast<LossStep*>(ctx);
   return guarded([&] {
     FC_CUDA(cudaDeviceSynchronize());
-    if (s->dbg_buf) FC_CUDA(cudaMemcpy(out, s->dbg_buf, (2 * 2688 + 160 * 16) * 8, cudaMemcpyDeviceToHost));
+    if (s->dbg_buf) FC_CUDA(cudaMemcpy(out, s->dbg_buf, (2 * 2688 + 160 * 16 + 8192) * 8, cudaMemcpyDeviceToHost));
   });
 }
 

@@ -112,7 +112,7 @@ __global__ void fc_prep_kernel(const __nv_bfloat16* __restrict__ e1, const __nv_
 
 // Anchors per warp of the per-anchor kernels: kGroup lanes reduce one anchor's partials, and
 // the scalar fp64 chain then runs on the group leaders, four anchors per warp instruction.
-constexpr int kGroup = 8;
+constexpr int kGroup = kAnchorLanes;
 
 // Fixed-order (group-lane-strided + xor tree) reduction of one anchor's pass-1 partials; every
 // lane of the warp must call it (valid = false contributes nothing).
@@ -313,9 +313,17 @@ __global__ void fc_weights_kernel(StepArgs a) {
 // K = 1: no collective separates the u update from the weights, so a lane group per anchor does
 // the partial reduction, and its leader the table update, weights and local terms from
 // registers; then the per-block partial sums (reduced off the critical path by fc_reduce_kernel).
+__device__ __forceinline__ long long gtime() {
+  long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
 __global__ void __launch_bounds__(128) fc_anchor_kernel(StepArgs a) {
+  long long t_entry = a.dbg ? gtime() : 0;
   asm volatile("griddepcontrol.wait;" ::: "memory");   // pass-1 partials (programmatic launch)
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  long long t_wait = a.dbg ? gtime() : 0;
   const int r = (blockIdx.x * blockDim.x + threadIdx.x) / kGroup;
   const int sub = threadIdx.x % kGroup;
   const bool valid = r < a.Bl;
@@ -333,6 +341,7 @@ __global__ void __launch_bounds__(128) fc_anchor_kernel(StepArgs a) {
     const float s_ii = a.diag[a.row0 + rr];
     double s1, x1, s2, x2;
     reduce_partials(a, rr, valid, sub, s1, x1, s2, x2);
+    if (a.dbg && threadIdx.x == 0) { a.dbg[blockIdx.x * 8 + 2] = gtime(); a.dbg[blockIdx.x * 8 + 5] = __double_as_longlong(s1); }
     if (sub == 0 && valid) {
       const TableVals v = table_math(a, s1, x1, s2, x2, kr, kc, uo1, uo2, gamma);
       const AnchorParams p = anchor_params(a, v.u1, v.u2, t1, t2, tau, eps);
@@ -343,8 +352,10 @@ __global__ void __launch_bounds__(128) fc_anchor_kernel(StepArgs a) {
       a.sum1[r] = s1; a.dx1[r] = v.dx1; a.sum2[r] = s2; a.dx2[r] = v.dx2;
       store_payload(a, r, id, v, t1, t2);
     }
+    if (a.dbg && threadIdx.x == 0) a.dbg[blockIdx.x * 8 + 3] = gtime();
   }
   block_partials(a, ta, tb, tl, kmax);
+  if (a.dbg && threadIdx.x == 0) { a.dbg[blockIdx.x * 8 + 0] = t_entry; a.dbg[blockIdx.x * 8 + 1] = t_wait; a.dbg[blockIdx.x * 8 + 4] = gtime(); }
 }
 
 

@@ -26,6 +26,9 @@ struct StepResult {
   int err;
 };
 
+// lanes per anchor in fc_anchor_kernel (partial reduction width; the leader runs the fp64 chain)
+constexpr int kAnchorLanes = 8;
+
 struct StepArgs {
   // shapes / config
   int B, Bl, d, world, rank, row0, n_jt;
@@ -75,6 +78,7 @@ struct StepArgs {
   int* err;
   StepResult* result;
   float gscale;                          // c = 1 / (Bl (B-1)), engine.cpp:84-85
+  long long* dbg;                        // FC_SIM_DEBUG=9: per-block globaltimer stamps of fc_anchor_kernel
 };
 
 __global__ void fc_prep_kernel(const __nv_bfloat16* __restrict__ e1, const __nv_bfloat16* __restrict__ e2,

@@ -16,7 +16,7 @@ ids = torch.from_numpy(S.ids(B, N, 0)).cuda()
 for _ in range(3): st.step(e1, e2, ids, 0.6, 1e-14)
 torch.cuda.synchronize()
 R = 2688
-out = np.zeros(2 * R + 160 * 16, dtype=np.int64)
+out = np.zeros(2 * R + 160 * 16 + 4096, dtype=np.int64)
 P.lib().fc_debug_counters(st._h, out.ctypes.data_as(C.POINTER(C.c_longlong)))
 for k, name in enumerate(('pass1', 'pass2')):
     reg = out[k * R:(k + 1) * R]
@@ -61,3 +61,7 @@ print('  pass1: first entry', f(tls[0][:, 0].min()), 'last entry', f(tls[0][:, 0
 print('  pass2: first entry', f(tls[1][:, 0].min()), 'last entry', f(tls[1][:, 0].max()), 'first exit', f(tls[1][:, 2].min()), 'last exit', f(tls[1][:, 2].max()))
 if os.environ.get('FC_GEMM_DEBUG') in ('9', '10'):
     print('  gemm : first entry', f(g[:, 11].min()), 'last entry', f(g[:, 11].max()), 'epi end min', f(g[:, 10].min()), 'epi end max', f(g[:, 10].max()))
+an = out[2 * R + 160 * 16:2 * R + 160 * 16 + 640 * 8].reshape(640, 8)
+print('  anchor: entry', f(an[:, 0].min()), '..', f(an[:, 0].max()), 'wait done', f(an[:, 1].min()), '..', f(an[:, 1].max()),
+      'partials reduced', f(an[:, 2].min()), '..', f(an[:, 2].max()), 'fp64 done', f(an[:, 3].min()), '..', f(an[:, 3].max()),
+      'exit', f(an[:, 4].min()), '..', f(an[:, 4].max()))

@@ -114,3 +114,32 @@ def test_golden_fixtures_k1(golden_files):
             # (3e-3 at the tau floor); g/u/loss/tau/G_tau stay at 1e-3.
             _check(got, ref, f"{path} s{s}", tol_de=3e-3 if float(cfg["tau_init"]) <= 0.0051 else 2e-3)
         np.testing.assert_allclose(step.tables()["u1"], z["state_end_u1"], rtol=TOL)
+
+
+@pytest.mark.parametrize("variant,d", [("fastclip_v3", 768), ("fastclip_v1", 768), ("fastclip_v0", 1024),
+                                       ("fastclip_v2", 1024)])
+def test_step_wide_embeddings(variant, d):
+    # BASELINE configs 3/4: d = 768 / 1024 -> the anchor rows no longer fit the 8 resident
+    # K-block slots (A streams in 512-wide chunks) and the GEMM has two 512-column blocks
+    res, _, _, _ = run_pair(variant, B=384, d=d, N=3000, steps=2, seed=13)
+    for i, (got, ref) in enumerate(res):
+        _check(got, ref, f"{variant} d={d} step {i}")
+
+
+def test_large_table_indexing():
+    # BASELINE config 3 indexes a 315M-entry table: ids near the top of a large table (fp64
+    # SoA, 2.5 GB per u column) must land exactly; untouched entries stay bit-identical
+    import torch
+    import paper_2407_01445_b200 as P
+    N, B, d = 315_000_000, 256, 128
+    ocfg = O.default_config("fastclip_v3", N)
+    step = P.LossStep(gpu_cfg(ocfg, d, B))
+    ids = (N - 1 - np.arange(B, dtype=np.int64) * 977).astype(np.int32)
+    b1, b2 = S.embeddings(B, d, 21)
+    step.step(to_dev_bf16(b1), to_dev_bf16(b2), torch.from_numpy(ids).cuda(), 0.6, 1e-14)
+    views = step.local_views()
+    u = step.tables()["u1"]
+    np.testing.assert_array_equal(u[ids], views["u1"])     # the snapshot landed at exactly these ids
+    mask = np.ones(N, bool)
+    mask[ids] = False
+    assert not np.any(u[mask])                               # everything else untouched (zero-initialised)
