@@ -107,6 +107,8 @@ struct GemmParams {
   float scale;       // 1 / (Bl (B-1)), engine.cpp:84-85
   int debug;         // perf experiments: 1 = skip epilogue stores; 9 = counters / timelines into dbg_out
   long long* dbg_out;   // debug == 9: [cta][8] MMA / epilogue counters, globaltimer stamps
+  float* reset_at_exit; // 4 floats zeroed when the GEMM (the step's last kernel) retires: the
+                        // next step's norm / kappa bounds start from 0 without a memset node
 };
 
 // kSimFused (K = 1): one S tile gives both the row statistics (segment R) and the column

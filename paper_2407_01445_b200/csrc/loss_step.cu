@@ -118,8 +118,8 @@ struct LossStep {
   float* rcoef = nullptr;
   __nv_bfloat16* q = nullptr;   // [2][Bl][ldq]
   int* err = nullptr;
-  fc::StepResult* result_d = nullptr;
-  fc::StepResult* result_h = nullptr;   // pinned
+  fc::StepResult* result_d = nullptr;   // device alias of result_h (mapped pinned memory)
+  fc::StepResult* result_h = nullptr;   // written by the reduce kernel over PCIe: no D2H copy node
   cudaEvent_t done{}, fork{}, side_fork{}, side_join{}, zero_fork{}, zero_join{};
   cudaStream_t ws = nullptr;     // context stream (capturable), joined to the caller's stream
   cudaStream_t ws2 = nullptr;    // side branch: reductions / tau updates off the critical path
@@ -136,6 +136,12 @@ struct LossStep {
   struct GraphEntry {
     const void* key[5];
     cudaGraphExec_t exec;
+    cudaGraph_t graph;                 // kept: its prep node addresses the per-step parameter update
+    cudaGraphNode_t prep_node;
+    cudaKernelNodeParams prep_params;  // captured launch shape of fc_prep_kernel
+    const void* prep_e1;
+    const void* prep_e2;
+    fc::StepArgs prep_args;
   };
   std::vector<GraphEntry> graphs;
   // optional per-phase CUDA events (bench roofline): phases of the last step
@@ -220,6 +226,7 @@ struct LossStep {
       col_partial = dalloc<float2>(static_cast<size_t>((Bl + fc::kPairM - 1) / fc::kPairM) * 8 * ((B + 31) / 32 * 32));
     clamps = dalloc<unsigned long long>(1);
     bounds = dalloc<float>(4);
+    FC_CUDA(cudaMemset(bounds, 0, 4 * sizeof(float)));
     f64 = dalloc<double>(static_cast<size_t>(Bl) * 18);
     nblk = (Bl * fc::kAnchorLanes + kAnchorBlock - 1) / kAnchorBlock;
     pstride = 7 * Bl + 3 * nblk;
@@ -232,9 +239,9 @@ struct LossStep {
     q = dalloc<__nv_bfloat16>(2 * static_cast<size_t>(Bl) * ldq);
     err = dalloc<int>(1);
     FC_CUDA(cudaMemset(err, 0, sizeof(int)));
-    result_d = dalloc<fc::StepResult>(1);
-    FC_CUDA(cudaMallocHost(&result_h, sizeof(fc::StepResult)));
+    FC_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&result_h), sizeof(fc::StepResult), cudaHostAllocMapped));
     std::memset(result_h, 0, sizeof(*result_h));
+    FC_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&result_d), result_h, 0));
     FC_CUDA(cudaEventCreateWithFlags(&done, cudaEventDisableTiming));
     FC_CUDA(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming));
     FC_CUDA(cudaStreamCreateWithFlags(&ws, cudaStreamNonBlocking));
@@ -367,46 +374,75 @@ struct LossStep {
       throw FcError{FC_ERR_SHAPE, "fc_loss_step: null input/output pointer"};
     if (in->eps < 0.0) throw FcError{FC_ERR_DOMAIN, "epsilon must be non-negative"};
     if (track_u && (!(in->gamma > 0.0) || in->gamma > 1.0)) throw FcError{FC_ERR_DOMAIN, "gamma must be in (0,1]"};
-    const double sc[2] = {in->gamma, in->eps};
-    FC_CUDA(cudaEventRecord(fork, caller));
-    FC_CUDA(cudaStreamWaitEvent(ws, fork, 0));
-    // pageable source: the values are staged at call time, the copy runs in stream order
-    FC_CUDA(cudaMemcpyAsync(scal, sc, sizeof(sc), cudaMemcpyHostToDevice, ws));
     if (use_graph && !timing) {   // phase timing: direct launches (events between kernels)
       const void* key[5] = {in->e1, in->e2, in->ids, out->de1, timing ? nullptr : out->de2};
-      cudaGraphExec_t exec = nullptr;
+      GraphEntry* ge = nullptr;
       for (auto& g : graphs)
-        if (std::memcmp(g.key, key, sizeof(key)) == 0) exec = g.exec;
-      if (!exec) {
+        if (std::memcmp(g.key, key, sizeof(key)) == 0) ge = &g;
+      if (!ge) {
         if (graphs.size() >= 8) {
           cudaGraphExecDestroy(graphs.front().exec);
+          cudaGraphDestroy(graphs.front().graph);
           graphs.erase(graphs.begin());
         }
-        cudaGraph_t graph;
+        GraphEntry g{};
         FC_CUDA(cudaStreamBeginCapture(ws, cudaStreamCaptureModeThreadLocal));
         try {
           enqueue(in, out, ws);
         } catch (...) {
-          cudaStreamEndCapture(ws, &graph);
+          cudaStreamEndCapture(ws, &g.graph);
+          if (g.graph) cudaGraphDestroy(g.graph);
           throw;
         }
-        FC_CUDA(cudaStreamEndCapture(ws, &graph));
-        FC_CUDA(cudaGraphInstantiate(&exec, graph, 0));
-        cudaGraphDestroy(graph);
-        GraphEntry ge;
-        std::memcpy(ge.key, key, sizeof(key));
-        ge.exec = exec;
-        graphs.push_back(ge);
+        FC_CUDA(cudaStreamEndCapture(ws, &g.graph));
+        FC_CUDA(cudaGraphInstantiate(&g.exec, g.graph, 0));
+        // the prep kernel node carries the step scalars (gamma_t, eps_t) as parameters
+        size_t n = 0;
+        FC_CUDA(cudaGraphGetNodes(g.graph, nullptr, &n));
+        std::vector<cudaGraphNode_t> nodes(n);
+        FC_CUDA(cudaGraphGetNodes(g.graph, nodes.data(), &n));
+        for (auto nd : nodes) {
+          cudaGraphNodeType t;
+          FC_CUDA(cudaGraphNodeGetType(nd, &t));
+          if (t != cudaGraphNodeTypeKernel) continue;
+          cudaKernelNodeParams kp{};
+          FC_CUDA(cudaGraphKernelNodeGetParams(nd, &kp));
+          if (kp.func == reinterpret_cast<void*>(fc::fc_prep_kernel)) {
+            g.prep_node = nd;
+            g.prep_params = kp;
+          }
+        }
+        if (!g.prep_node) throw FcError{FC_ERR_CUDA, "captured step graph has no prep node"};
+        g.prep_e1 = last_prep_e1;
+        g.prep_e2 = last_prep_e2;
+        g.prep_args = last_prep_args;
+        std::memcpy(g.key, key, sizeof(key));
+        graphs.push_back(g);
+        ge = &graphs.back();
       }
-      FC_CUDA(cudaGraphLaunch(exec, ws));
+      double gamma = in->gamma, eps = in->eps;
+      const void* e1 = ge->prep_e1;
+      const void* e2 = ge->prep_e2;
+      void* args[5] = {&e1, &e2, &ge->prep_args, &gamma, &eps};
+      cudaKernelNodeParams kp = ge->prep_params;
+      kp.kernelParams = args;
+      kp.extra = nullptr;
+      FC_CUDA(cudaGraphExecKernelNodeSetParams(ge->exec, ge->prep_node, &kp));
+      FC_CUDA(cudaGraphLaunch(ge->exec, caller));   // the replay joins the caller's stream directly
+      FC_CUDA(cudaEventRecord(done, caller));        // fc_step_scalars_get waits on it
     } else {
+      FC_CUDA(cudaEventRecord(fork, caller));
+      FC_CUDA(cudaStreamWaitEvent(ws, fork, 0));
       enqueue(in, out, ws);
+      FC_CUDA(cudaEventRecord(done, ws));
+      FC_CUDA(cudaStreamWaitEvent(caller, done, 0));
     }
-    FC_CUDA(cudaEventRecord(done, ws));
-    FC_CUDA(cudaStreamWaitEvent(caller, done, 0));
     if (timing) ev_last = ev_cur, ev_cur = (ev_cur + 1) % ev_slots;
   }
   int ev_last = 0;
+  const void* last_prep_e1 = nullptr;   // arguments of the last enqueued prep kernel (graph capture)
+  const void* last_prep_e2 = nullptr;
+  fc::StepArgs last_prep_args{};
 
   void enqueue(const fc_step_in* in, fc_step_out* out, cudaStream_t st) {
     const __nv_bfloat16* E1 = static_cast<const __nv_bfloat16*>(in->e1);
@@ -434,8 +470,12 @@ struct LossStep {
                                               static_cast<long long>(Bl) * d / 4);
     FC_CUDA(cudaGetLastError());
     FC_CUDA(cudaEventRecord(zero_join, ws2));
-    FC_CUDA(cudaMemsetAsync(bounds, 0, 4 * sizeof(float), st));
-    fc::fc_prep_kernel<<<(B * 32 + 127) / 128, 128, 0, st>>>(E1, E2, a);   // one wave: <= 9 blocks/SM
+    if (sim_debug == 9) a.dbg = dbg_buf + 2 * 2688 + 160 * 16;
+    // bounds were zeroed by the previous step's GEMM (and at creation)
+    fc::fc_prep_kernel<<<(B * 32 + 127) / 128, 128, 0, st>>>(E1, E2, a, in->gamma, in->eps);   // one wave
+    last_prep_e1 = E1;
+    last_prep_e2 = E2;
+    last_prep_args = a;
     FC_CUDA(cudaGetLastError());
 
     // ---- pass 1: row statistics of S[L,G] (segment R) and S^T[L,G] (segment C) ----
@@ -550,6 +590,7 @@ struct LossStep {
     gp.kb_total = ldq / fc::kBlockK;
     gp.scale = static_cast<float>(1.0 / (static_cast<double>(Bl) * static_cast<double>(B - 1)));
     gp.debug = gemm_debug;
+    gp.reset_at_exit = bounds;
     if (gemm_debug >= 9) gp.dbg_out = dbg_buf + 2 * 2688;
     for (int s = 0; s < 2; ++s) {
       fc::GemmSeg& g = gp.seg[s];
@@ -580,7 +621,6 @@ struct LossStep {
     mark(6, st);
 
     FC_CUDA(cudaStreamWaitEvent(st, side_join, 0));
-    FC_CUDA(cudaMemcpyAsync(result_h, result_d, sizeof(fc::StepResult), cudaMemcpyDeviceToHost, st));
   }
 
   int kernels_per_step() const {
@@ -591,7 +631,10 @@ struct LossStep {
   void destroy() {
     // graphs first: NCCL keeps the communicator alive while a graph holds captured collectives
     cudaDeviceSynchronize();
-    for (auto& g : graphs) cudaGraphExecDestroy(g.exec);
+    for (auto& g : graphs) {
+      cudaGraphExecDestroy(g.exec);
+      cudaGraphDestroy(g.graph);
+    }
     graphs.clear();
     if (comm) {
       cudaDeviceSynchronize();
@@ -600,7 +643,7 @@ struct LossStep {
     for (void* p : {(void*)u1, (void*)u2, (void*)tau1, (void*)tau2, (void*)m1, (void*)v1, (void*)m2, (void*)v2,
                     (void*)s1, (void*)s2, (void*)tau_state, (void*)e1g, (void*)e2g, (void*)diag, (void*)rowstat,
                     (void*)partial, (void*)col_partial, (void*)clamps, (void*)bounds, (void*)f64, (void*)red, (void*)par, (void*)rcoef,
-                    (void*)q, (void*)err, (void*)result_d})
+                    (void*)q, (void*)err})
       if (p) cudaFree(p);
     if (recv && recv != send) cudaFree(recv);
     if (send) cudaFree(send);
@@ -850,6 +893,19 @@ int fc_phase_times(void* ctx, int32_t slot, float* ms, int32_t n) {
     cudaEvent_t* e = s->ev.data() + static_cast<size_t>(k) * (LossStep::kPhases + 1);
     FC_CUDA(cudaEventSynchronize(e[LossStep::kPhases]));
     for (int i = 0; i < n && i < LossStep::kPhases; ++i) FC_CUDA(cudaEventElapsedTime(&ms[i], e[i], e[i + 1]));
+  });
+}
+
+int fc_debug_reset(void* ctx) {   // debug timeline: prep first-entry (min) / last-exit (max) slots
+  if (!ctx) return FC_ERR_SHAPE;
+  auto* s = static_cast<LossStep*>(ctx);
+  return guarded([&] {
+    FC_CUDA(cudaDeviceSynchronize());
+    if (s->dbg_buf) {
+      long long* slot = s->dbg_buf + 2 * 2688 + 160 * 16 + 8 * 640;
+      FC_CUDA(cudaMemset(slot, 0xff, 8));
+      FC_CUDA(cudaMemset(slot + 1, 0, 8));
+    }
   });
 }
 

@@ -32,10 +32,22 @@ constexpr double kLog2eD = 1.4426950408889634073599;
 // anchors also snapshot tau^t (global tau, or IndividualTemp by id, state.cpp:112-122) and
 // emit the pass-1 row parameters.
 __global__ void fc_prep_kernel(const __nv_bfloat16* __restrict__ e1, const __nv_bfloat16* __restrict__ e2,
-                               StepArgs a) {
+                               StepArgs a, double gamma, double eps) {
   const int w = (blockIdx.x * blockDim.x + threadIdx.x) / 32;
   const int lane = threadIdx.x & 31;
-  if (w == 0 && lane == 0) *a.clamps = 0ull;
+  if (a.dbg && threadIdx.x == 0) {   // debug timeline: first entry / last exit of the grid
+    long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    atomicMin(reinterpret_cast<unsigned long long*>(a.dbg + 8 * 640), static_cast<unsigned long long>(t));
+  }
+  if (w == 0 && lane == 0) {
+    *a.clamps = 0ull;
+    // the step scalars arrive as kernel parameters (updated in the replayed graph per step,
+    // no host-to-device copy) and are published for the later kernels of the step
+    double* sc = const_cast<double*>(a.scal);
+    sc[0] = gamma;
+    sc[1] = eps;
+  }
   const bool valid = w < a.B;
   const int r = w - a.row0;
   const bool lead = valid && lane == 0 && r >= 0 && r < a.Bl;   // this rank's anchor, lane 0
@@ -105,6 +117,11 @@ __global__ void fc_prep_kernel(const __nv_bfloat16* __restrict__ e1, const __nv_
   const float k1 = static_cast<float>(kLog2eD / t1), k2 = static_cast<float>(kLog2eD / t2);
   a.rowstat_R[r] = make_float2(k1, -acc * k1);   // y = s * kappa + beta (log2-domain exponent)
   a.rowstat_C[r] = make_float2(k2, -acc * k2);
+  if (a.dbg) {
+    long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    atomicMax(reinterpret_cast<unsigned long long*>(a.dbg + 8 * 640 + 1), static_cast<unsigned long long>(t));
+  }
 }
 
 // ---- per-anchor arithmetic as pure functions of register values; the kernels below do the

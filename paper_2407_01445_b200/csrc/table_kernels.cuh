@@ -82,7 +82,7 @@ struct StepArgs {
 };
 
 __global__ void fc_prep_kernel(const __nv_bfloat16* __restrict__ e1, const __nv_bfloat16* __restrict__ e2,
-                               StepArgs a);
+                               StepArgs a, double gamma, double eps);
 __global__ void fc_weights_kernel(StepArgs a);
 __global__ void fc_anchor_kernel(StepArgs a);
 __global__ void fc_zero_kernel(float4* a0, float4* a1, long long n4);

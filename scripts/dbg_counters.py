@@ -16,7 +16,7 @@ ids = torch.from_numpy(S.ids(B, N, 0)).cuda()
 for _ in range(3): st.step(e1, e2, ids, 0.6, 1e-14)
 torch.cuda.synchronize()
 R = 2688
-out = np.zeros(2 * R + 160 * 16 + 4096, dtype=np.int64)
+out = np.zeros(2 * R + 160 * 16 + 8192, dtype=np.int64)
 P.lib().fc_debug_counters(st._h, out.ctypes.data_as(C.POINTER(C.c_longlong)))
 for k, name in enumerate(('pass1', 'pass2')):
     reg = out[k * R:(k + 1) * R]
@@ -51,6 +51,9 @@ st.disable_phase_timing()
 for _ in range(3): st.step(e1, e2, ids, 0.6, 1e-14)
 torch.cuda.synchronize()
 out[:] = 0
+P.lib().fc_debug_reset(st._h)
+st.step(e1, e2, ids, 0.6, 1e-14)
+torch.cuda.synchronize()
 P.lib().fc_debug_counters(st._h, out.ctypes.data_as(C.POINTER(C.c_longlong)))
 tls = [out[k * R + 2048:k * R + 2048 + 148 * 4].reshape(148, 4) for k in range(2)]
 g = out[2 * R:2 * R + 160 * 16].reshape(160, 16)[:148]
@@ -65,3 +68,4 @@ an = out[2 * R + 160 * 16:2 * R + 160 * 16 + 640 * 8].reshape(640, 8)
 print('  anchor: entry', f(an[:, 0].min()), '..', f(an[:, 0].max()), 'wait done', f(an[:, 1].min()), '..', f(an[:, 1].max()),
       'partials reduced', f(an[:, 2].min()), '..', f(an[:, 2].max()), 'fp64 done', f(an[:, 3].min()), '..', f(an[:, 3].max()),
       'exit', f(an[:, 4].min()), '..', f(an[:, 4].max()))
+print('  prep: first entry', f(out[2 * R + 160 * 16 + 8 * 640]), 'last exit', f(out[2 * R + 160 * 16 + 8 * 640 + 1]))
