@@ -133,21 +133,29 @@ constexpr int kGroup = kAnchorLanes;
 
 // Fixed-order (group-lane-strided + xor tree) reduction of one anchor's pass-1 partials; every
 // lane of the warp must call it (valid = false contributes nothing).
-// Sum of n strided float2 partials, lane `sub` of the group taking q = sub, sub + kGroup, ...
-// in ascending order; loads are issued eight at a time so their latencies overlap.
-__device__ __forceinline__ void sum_partials(const float2* __restrict__ base, size_t stride, int n, int sub,
-                                             double& s, double& x) {
-  for (int q0 = sub; q0 < n; q0 += 8 * kGroup) {
-    float2 v[8];
+// The anchor's row partials (n_r, contiguous) and column partials (n_c, stride cs) are summed
+// by the kGroup lanes in a fixed order (lane `sub` takes q = sub, sub + kGroup, ... of each
+// list, row list first). The loads of both lists go out 16 at a time from one virtual index
+// space, so a lane waits for ~2 memory round trips instead of one per 8 loads.
+__device__ __forceinline__ void sum_two(const float2* __restrict__ rp, int n_r, const float2* __restrict__ cp,
+                                        size_t cs, int n_c, int sub, double& s1, double& x1, double& s2,
+                                        double& x2) {
+  const int m_r = n_r > sub ? (n_r - sub + kGroup - 1) / kGroup : 0;   // this lane's row items
+  const int m_c = n_c > sub ? (n_c - sub + kGroup - 1) / kGroup : 0;
+  const int m = m_r + m_c;
+  for (int t0 = 0; t0 < m; t0 += 16) {
+    float2 v[16];
 #pragma unroll
-    for (int t = 0; t < 8; ++t) {
-      const int q = q0 + t * kGroup;
-      v[t] = q < n ? __ldg(base + q * stride) : make_float2(0.f, 0.f);
+    for (int t = 0; t < 16; ++t) {
+      const int i = t0 + t;
+      v[t] = i < m_r ? __ldg(rp + sub + i * kGroup)
+           : (i < m ? __ldg(cp + (sub + (i - m_r) * kGroup) * cs) : make_float2(0.f, 0.f));
     }
 #pragma unroll
-    for (int t = 0; t < 8; ++t) {
-      s += v[t].x;
-      x += v[t].y;
+    for (int t = 0; t < 16; ++t) {
+      const int i = t0 + t;
+      if (i < m_r) { s1 += v[t].x; x1 += v[t].y; }
+      else if (i < m) { s2 += v[t].x; x2 += v[t].y; }
     }
   }
 }
@@ -157,12 +165,13 @@ __device__ __forceinline__ void reduce_partials(const StepArgs& a, int r, bool v
   const int nparts = a.n_jt * 4;
   s1 = 0.0; x1 = 0.0; s2 = 0.0; x2 = 0.0;
   if (valid) {
-    sum_partials(a.partial_R + static_cast<size_t>(r) * nparts, 1, nparts, sub, s1, x1);
+    const float2* rp = a.partial_R + static_cast<size_t>(r) * nparts;
     if (a.col_slots > 0) {   // fused pass 1: column statistics of S, [B/32][slots][32]
       const int j = a.row0 + r;
-      sum_partials(a.col_partial + static_cast<size_t>(j >> 5) * a.col_slots * 32 + (j & 31), 32, a.col_slots, sub, s2, x2);
+      sum_two(rp, nparts, a.col_partial + static_cast<size_t>(j >> 5) * a.col_slots * 32 + (j & 31), 32,
+              a.col_slots, sub, s1, x1, s2, x2);
     } else {
-      sum_partials(a.partial_C + static_cast<size_t>(r) * nparts, 1, nparts, sub, s2, x2);
+      sum_two(rp, nparts, a.partial_C + static_cast<size_t>(r) * nparts, 1, nparts, sub, s1, x1, s2, x2);
     }
   }
 #pragma unroll
