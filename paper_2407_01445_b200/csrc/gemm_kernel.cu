@@ -253,6 +253,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     const uint32_t cg = warp >> 2;
     uint8_t* stage_out = L.out + warp * kGemmStageOut;
     const uint32_t leader = crank & ~1u;
+    // r_i (per-anchor kernel) and the X rows are read before the first accumulator wait:
+    // wait for the predecessor grid like the producer does (programmatic launch)
+    griddep_wait();
     const bool eprof = p.debug >= 9 && warp == 0;
     long long e0 = clock64(), e_wait = 0;
     int it = 0;

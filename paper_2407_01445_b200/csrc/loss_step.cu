@@ -245,7 +245,11 @@ struct LossStep {
     FC_CUDA(cudaEventCreateWithFlags(&done, cudaEventDisableTiming));
     FC_CUDA(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming));
     FC_CUDA(cudaStreamCreateWithFlags(&ws, cudaStreamNonBlocking));
-    FC_CUDA(cudaStreamCreateWithFlags(&ws2, cudaStreamNonBlocking));
+    {
+      int lo = 0, hi = 0;   // numerically greatest = lowest priority
+      FC_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+      FC_CUDA(cudaStreamCreateWithPriority(&ws2, cudaStreamNonBlocking, lo));
+    }
     FC_CUDA(cudaEventCreateWithFlags(&side_fork, cudaEventDisableTiming));
     FC_CUDA(cudaEventCreateWithFlags(&side_join, cudaEventDisableTiming));
     FC_CUDA(cudaEventCreateWithFlags(&zero_fork, cudaEventDisableTiming));
@@ -463,20 +467,21 @@ struct LossStep {
     a.scal = scal;
 
     mark(1, st);
-    if (sim_debug == 9) a.dbg = dbg_buf + 2 * 2688 + 160 * 16;
-    // bounds were zeroed by the previous step's GEMM (and at creation)
-    fc::fc_prep_kernel<<<(B * 32 + 127) / 128, 128, 0, st>>>(E1, E2, a, in->gamma, in->eps);   // one wave
-    last_prep_e1 = E1;
-    last_prep_e2 = E2;
-    last_prep_args = a;
-    // side branch: zero dE (the GEMM's reduce-add target) while pass 1 runs -- after prep, so
-    // the 2 Bl d fp32 writes do not compete with prep's embedding reads for HBM
+    // side branch: zero dE (the GEMM's reduce-add target). ws2 has the lowest stream priority,
+    // so the block scheduler dispatches prep / pass 1 first and the zeroing fills in behind
+    // them (no event between the programmatically linked kernels of the main stream)
     FC_CUDA(cudaEventRecord(zero_fork, st));
     FC_CUDA(cudaStreamWaitEvent(ws2, zero_fork, 0));
     fc::fc_zero_kernel<<<n_sm, 256, 0, ws2>>>(reinterpret_cast<float4*>(out->de1), reinterpret_cast<float4*>(out->de2),
                                               static_cast<long long>(Bl) * d / 4);
     FC_CUDA(cudaGetLastError());
     FC_CUDA(cudaEventRecord(zero_join, ws2));
+    if (sim_debug == 9) a.dbg = dbg_buf + 2 * 2688 + 160 * 16;
+    // bounds were zeroed by the previous step's GEMM (and at creation)
+    fc::fc_prep_kernel<<<(B * 32 + 127) / 128, 128, 0, st>>>(E1, E2, a, in->gamma, in->eps);   // one wave
+    last_prep_e1 = E1;
+    last_prep_e2 = E2;
+    last_prep_args = a;
     FC_CUDA(cudaGetLastError());
 
     // ---- pass 1: row statistics of S[L,G] (segment R) and S^T[L,G] (segment C) ----
