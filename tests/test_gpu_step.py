@@ -143,3 +143,16 @@ def test_large_table_indexing():
     mask = np.ones(N, bool)
     mask[ids] = False
     assert not np.any(u[mask])                               # everything else untouched (zero-initialised)
+
+
+@pytest.mark.parametrize("env", [{"FC_GRAPH": "0"}, {"FC_PDL": "0"}, {"FC_FUSED_P1": "0"}, {"FC_Q_FACTOR": "0"}])
+def test_step_launch_modes(env, monkeypatch):
+    # the same step through the non-default launch paths: direct launches (programmatic
+    # dependent launches without a graph), no PDL, the two-segment pass 1 and the
+    # two-exponential Q path -- all must agree with the oracle
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    for variant in ("fastclip_v3", "fastclip_v2"):
+        res, _, _, _ = run_pair(variant, B=320, d=96, N=4000, steps=3, seed=17)
+        for i, (got, ref) in enumerate(res):
+            _check(got, ref, f"{env} {variant} step {i}")
