@@ -113,6 +113,23 @@ struct GemmParams {
 
 // kSimFused (K = 1): one S tile gives both the row statistics (segment R) and the column
 // statistics (segment C = S^T), so pass 1 multiplies S once instead of twice.
+// ---- NVLink peer all-gather (K > 1): this rank's slices into every rank's buffer + flags ----
+constexpr int kMaxPeers = 8;
+struct PeerGather {
+  const uint8_t* src[2];              // this rank's slices (bytes each)
+  uint8_t* dst[2][kMaxPeers];         // every rank's gather destination (peer-mapped), slice at rank*bytes
+  size_t bytes;                       // bytes per slice (multiple of 16)
+  int n_src;
+  int world, rank;
+  unsigned long long seq;             // per-step sequence number (updated in the replayed graph)
+  unsigned long long* peer_flag[kMaxPeers];   // rank k's flag array for this gather (peer-mapped)
+  unsigned long long* my_flag;        // local flag array [world]
+  unsigned* ticket;                   // local grid-completion ticket
+  int* err;
+};
+cudaError_t launch_peer_gather(const PeerGather& g, int blocks, cudaStream_t s);
+void* peer_gather_kernel_fn();
+
 enum SimMode { kSimStats = 0, kSimQ = 1, kSimRaw = 2, kSimFused = 3 };
 
 cudaError_t launch_sim(int mode, const SimParams& p, const CUtensorMap* mapA, const CUtensorMap* mapB,

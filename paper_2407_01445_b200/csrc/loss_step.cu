@@ -107,6 +107,14 @@ struct LossStep {
   fc::TauState* tau_state = nullptr;
   // workspaces
   __nv_bfloat16 *e1g = nullptr, *e2g = nullptr;   // gathered embeddings (K > 1)
+  // NVLink peer gathers (K > 1, all ranks P2P-capable; FC_PEER=0 forces the NCCL path)
+  bool use_peer = false;
+  int my_dev = 0;
+  unsigned long long* pflags = nullptr;   // [2][kMaxPeers] local flags: E gather, payload gather
+  unsigned* ptickets = nullptr;           // [2] grid-completion tickets
+  std::vector<void*> peer_maps;           // cudaIpcOpenMemHandle mappings to close
+  fc::PeerGather pg_e{}, pg_p{};
+  unsigned long long seq = 0;             // per-step sequence number (same on every rank)
   float* diag = nullptr;
   float2 *rowstat = nullptr, *partial = nullptr, *col_partial = nullptr;
   unsigned long long* clamps = nullptr;
@@ -142,6 +150,12 @@ struct LossStep {
     const void* prep_e1;
     const void* prep_e2;
     fc::StepArgs prep_args;
+    struct PeerNode {
+      cudaGraphNode_t node;
+      cudaKernelNodeParams kp;
+      fc::PeerGather pg;
+    };
+    std::vector<PeerNode> peer_nodes;   // gathers whose sequence number changes every replay
   };
   std::vector<GraphEntry> graphs;
   // optional per-phase CUDA events (bench roofline): phases of the last step
@@ -191,6 +205,7 @@ struct LossStep {
     n_jt = (B + fc::kPairN - 1) / fc::kPairN;
     FC_CUDA(cudaSetDevice(cfg.device));
     n_sm = sm_count(cfg.device);
+    my_dev = cfg.device;
 
     const size_t N = static_cast<size_t>(cfg.n_train);
     u1 = dalloc<double>(N);
@@ -238,6 +253,7 @@ struct LossStep {
     rcoef = dalloc<float>(Bl);
     q = dalloc<__nv_bfloat16>(2 * static_cast<size_t>(Bl) * ldq);
     err = dalloc<int>(1);
+    if (K > 1) setup_peers();
     FC_CUDA(cudaMemset(err, 0, sizeof(int)));
     FC_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&result_h), sizeof(fc::StepResult), cudaHostAllocMapped));
     std::memset(result_h, 0, sizeof(*result_h));
@@ -321,6 +337,91 @@ struct LossStep {
     a.red = red; a.err = err; a.result = result_d;
   }
 
+  // CUDA IPC mappings of every rank's gather destinations and flag arrays; handles travel
+  // over the NCCL communicator once. Falls back to NCCL gathers when a pair of GPUs cannot
+  // map each other's memory.
+  void setup_peers() {
+    if (const char* e = std::getenv("FC_PEER"))
+      if (atoi(e) == 0) return;
+    if (K > fc::kMaxPeers) return;
+    // the ranks' device ordinals (one node), then every pair must be able to map the other
+    cudaStream_t s0;
+    FC_CUDA(cudaStreamCreateWithFlags(&s0, cudaStreamNonBlocking));
+    int* ddev = dalloc<int>(K + 1);
+    FC_CUDA(cudaMemcpy(ddev + K, &my_dev, sizeof(int), cudaMemcpyHostToDevice));
+    FC_NCCL(ncclAllGather(ddev + K, ddev, 1, ncclInt32, comm, s0));
+    FC_CUDA(cudaStreamSynchronize(s0));
+    std::vector<int> devs(K);
+    FC_CUDA(cudaMemcpy(devs.data(), ddev, K * sizeof(int), cudaMemcpyDeviceToHost));
+    cudaFree(ddev);
+    int ok = 1;
+    for (int k = 0; k < K; ++k) {
+      if (devs[k] == my_dev) continue;
+      int can = 0;
+      if (cudaDeviceCanAccessPeer(&can, my_dev, devs[k]) != cudaSuccess || !can) ok = 0;
+    }
+    // every rank must agree: all-reduce the capability (min) over the communicator
+    int* dok = dalloc<int>(1);
+    FC_CUDA(cudaMemcpy(dok, &ok, sizeof(int), cudaMemcpyHostToDevice));
+    FC_NCCL(ncclAllReduce(dok, dok, 1, ncclInt32, ncclMin, comm, s0));
+    FC_CUDA(cudaStreamSynchronize(s0));
+    FC_CUDA(cudaMemcpy(&ok, dok, sizeof(int), cudaMemcpyDeviceToHost));
+    cudaFree(dok);
+    if (!ok) {
+      cudaStreamDestroy(s0);
+      return;
+    }
+    pflags = dalloc<unsigned long long>(2 * fc::kMaxPeers);
+    FC_CUDA(cudaMemset(pflags, 0, 2 * fc::kMaxPeers * sizeof(unsigned long long)));
+    ptickets = dalloc<unsigned>(2);
+    FC_CUDA(cudaMemset(ptickets, 0, 2 * sizeof(unsigned)));
+    void* mine[4] = {e1g, e2g, recv, pflags};
+    cudaIpcMemHandle_t h[4];
+    for (int i = 0; i < 4; ++i) FC_CUDA(cudaIpcGetMemHandle(&h[i], mine[i]));
+    uint8_t* dh = dalloc<uint8_t>(sizeof(h) * (K + 1));
+    FC_CUDA(cudaMemcpy(dh + sizeof(h) * K, h, sizeof(h), cudaMemcpyHostToDevice));
+    FC_NCCL(ncclAllGather(dh + sizeof(h) * K, dh, sizeof(h), ncclUint8, comm, s0));
+    FC_CUDA(cudaStreamSynchronize(s0));
+    cudaStreamDestroy(s0);
+    std::vector<cudaIpcMemHandle_t> all(4 * static_cast<size_t>(K));
+    FC_CUDA(cudaMemcpy(all.data(), dh, sizeof(h) * K, cudaMemcpyDeviceToHost));
+    cudaFree(dh);
+    void* peer[4][fc::kMaxPeers] = {};
+    for (int k = 0; k < K; ++k)
+      for (int i = 0; i < 4; ++i) {
+        if (k == rank) {
+          peer[i][k] = mine[i];
+        } else {
+          FC_CUDA(cudaIpcOpenMemHandle(&peer[i][k], all[4 * k + i], cudaIpcMemLazyEnablePeerAccess));
+          peer_maps.push_back(peer[i][k]);
+        }
+      }
+    pg_e = fc::PeerGather{};
+    pg_e.bytes = static_cast<size_t>(Bl) * d * 2;
+    pg_e.n_src = 2;
+    pg_p = fc::PeerGather{};
+    pg_p.bytes = static_cast<size_t>(pstride) * 8;
+    pg_p.n_src = 1;
+    pg_p.src[0] = reinterpret_cast<const uint8_t*>(send);
+    for (fc::PeerGather* g : {&pg_e, &pg_p}) {
+      g->world = K;
+      g->rank = rank;
+      g->err = err;
+    }
+    for (int k = 0; k < K; ++k) {
+      pg_e.dst[0][k] = static_cast<uint8_t*>(peer[0][k]);
+      pg_e.dst[1][k] = static_cast<uint8_t*>(peer[1][k]);
+      pg_p.dst[0][k] = static_cast<uint8_t*>(peer[2][k]);
+      pg_e.peer_flag[k] = static_cast<unsigned long long*>(peer[3][k]);
+      pg_p.peer_flag[k] = static_cast<unsigned long long*>(peer[3][k]) + fc::kMaxPeers;
+    }
+    pg_e.my_flag = pflags;
+    pg_p.my_flag = pflags + fc::kMaxPeers;
+    pg_e.ticket = ptickets;
+    pg_p.ticket = ptickets + 1;
+    use_peer = true;
+  }
+
   void ensure_maps(const void* e1, const void* e2) {
     if (e1 == map_e1 && e2 == map_e2) return;
     const uint64_t rb = static_cast<uint64_t>(d) * 2;
@@ -378,6 +479,7 @@ struct LossStep {
       throw FcError{FC_ERR_SHAPE, "fc_loss_step: null input/output pointer"};
     if (in->eps < 0.0) throw FcError{FC_ERR_DOMAIN, "epsilon must be non-negative"};
     if (track_u && (!(in->gamma > 0.0) || in->gamma > 1.0)) throw FcError{FC_ERR_DOMAIN, "gamma must be in (0,1]"};
+    ++seq;   // every rank calls step() the same number of times: the peer-gather handshake value
     if (use_graph && !timing) {   // phase timing: direct launches (events between kernels)
       const void* key[5] = {in->e1, in->e2, in->ids, out->de1, timing ? nullptr : out->de2};
       GraphEntry* ge = nullptr;
@@ -410,10 +512,17 @@ struct LossStep {
           FC_CUDA(cudaGraphNodeGetType(nd, &t));
           if (t != cudaGraphNodeTypeKernel) continue;
           cudaKernelNodeParams kp{};
-          FC_CUDA(cudaGraphKernelNodeGetParams(nd, &kp));
+          if (cudaGraphKernelNodeGetParams(nd, &kp) != cudaSuccess) {   // e.g. NCCL's own kernels
+            cudaGetLastError();
+            continue;
+          }
           if (kp.func == reinterpret_cast<void*>(fc::fc_prep_kernel)) {
             g.prep_node = nd;
             g.prep_params = kp;
+          }
+          if (kp.func == fc::peer_gather_kernel_fn()) {
+            GraphEntry::PeerNode pn{nd, kp, *static_cast<fc::PeerGather*>(kp.kernelParams[0])};
+            g.peer_nodes.push_back(pn);
           }
         }
         if (!g.prep_node) throw FcError{FC_ERR_CUDA, "captured step graph has no prep node"};
@@ -432,6 +541,14 @@ struct LossStep {
       kp.kernelParams = args;
       kp.extra = nullptr;
       FC_CUDA(cudaGraphExecKernelNodeSetParams(ge->exec, ge->prep_node, &kp));
+      for (auto& pn : ge->peer_nodes) {
+        pn.pg.seq = seq;
+        void* pargs[1] = {&pn.pg};
+        cudaKernelNodeParams pk = pn.kp;
+        pk.kernelParams = pargs;
+        pk.extra = nullptr;
+        FC_CUDA(cudaGraphExecKernelNodeSetParams(ge->exec, pn.node, &pk));
+      }
       FC_CUDA(cudaGraphLaunch(ge->exec, caller));   // the replay joins the caller's stream directly
       FC_CUDA(cudaEventRecord(done, caller));        // fc_step_scalars_get waits on it
     } else {
@@ -453,10 +570,18 @@ struct LossStep {
     const __nv_bfloat16* E2 = static_cast<const __nv_bfloat16*>(in->e2);
     mark(0, st);
     if (K > 1) {
-      FC_NCCL(ncclGroupStart());
-      FC_NCCL(ncclAllGather(E1, e1g, static_cast<size_t>(Bl) * d * 2, ncclUint8, comm, st));
-      FC_NCCL(ncclAllGather(E2, e2g, static_cast<size_t>(Bl) * d * 2, ncclUint8, comm, st));
-      FC_NCCL(ncclGroupEnd());
+      if (use_peer) {   // NVLink stores into every rank's e1g / e2g, flag handshake
+        fc::PeerGather g = pg_e;
+        g.src[0] = reinterpret_cast<const uint8_t*>(E1);
+        g.src[1] = reinterpret_cast<const uint8_t*>(E2);
+        g.seq = seq;
+        FC_CUDA(fc::launch_peer_gather(g, n_sm, st));
+      } else {
+        FC_NCCL(ncclGroupStart());
+        FC_NCCL(ncclAllGather(E1, e1g, static_cast<size_t>(Bl) * d * 2, ncclUint8, comm, st));
+        FC_NCCL(ncclAllGather(E2, e2g, static_cast<size_t>(Bl) * d * 2, ncclUint8, comm, st));
+        FC_NCCL(ncclGroupEnd());
+      }
       E1 = e1g;
       E2 = e2g;
     }
@@ -546,7 +671,13 @@ struct LossStep {
     if (K > 1) {
       // ONE all-gather carries u/tau/id, the v2 per-index tau gradients and the G_tau / loss
       // block partials of every rank (no scalar all-reduce, no second gather)
-      FC_NCCL(ncclAllGather(send, recv, static_cast<size_t>(pstride), ncclFloat64, comm, st));
+      if (use_peer) {
+        fc::PeerGather g = pg_p;
+        g.seq = seq;
+        FC_CUDA(fc::launch_peer_gather(g, 32, st));
+      } else {
+        FC_NCCL(ncclAllGather(send, recv, static_cast<size_t>(pstride), ncclFloat64, comm, st));
+      }
       fc::fc_weights_kernel<<<(B + kWeightsBlock - 1) / kWeightsBlock, kWeightsBlock, 0, st>>>(a);
       FC_CUDA(cudaGetLastError());
     }
@@ -642,6 +773,8 @@ struct LossStep {
       cudaGraphDestroy(g.graph);
     }
     graphs.clear();
+    for (void* m : peer_maps) cudaIpcCloseMemHandle(m);
+    peer_maps.clear();
     if (comm) {
       cudaDeviceSynchronize();
       ncclCommDestroy(comm);
@@ -649,7 +782,7 @@ struct LossStep {
     for (void* p : {(void*)u1, (void*)u2, (void*)tau1, (void*)tau2, (void*)m1, (void*)v1, (void*)m2, (void*)v2,
                     (void*)s1, (void*)s2, (void*)tau_state, (void*)e1g, (void*)e2g, (void*)diag, (void*)rowstat,
                     (void*)partial, (void*)col_partial, (void*)clamps, (void*)bounds, (void*)f64, (void*)red, (void*)par, (void*)rcoef,
-                    (void*)q, (void*)err})
+                    (void*)q, (void*)err, (void*)pflags, (void*)ptickets})
       if (p) cudaFree(p);
     if (recv && recv != send) cudaFree(recv);
     if (send) cudaFree(send);
