@@ -358,7 +358,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   if (warp == 0) tmem_dealloc<2>(tmem_base, 512);
   // every CTA is past its producer's griddep_wait here, so pass 2 (the last reader of the
   // bounds) has completed
-  if (blockIdx.x == 0 && threadIdx.x < 4 && p.reset_at_exit) p.reset_at_exit[threadIdx.x] = 0.f;
+  if (blockIdx.x == 0 && static_cast<int>(threadIdx.x) < 4 * p.n_reset && p.reset_at_exit) p.reset_at_exit[threadIdx.x] = 0.f;
 }
 
 namespace {

@@ -67,7 +67,8 @@ struct SimParams {
   int n_rb[2];
   int n_items;
   unsigned long long* clamps;  // STATS: exponent clamps (safe_exp, losses.cpp:22-28)
-  const float* bounds;         // {max |E1_i|^2, max |E2_j|^2, max kappa over G}: clamp-free fast paths
+  const float* bounds;         // [n_bounds][4] {max |E1_i|^2, max |E2_j|^2, max kappa}: one slot per rank,
+  int n_bounds;                // the maxima over G are the max over the slots (clamp-free fast paths)
   int q_factor;                // Q: one shared temperature -> factorized single-exponential fast path
   // STATS pass prologue (idle epilogue warps): zero the step's gradient outputs, which the
   // gradient GEMM later accumulates into with TMA reduce-add
@@ -107,7 +108,8 @@ struct GemmParams {
   float scale;       // 1 / (Bl (B-1)), engine.cpp:84-85
   int debug;         // perf experiments: 1 = skip epilogue stores; 9 = counters / timelines into dbg_out
   long long* dbg_out;   // debug == 9: [cta][8] MMA / epilogue counters, globaltimer stamps
-  float* reset_at_exit; // 4 floats zeroed when the GEMM (the step's last kernel) retires: the
+  float* reset_at_exit; // 4 * n_reset floats zeroed when the GEMM (the step's last kernel) retires: the
+  int n_reset;
                         // next step's norm / kappa bounds start from 0 without a memset node
 };
 
@@ -115,10 +117,11 @@ struct GemmParams {
 // statistics (segment C = S^T), so pass 1 multiplies S once instead of twice.
 // ---- NVLink peer all-gather (K > 1): this rank's slices into every rank's buffer + flags ----
 constexpr int kMaxPeers = 8;
+constexpr int kMaxGatherSrc = 10;
 struct PeerGather {
-  const uint8_t* src[2];              // this rank's slices (bytes each)
-  uint8_t* dst[2][kMaxPeers];         // every rank's gather destination (peer-mapped), slice at rank*bytes
-  size_t bytes;                       // bytes per slice (multiple of 16)
+  const uint8_t* src[kMaxGatherSrc];            // this rank's slices
+  uint8_t* dst[kMaxGatherSrc][kMaxPeers];       // every rank's destination (peer-mapped), slice at rank*bytes[t]
+  size_t bytes[kMaxGatherSrc];                  // bytes per slice (multiples of 16)
   int n_src;
   int world, rank;
   unsigned long long seq;             // per-step sequence number (updated in the replayed graph)

@@ -240,11 +240,11 @@ struct LossStep {
     if (K == 1)   // [ceil(B/32)][n_slots][32]: 256-byte warp stores, 32-byte reads per 4 anchors
       col_partial = dalloc<float2>(static_cast<size_t>((Bl + fc::kPairM - 1) / fc::kPairM) * 8 * ((B + 31) / 32 * 32));
     clamps = dalloc<unsigned long long>(1);
-    bounds = dalloc<float>(4);
-    FC_CUDA(cudaMemset(bounds, 0, 4 * sizeof(float)));
+    bounds = dalloc<float>(4 * fc::kMaxPeers);   // one {norm1, norm2, kappa, -} slot per rank
+    FC_CUDA(cudaMemset(bounds, 0, 4 * fc::kMaxPeers * sizeof(float)));
     f64 = dalloc<double>(static_cast<size_t>(Bl) * 18);
     nblk = (Bl * fc::kAnchorLanes + kAnchorBlock - 1) / kAnchorBlock;
-    pstride = 7 * Bl + 3 * nblk;
+    pstride = (7 * Bl + 3 * nblk + 1) & ~1;   // even: 16-byte slices for the peer gather
     send = dalloc<double>(static_cast<size_t>(pstride));
     recv = K > 1 ? dalloc<double>(static_cast<size_t>(K) * pstride) : send;
     red = dalloc<double>(2);
@@ -319,7 +319,7 @@ struct LossStep {
     a.rowstat_R = rowstat; a.rowstat_C = rowstat + Bl;
     a.partial_R = partial; a.partial_C = partial + static_cast<size_t>(Bl) * n_jt * 4;
     a.clamps = clamps;
-    a.bounds = bounds;
+    a.bounds = bounds + 4 * rank;
     a.t_loc1 = F(0); a.t_loc2 = F(1);
     a.sum1 = F(2); a.dx1 = F(3); a.sum2 = F(4); a.dx2 = F(5);
     a.g1 = F(6); a.g2 = F(7); a.u1 = F(8); a.u2 = F(9);
@@ -343,7 +343,7 @@ struct LossStep {
   void setup_peers() {
     if (const char* e = std::getenv("FC_PEER"))
       if (atoi(e) == 0) return;
-    if (K > fc::kMaxPeers) return;
+    if (K > fc::kMaxPeers || Bl % 4 != 0) return;   // 16-byte parameter slices
     // the ranks' device ordinals (one node), then every pair must be able to map the other
     cudaStream_t s0;
     FC_CUDA(cudaStreamCreateWithFlags(&s0, cudaStreamNonBlocking));
@@ -375,34 +375,46 @@ struct LossStep {
     FC_CUDA(cudaMemset(pflags, 0, 2 * fc::kMaxPeers * sizeof(unsigned long long)));
     ptickets = dalloc<unsigned>(2);
     FC_CUDA(cudaMemset(ptickets, 0, 2 * sizeof(unsigned)));
-    void* mine[4] = {e1g, e2g, recv, pflags};
-    cudaIpcMemHandle_t h[4];
-    for (int i = 0; i < 4; ++i) FC_CUDA(cudaIpcGetMemHandle(&h[i], mine[i]));
+    void* mine[6] = {e1g, e2g, recv, pflags, par, bounds};
+    cudaIpcMemHandle_t h[6];
+    for (int i = 0; i < 6; ++i) FC_CUDA(cudaIpcGetMemHandle(&h[i], mine[i]));
     uint8_t* dh = dalloc<uint8_t>(sizeof(h) * (K + 1));
     FC_CUDA(cudaMemcpy(dh + sizeof(h) * K, h, sizeof(h), cudaMemcpyHostToDevice));
     FC_NCCL(ncclAllGather(dh + sizeof(h) * K, dh, sizeof(h), ncclUint8, comm, s0));
     FC_CUDA(cudaStreamSynchronize(s0));
     cudaStreamDestroy(s0);
-    std::vector<cudaIpcMemHandle_t> all(4 * static_cast<size_t>(K));
+    std::vector<cudaIpcMemHandle_t> all(6 * static_cast<size_t>(K));
     FC_CUDA(cudaMemcpy(all.data(), dh, sizeof(h) * K, cudaMemcpyDeviceToHost));
     cudaFree(dh);
-    void* peer[4][fc::kMaxPeers] = {};
+    void* peer[6][fc::kMaxPeers] = {};
     for (int k = 0; k < K; ++k)
-      for (int i = 0; i < 4; ++i) {
+      for (int i = 0; i < 6; ++i) {
         if (k == rank) {
           peer[i][k] = mine[i];
         } else {
-          FC_CUDA(cudaIpcOpenMemHandle(&peer[i][k], all[4 * k + i], cudaIpcMemLazyEnablePeerAccess));
+          FC_CUDA(cudaIpcOpenMemHandle(&peer[i][k], all[6 * k + i], cudaIpcMemLazyEnablePeerAccess));
           peer_maps.push_back(peer[i][k]);
         }
       }
+    // E gather: the two embedding slices. Payload gather: [u|t|id|gt|partials] plus this
+    // rank's slice of the 8 pass-2 parameter arrays (kappa, beta, coef, fac x 2 tracks), so the
+    // pass-2 parameters of every anchor arrive ready-made (no weights kernel on the step path)
+    const size_t np = static_cast<size_t>(n_jt) * fc::kPairN;
     pg_e = fc::PeerGather{};
-    pg_e.bytes = static_cast<size_t>(Bl) * d * 2;
-    pg_e.n_src = 2;
+    pg_e.bytes[0] = pg_e.bytes[1] = static_cast<size_t>(Bl) * d * 2;
+    pg_e.bytes[2] = 16;   // this rank's bounds slot (norm maxima written by prep)
+    pg_e.src[2] = reinterpret_cast<const uint8_t*>(bounds + 4 * rank);
+    pg_e.n_src = 3;
     pg_p = fc::PeerGather{};
-    pg_p.bytes = static_cast<size_t>(pstride) * 8;
-    pg_p.n_src = 1;
+    pg_p.bytes[0] = static_cast<size_t>(pstride) * 8;
     pg_p.src[0] = reinterpret_cast<const uint8_t*>(send);
+    pg_p.n_src = 1 + 8 + 1;
+    for (int j = 0; j < 8; ++j) {
+      pg_p.bytes[1 + j] = static_cast<size_t>(Bl) * 4;
+      pg_p.src[1 + j] = reinterpret_cast<const uint8_t*>(par + j * np + static_cast<size_t>(rank) * Bl);
+    }
+    pg_p.bytes[9] = 16;   // bounds slot again, now with the kappa maximum of the anchor kernel
+    pg_p.src[9] = reinterpret_cast<const uint8_t*>(bounds + 4 * rank);
     for (fc::PeerGather* g : {&pg_e, &pg_p}) {
       g->world = K;
       g->rank = rank;
@@ -412,6 +424,10 @@ struct LossStep {
       pg_e.dst[0][k] = static_cast<uint8_t*>(peer[0][k]);
       pg_e.dst[1][k] = static_cast<uint8_t*>(peer[1][k]);
       pg_p.dst[0][k] = static_cast<uint8_t*>(peer[2][k]);
+      for (int j = 0; j < 8; ++j)
+        pg_p.dst[1 + j][k] = static_cast<uint8_t*>(peer[4][k]) + j * np * 4;
+      pg_e.dst[2][k] = static_cast<uint8_t*>(peer[5][k]);   // norm maxima slot
+      pg_p.dst[9][k] = static_cast<uint8_t*>(peer[5][k]);
       pg_e.peer_flag[k] = static_cast<unsigned long long*>(peer[3][k]);
       pg_p.peer_flag[k] = static_cast<unsigned long long*>(peer[3][k]) + fc::kMaxPeers;
     }
@@ -569,6 +585,37 @@ struct LossStep {
     const __nv_bfloat16* E1 = static_cast<const __nv_bfloat16*>(in->e1);
     const __nv_bfloat16* E2 = static_cast<const __nv_bfloat16*>(in->e2);
     mark(0, st);
+    fc::StepArgs a = args;
+    a.ids = in->ids;
+    a.gscale = static_cast<float>(1.0 / (static_cast<double>(Bl) * static_cast<double>(B - 1)));
+    a.scal = scal;
+    if (sim_debug == 9) a.dbg = dbg_buf + 2 * 2688 + 160 * 16;
+    // side branch: zero dE (the GEMM's reduce-add target). ws2 has the lowest stream priority,
+    // so the block scheduler dispatches prep / pass 1 first and the zeroing fills in behind
+    // them (no event between the programmatically linked kernels of the main stream)
+    FC_CUDA(cudaEventRecord(zero_fork, st));
+    FC_CUDA(cudaStreamWaitEvent(ws2, zero_fork, 0));
+    fc::fc_zero_kernel<<<n_sm, 256, 0, ws2>>>(reinterpret_cast<float4*>(out->de1), reinterpret_cast<float4*>(out->de2),
+                                              static_cast<long long>(Bl) * d / 4);
+    FC_CUDA(cudaGetLastError());
+    FC_CUDA(cudaEventRecord(zero_join, ws2));
+    // prep: with peer memory every rank preps only its own anchors, BEFORE the gather (the
+    // diagonal and tau^t of non-local anchors are never needed: their pass-2 parameters arrive
+    // ready-made); its norm maxima sit in this rank's bounds slot, which the gather copies
+    // into every rank (consumers take the max over the slots). Otherwise prep covers G after
+    // the gather.
+    const bool local_prep = K > 1 && use_peer;
+    auto launch_prep = [&](const __nv_bfloat16* p1, const __nv_bfloat16* p2, int row0_, int rows) {
+      a.prep_row0 = row0_;
+      a.prep_rows = rows;
+      // bounds were zeroed by the previous step's GEMM (and at creation)
+      fc::fc_prep_kernel<<<(rows * 32 + 127) / 128, 128, 0, st>>>(p1, p2, a, in->gamma, in->eps);   // one wave
+      FC_CUDA(cudaGetLastError());
+      last_prep_e1 = p1;
+      last_prep_e2 = p2;
+      last_prep_args = a;
+    };
+    if (local_prep) launch_prep(E1, E2, rank * Bl, Bl);
     if (K > 1) {
       if (use_peer) {   // NVLink stores into every rank's e1g / e2g, flag handshake
         fc::PeerGather g = pg_e;
@@ -586,28 +633,8 @@ struct LossStep {
       E2 = e2g;
     }
     ensure_maps(E1, E2);
-    fc::StepArgs a = args;
-    a.ids = in->ids;
-    a.gscale = static_cast<float>(1.0 / (static_cast<double>(Bl) * static_cast<double>(B - 1)));
-    a.scal = scal;
-
     mark(1, st);
-    // side branch: zero dE (the GEMM's reduce-add target). ws2 has the lowest stream priority,
-    // so the block scheduler dispatches prep / pass 1 first and the zeroing fills in behind
-    // them (no event between the programmatically linked kernels of the main stream)
-    FC_CUDA(cudaEventRecord(zero_fork, st));
-    FC_CUDA(cudaStreamWaitEvent(ws2, zero_fork, 0));
-    fc::fc_zero_kernel<<<n_sm, 256, 0, ws2>>>(reinterpret_cast<float4*>(out->de1), reinterpret_cast<float4*>(out->de2),
-                                              static_cast<long long>(Bl) * d / 4);
-    FC_CUDA(cudaGetLastError());
-    FC_CUDA(cudaEventRecord(zero_join, ws2));
-    if (sim_debug == 9) a.dbg = dbg_buf + 2 * 2688 + 160 * 16;
-    // bounds were zeroed by the previous step's GEMM (and at creation)
-    fc::fc_prep_kernel<<<(B * 32 + 127) / 128, 128, 0, st>>>(E1, E2, a, in->gamma, in->eps);   // one wave
-    last_prep_e1 = E1;
-    last_prep_e2 = E2;
-    last_prep_args = a;
-    FC_CUDA(cudaGetLastError());
+    if (!local_prep) launch_prep(E1, E2, 0, B);
 
     // ---- pass 1: row statistics of S[L,G] (segment R) and S^T[L,G] (segment C) ----
     fc::SimParams sp{};
@@ -627,6 +654,7 @@ struct LossStep {
     sp.n_items = (sp.n_rb[0] + sp.n_rb[1]) * n_jt;
     sp.clamps = clamps;
     sp.bounds = bounds;
+    sp.n_bounds = K;
     sp.debug = sim_debug;
     sp.zero_a = sp.zero_b = nullptr;
     if (sim_debug == 9) sp.dbg_out = dbg_buf;
@@ -672,20 +700,27 @@ struct LossStep {
       // ONE all-gather carries u/tau/id, the v2 per-index tau gradients and the G_tau / loss
       // block partials of every rank (no scalar all-reduce, no second gather)
       if (use_peer) {
+        // payload + this rank's pass-2 parameters into every rank (the u replica update of the
+        // other ranks' ids follows on the side branch)
         fc::PeerGather g = pg_p;
         g.seq = seq;
-        FC_CUDA(fc::launch_peer_gather(g, 32, st));
+        FC_CUDA(fc::launch_peer_gather(g, 64, st));
       } else {
         FC_NCCL(ncclAllGather(send, recv, static_cast<size_t>(pstride), ncclFloat64, comm, st));
+        a.weights_replica_only = 0;
+        fc::fc_weights_kernel<<<(B + kWeightsBlock - 1) / kWeightsBlock, kWeightsBlock, 0, st>>>(a);
+        FC_CUDA(cudaGetLastError());
       }
-      fc::fc_weights_kernel<<<(B + kWeightsBlock - 1) / kWeightsBlock, kWeightsBlock, 0, st>>>(a);
-      FC_CUDA(cudaGetLastError());
     }
     // the G_tau reduction, temperature step and IndividualTemp update only feed the next step
     // and the step scalars: they run on the side branch
     FC_CUDA(cudaEventRecord(side_fork, st));
     FC_CUDA(cudaStreamWaitEvent(ws2, side_fork, 0));
     fc::fc_reduce_kernel<<<1, 32, 0, ws2>>>(a);
+    if (K > 1 && use_peer) {
+      a.weights_replica_only = 1;
+      fc::fc_weights_kernel<<<(B + kWeightsBlock - 1) / kWeightsBlock, kWeightsBlock, 0, ws2>>>(a);
+    }
     if (indiv) fc::fc_indiv_update_kernel<<<(B + 255) / 256, 256, 0, ws2>>>(a);
     FC_CUDA(cudaGetLastError());
     FC_CUDA(cudaEventRecord(side_join, ws2));
@@ -728,6 +763,7 @@ struct LossStep {
     gp.scale = static_cast<float>(1.0 / (static_cast<double>(Bl) * static_cast<double>(B - 1)));
     gp.debug = gemm_debug;
     gp.reset_at_exit = bounds;
+    gp.n_reset = K;
     if (gemm_debug >= 9) gp.dbg_out = dbg_buf + 2 * 2688;
     for (int s = 0; s < 2; ++s) {
       fc::GemmSeg& g = gp.seg[s];
@@ -1083,6 +1119,7 @@ int fc_debug_similarity(const void* a, const void* b, int32_t rows, int32_t cols
       FC_CUDA(cudaMemcpy(dbg_bounds, big, sizeof(big), cudaMemcpyHostToDevice));
     }
     sp.bounds = dbg_bounds;
+    sp.n_bounds = 1;
     int dev = 0;
     cudaGetDevice(&dev);
     FC_CUDA(fc::sim_set_smem());

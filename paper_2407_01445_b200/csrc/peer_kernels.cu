@@ -33,15 +33,15 @@ __device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long
 
 __global__ void __launch_bounds__(256) peer_gather_kernel(PeerGather g) {
   // ---- this rank's slices -> every rank's destination (row offset rank * bytes) ----
-  const size_t n16 = g.bytes / 16;
   const size_t stride = static_cast<size_t>(gridDim.x) * blockDim.x;
   for (int t = 0; t < g.n_src; ++t) {
+    const size_t n16 = g.bytes[t] / 16;
     const uint4* src = reinterpret_cast<const uint4*>(g.src[t]);
     for (size_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n16; i += stride) {
       const uint4 v = src[i];
 #pragma unroll 1
       for (int k = 0; k < g.world; ++k)
-        reinterpret_cast<uint4*>(g.dst[t][k] + static_cast<size_t>(g.rank) * g.bytes)[i] = v;
+        reinterpret_cast<uint4*>(g.dst[t][k] + static_cast<size_t>(g.rank) * g.bytes[t])[i] = v;
     }
   }
   // ---- grid completion: the last CTA publishes and waits ----

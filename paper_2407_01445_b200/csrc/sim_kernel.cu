@@ -549,7 +549,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(SimCfg<kMode>::kThre
       }
 
       // every global load of the tile is issued before the accumulator wait (latency hidden)
-      const float bnd0 = p.bounds[0], bnd1 = p.bounds[1];
+      float bnd0 = 0.f, bnd1 = 0.f, bnd2 = 0.f;
+      for (int k = 0; k < p.n_bounds; ++k) {
+        bnd0 = fmaxf(bnd0, p.bounds[4 * k]);
+        bnd1 = fmaxf(bnd1, p.bounds[4 * k + 1]);
+        bnd2 = fmaxf(bnd2, p.bounds[4 * k + 2]);
+      }
       float2 cst_all[kMode == kSimFused ? kChunksW : 1];
       if constexpr (kMode == kSimFused) {
 #pragma unroll
@@ -576,7 +581,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(SimCfg<kMode>::kThre
         ps = it % kSimPSlots;
         mbar_wait(&L.pfull[ps], (it / kSimPSlots) & 1);
         par = L.par + ps * (kSimPSlotBytes / 4) + cq * kColsW;
-        q_col_safe = 2.f * smax * p.bounds[2] <= kClampLog2;
+        q_col_safe = 2.f * smax * bnd2 <= kClampLog2;
         // factorized form: 2^(s kappa) stays within [2^-63, 2^63] and fac within fp32 range
         q_fact = p.q_factor && __all_sync(0xffffffffu, rk * smax <= kFactMaxLog2);
       }

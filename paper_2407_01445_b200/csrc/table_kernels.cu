@@ -48,11 +48,14 @@ __global__ void fc_prep_kernel(const __nv_bfloat16* __restrict__ e1, const __nv_
     sc[0] = gamma;
     sc[1] = eps;
   }
-  const bool valid = w < a.B;
-  const int r = w - a.row0;
+  // warp w covers row w of [prep_row0, prep_row0 + prep_rows) (e1 / e2 point at that range)
+  const bool valid = w < a.prep_rows;
+  const int wl = valid ? w : 0;
+  const int wg = a.prep_row0 + w;   // global anchor index
+  const int r = wg - a.row0;
   const bool lead = valid && lane == 0 && r >= 0 && r < a.Bl;   // this rank's anchor, lane 0
-  const uint4* x4 = reinterpret_cast<const uint4*>(e1 + static_cast<size_t>(valid ? w : 0) * a.d);
-  const uint4* y4 = reinterpret_cast<const uint4*>(e2 + static_cast<size_t>(valid ? w : 0) * a.d);
+  const uint4* x4 = reinterpret_cast<const uint4*>(e1 + static_cast<size_t>(wl) * a.d);
+  const uint4* y4 = reinterpret_cast<const uint4*>(e2 + static_cast<size_t>(wl) * a.d);
   const int nv = valid ? a.d / 8 : 0;
   // the row loads (two per lane at d = 512) and the id load are all issued before any use
   constexpr int kPre = 2;
@@ -103,10 +106,10 @@ __global__ void fc_prep_kernel(const __nv_bfloat16* __restrict__ e1, const __nv_
   if (threadIdx.x < 2) {
     float m = 0.f;
     for (int k = 0; k < static_cast<int>(blockDim.x >> 5); ++k) m = fmaxf(m, bmax[threadIdx.x][k]);
-    atomicMax(reinterpret_cast<int*>(a.bounds) + threadIdx.x, __float_as_int(m));
+    atomicMax(reinterpret_cast<int*>(a.bounds) + threadIdx.x, __float_as_int(m));   // this rank's slot
   }
   if (lane != 0 || !valid) return;
-  a.diag[w] = acc;
+  a.diag[wg] = acc;
   if (!lead) return;
   if (a.track_u) {
     a.uold1[r] = uo1;
@@ -319,11 +322,14 @@ __global__ void fc_weights_kernel(StepArgs a) {
       a.u1_tab[id] = u1;
       a.u2_tab[id] = u2;
     }
-    const float s_ii = a.diag[i];
-    const AnchorParams p = anchor_params(a, u1, u2, t1, t2, a.tau_state->tau, eps);
-    store_params(a, i, p, s_ii);
-    kmax = fmaxf(p.k1, p.k2);
+    if (!a.weights_replica_only) {
+      const float s_ii = a.diag[i];
+      const AnchorParams p = anchor_params(a, u1, u2, t1, t2, a.tau_state->tau, eps);
+      store_params(a, i, p, s_ii);
+      kmax = fmaxf(p.k1, p.k2);
+    }
   }
+  if (a.weights_replica_only) return;   // grid-uniform: parameters and kappa max arrived already
   __shared__ float shk[32];
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) kmax = fmaxf(kmax, __shfl_xor_sync(0xffffffffu, kmax, o));
@@ -445,7 +451,7 @@ __device__ void block_partials(const StepArgs& a, double ta, double tb, double t
     double b0 = 0.0, b1 = 0.0, b2 = 0.0;
     float km = 0.f;
     for (int w = 0; w < nw; ++w) { b0 += sh[0][w]; b1 += sh[1][w]; b2 += sh[2][w]; km = fmaxf(km, shk[w]); }
-    atomicMax(reinterpret_cast<int*>(a.bounds) + 2, __float_as_int(km));   // max kappa (pass-2 fast path)
+    atomicMax(reinterpret_cast<int*>(a.bounds) + 2, __float_as_int(km));   // max kappa, this rank's slot
     double* bp = a.blockpart + 3 * blockIdx.x;
     bp[0] = b0; bp[1] = b1; bp[2] = b2;
   }

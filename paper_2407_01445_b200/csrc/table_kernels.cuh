@@ -51,7 +51,7 @@ struct StepArgs {
   const float2* col_partial;             // fused pass 1 (K = 1): segment-C stats [B/32][col_slots][32]
   int col_slots;                         // 0: segment-C stats are row partials in partial_C
   unsigned long long* clamps;
-  float* bounds;                         // {max |E1|^2, max |E2|^2, max kappa} (atomicMax on float bits)
+  float* bounds;                         // this rank's slot {max |E1|^2, max |E2|^2, max kappa} (atomicMax on float bits)
   // per-local-anchor fp64 state of the step
   double* t_loc1; double* t_loc2;
   double* sum1; double* dx1; double* sum2; double* dx2;
@@ -79,6 +79,8 @@ struct StepArgs {
   StepResult* result;
   float gscale;                          // c = 1 / (Bl (B-1)), engine.cpp:84-85
   long long* dbg;                        // FC_SIM_DEBUG=9: per-block globaltimer stamps of fc_anchor_kernel
+  int prep_row0, prep_rows;              // rows of the prep kernel (all of G, or this rank's L before the gather)
+  int weights_replica_only;              // fc_weights_kernel: only the u replica update (parameters arrived)
 };
 
 __global__ void fc_prep_kernel(const __nv_bfloat16* __restrict__ e1, const __nv_bfloat16* __restrict__ e2,

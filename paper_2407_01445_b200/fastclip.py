@@ -75,7 +75,8 @@ def lib():
     """Loads (building if needed) the in-tree sm_100a library; raises if unavailable."""
     global _lib
     if _lib is None:
-        path = _build.build()
+        # FC_LIB_PATH: load another build of the same ABI (A/B diagnostics only)
+        path = os.environ.get("FC_LIB_PATH") or _build.build()
         if not os.path.exists(path):
             raise FastclipError(11, f"CUDA library missing: {path}")
         L = C.CDLL(path)
