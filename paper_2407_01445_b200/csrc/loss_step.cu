@@ -797,8 +797,10 @@ struct LossStep {
   }
 
   int kernels_per_step() const {
-    return 1 /*prep*/ + 1 /*pass1*/ + 1 /*anchor*/ + (K > 1 ? 1 : 0) /*weights*/ + 1 /*reduce*/ + (indiv ? 1 : 0) +
-           1 /*zero dE*/ + 1 /*pass2*/ + 1 /*gemm*/;
+    int n = 1 /*prep*/ + 1 /*pass1*/ + 1 /*reduce*/ + (indiv ? 1 : 0) + 1 /*zero dE*/ + 1 /*pass2*/ + 1 /*gemm*/;
+    n += 1;   // fc_anchor_kernel
+    if (K > 1) n += use_peer ? 3 /*two peer gathers + u replica*/ : 1 /*weights*/;
+    return n;
   }
 
   void destroy() {

@@ -335,6 +335,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(SimCfg<kMode>::kThre
     for (int i = 0; i < kSimPSlots; ++i) {
       mbar_init(&L.pfull[i], 1);                    // local producer + bulk-copy bytes
       mbar_init(&L.pempty[i], kEpi);                // local epilogue warps
+
     }
     fence_barrier_init();
   }
@@ -362,6 +363,26 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(SimCfg<kMode>::kThre
       uint32_t spar = 0;   // bit per A slot: parity of its load generation (afull/aempty phase), kept in a register
       int cur_key = -1;
       int it = 0;
+      // column parameters of the pair's j-th tile (each CTA keeps its own copy), written by the
+      // preceding per-anchor kernel: the first load waits for that grid (programmatic launch;
+      // the A / B operand loads do not depend on it)
+      auto load_params = [&](int j) {
+        int s, rb, jt;
+        decode_item(p, it_lo + j, s, rb, jt);
+        if (j == 0) griddep_wait();
+        const int ps = j % kSimPSlots;
+        mbar_wait(&L.pempty[ps], ((j / kSimPSlots) & 1) ^ 1);
+        if (issuer) {
+          mbar_arrive_expect_tx(&L.pfull[ps], kSimPSlotBytes);
+          float* dst = L.par + ps * (kSimPSlotBytes / 4);
+          const SimSeg& sg = p.seg[s];
+          bulk_load(dst, sg.col_kappa + jt * kPairN, kPairN * 4, &L.pfull[ps]);
+          bulk_load(dst + kPairN, sg.col_beta + jt * kPairN, kPairN * 4, &L.pfull[ps]);
+          bulk_load(dst + 2 * kPairN, sg.col_coef + jt * kPairN, kPairN * 4, &L.pfull[ps]);
+          bulk_load(dst + 3 * kPairN, sg.col_fac + jt * kPairN, kPairN * 4, &L.pfull[ps]);
+        }
+        __syncwarp();
+      };
       for (int item = it_lo; item < it_hi; ++item, ++it) {
         int s, rb, jt;
         decode_item(p, item, s, rb, jt);
@@ -369,24 +390,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(SimCfg<kMode>::kThre
         const CUtensorMap* mb = s ? &mapB1 : &mapB0;
         const int a_row = p.seg[s].a_row0 + rb * kPairM + static_cast<int>(rank) * kCtaM;
         const int b_row = jt * kPairN + static_cast<int>(rank) * (kPairN / 2);
-        if constexpr (kMode == kSimQ) {
-          // this tile's column parameters (each CTA keeps its own copy), written by the
-          // preceding per-anchor kernel: wait for it before the first parameter load (the A / B
-          // operand loads above do not depend on it)
-          if (it == 0) griddep_wait();
-          const int ps = it % kSimPSlots;
-          mbar_wait(&L.pempty[ps], ((it / kSimPSlots) & 1) ^ 1);
-          if (issuer) {
-            mbar_arrive_expect_tx(&L.pfull[ps], kSimPSlotBytes);
-            float* dst = L.par + ps * (kSimPSlotBytes / 4);
-            const SimSeg& sg = p.seg[s];
-            bulk_load(dst, sg.col_kappa + jt * kPairN, kPairN * 4, &L.pfull[ps]);
-            bulk_load(dst + kPairN, sg.col_beta + jt * kPairN, kPairN * 4, &L.pfull[ps]);
-            bulk_load(dst + 2 * kPairN, sg.col_coef + jt * kPairN, kPairN * 4, &L.pfull[ps]);
-            bulk_load(dst + 3 * kPairN, sg.col_fac + jt * kPairN, kPairN * 4, &L.pfull[ps]);
-          }
-          __syncwarp();
-        }
+        if constexpr (kMode == kSimQ) load_params(it);   // ahead of the tile's operands
         for (int c = 0; c < n_chunks; ++c) {
           const int kb_lo = c * kSimASlots;
           const int kb_hi = min(nkb, kb_lo + kSimASlots);
