@@ -70,6 +70,7 @@ struct SimParams {
   const float* bounds;         // [n_bounds][4] {max |E1_i|^2, max |E2_j|^2, max kappa}: one slot per rank,
   int n_bounds;                // the maxima over G are the max over the slots (clamp-free fast paths)
   int q_factor;                // Q: one shared temperature -> factorized single-exponential fast path
+  int split_tail;              // leftover tiles (T mod pairs) run as 256 x 128 halves on twice the pairs
   // STATS pass prologue (idle epilogue warps): zero the step's gradient outputs, which the
   // gradient GEMM later accumulates into with TMA reduce-add
   float4* zero_a; float4* zero_b;          // nullptr: nothing to zero

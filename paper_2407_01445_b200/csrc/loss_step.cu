@@ -139,6 +139,7 @@ struct LossStep {
   bool gemm_mc = false;          // FC_GEMM_MC=1: clusters of two pairs multicast the GEMM B operand
   bool fused_p1 = false;         // K == 1: row + column statistics from one S pass (FC_FUSED_P1=0: two passes)
   bool pdl = true;               // programmatic dependent launch between the step's kernels (FC_PDL=0: off)
+  bool split_tail = true;        // similarity kernels: leftover tiles as half tiles (FC_SPLIT_TAIL=0: off)
   int gemm_drain = 0;            // FC_GEMM_DRAIN: stream-K unit-boundary cost in k-blocks (0: KB / 10)
   long long* dbg_buf = nullptr;   // FC_SIM_DEBUG=9 MMA-warp counters: [launch 0: pass 1, 1: pass 2][pair][8]             // FC_SIM_DEBUG perf experiments (results invalid when set)
   struct GraphEntry {
@@ -279,6 +280,7 @@ struct LossStep {
     if (const char* e = std::getenv("FC_GEMM_MC")) gemm_mc = atoi(e) != 0;
     fused_p1 = K == 1;
     if (const char* e = std::getenv("FC_PDL")) pdl = atoi(e) != 0;
+    if (const char* e = std::getenv("FC_SPLIT_TAIL")) split_tail = atoi(e) != 0;
     if (const char* e = std::getenv("FC_GEMM_DRAIN")) gemm_drain = atoi(e);
     if (const char* e = std::getenv("FC_FUSED_P1")) fused_p1 = fused_p1 && atoi(e) != 0;
     if (const char* e = std::getenv("FC_GEMM_DEBUG")) gemm_debug = atoi(e);
@@ -656,6 +658,7 @@ struct LossStep {
     sp.bounds = bounds;
     sp.n_bounds = K;
     sp.debug = sim_debug;
+    sp.split_tail = split_tail ? 1 : 0;
     sp.zero_a = sp.zero_b = nullptr;
     if (sim_debug == 9) sp.dbg_out = dbg_buf;
     CUtensorMap mA[2] = {mE1k, mE2k}, mB[2] = {mE2k, mE1k};

@@ -60,23 +60,54 @@ __device__ __forceinline__ SmemLayout carve(uint8_t* base) {
   return L;
 }
 
-__device__ __forceinline__ void decode_item(const SimParams& p, int item, int& s, int& rb, int& jt) {
+// Work of one pair: q = floor(T / P) whole 256x256 tiles, contiguous (the resident anchor rows
+// A carry over between them), then the R = T mod P leftover tiles split into 2R half tiles
+// (256 x 128, UMMA N = 128) dealt round-robin, so the slowest pair runs q + 1/2 tiles
+// instead of q + 1.
+struct PairItems {
+  int q, tail_lo, n_pairs, pair, count;
+};
+__device__ __forceinline__ PairItems pair_items(int n_tiles, int pair, int n_pairs, bool split) {
+  PairItems pi;
+  pi.n_pairs = n_pairs;
+  pi.pair = pair;
+  if (!split) {   // contiguous ranges of whole tiles
+    pi.q = -1;
+    pi.tail_lo = static_cast<int>((static_cast<long long>(n_tiles) * pair) / n_pairs);
+    pi.count = static_cast<int>((static_cast<long long>(n_tiles) * (pair + 1)) / n_pairs) - pi.tail_lo;
+    return pi;
+  }
+  pi.q = n_tiles / n_pairs;
+  pi.tail_lo = pi.q * n_pairs;   // first leftover tile
+  const int halves = 2 * (n_tiles - pi.tail_lo);
+  pi.count = pi.q + (pair < halves ? (halves - pair + n_pairs - 1) / n_pairs : 0);
+  return pi;
+}
+// item -> (segment, row block, column tile, half: -1 whole tile, 0 / 1 the column half)
+__device__ __forceinline__ void decode_item(const SimParams& p, const PairItems& pi, int item, int& s, int& rb,
+                                            int& jt, int& half) {
+  int t;
+  if (pi.q < 0) {
+    t = pi.tail_lo + item;
+    half = -1;
+  } else if (item < pi.q) {
+    t = pi.pair * pi.q + item;
+    half = -1;
+  } else {
+    const int h = pi.pair + (item - pi.q) * pi.n_pairs;
+    t = pi.tail_lo + h / 2;
+    half = h & 1;
+  }
   const int n0 = p.n_rb[0] * p.n_jt;
-  s = item < n0 ? 0 : 1;
-  const int local = item - (s ? n0 : 0);
+  s = t < n0 ? 0 : 1;
+  const int local = t - (s ? n0 : 0);
   rb = local / p.n_jt;
   jt = local % p.n_jt;
 }
-
-// Contiguous item range of a pair (keeps the resident A block across consecutive items).
-__device__ __forceinline__ void pair_range(int n_items, int pair, int n_pairs, int& lo, int& hi) {
-  lo = static_cast<int>((static_cast<long long>(n_items) * pair) / n_pairs);
-  hi = static_cast<int>((static_cast<long long>(n_items) * (pair + 1)) / n_pairs);
-}
 // Identity of the A block an (item, chunk) needs: segment, row block, 512-wide K chunk.
-__device__ __forceinline__ int a_key(const SimParams& p, int item, int chunk, int n_chunks) {
-  int s, rb, jt;
-  decode_item(p, item, s, rb, jt);
+__device__ __forceinline__ int a_key(const SimParams& p, const PairItems& pi, int item, int chunk, int n_chunks) {
+  int s, rb, jt, half;
+  decode_item(p, pi, item, s, rb, jt, half);
   return ((s * 65536) + rb) * n_chunks + chunk;
 }
 
@@ -347,8 +378,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(SimCfg<kMode>::kThre
   griddep_launch_dependents();   // the next kernel may take SMs as this grid's CTAs retire
 
   const int n_chunks = (nkb + kSimASlots - 1) / kSimASlots;
-  int it_lo, it_hi;
-  pair_range(p.n_items, pair, n_pairs, it_lo, it_hi);
+  const PairItems pi = pair_items(p.n_items, pair, n_pairs, p.split_tail != 0);
+  const int it_lo = 0, it_hi = pi.count;
 
   if (warp == kProdWarp) {
     // ===================== TMA producer (both CTAs) =====================
@@ -367,8 +398,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(SimCfg<kMode>::kThre
       // preceding per-anchor kernel: the first load waits for that grid (programmatic launch;
       // the A / B operand loads do not depend on it)
       auto load_params = [&](int j) {
-        int s, rb, jt;
-        decode_item(p, it_lo + j, s, rb, jt);
+        int s, rb, jt, half;
+        decode_item(p, pi, it_lo + j, s, rb, jt, half);
         if (j == 0) griddep_wait();
         const int ps = j % kSimPSlots;
         mbar_wait(&L.pempty[ps], ((j / kSimPSlots) & 1) ^ 1);
@@ -384,17 +415,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(SimCfg<kMode>::kThre
         __syncwarp();
       };
       for (int item = it_lo; item < it_hi; ++item, ++it) {
-        int s, rb, jt;
-        decode_item(p, item, s, rb, jt);
+        int s, rb, jt, half;
+        decode_item(p, pi, item, s, rb, jt, half);
         const CUtensorMap* ma = s ? &mapA1 : &mapA0;
         const CUtensorMap* mb = s ? &mapB1 : &mapB0;
         const int a_row = p.seg[s].a_row0 + rb * kPairM + static_cast<int>(rank) * kCtaM;
-        const int b_row = jt * kPairN + static_cast<int>(rank) * (kPairN / 2);
+        // each CTA supplies half of the tile's columns: 128 of a whole tile, 64 of a half tile
+        // (the 128-row box then also brings 64 rows the UMMA does not read)
+        const int b_row = half < 0 ? jt * kPairN + static_cast<int>(rank) * (kPairN / 2)
+                                   : jt * kPairN + half * (kPairN / 2) + static_cast<int>(rank) * (kPairN / 4);
         if constexpr (kMode == kSimQ) load_params(it);   // ahead of the tile's operands
         for (int c = 0; c < n_chunks; ++c) {
           const int kb_lo = c * kSimASlots;
           const int kb_hi = min(nkb, kb_lo + kSimASlots);
-          const int key = a_key(p, item, c, n_chunks);
+          const int key = a_key(p, pi, item, c, n_chunks);
           if (key != cur_key) {
             for (int kb = kb_lo; kb < kb_hi; ++kb) {
               const int slot = kb - kb_lo;
@@ -433,7 +467,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(SimCfg<kMode>::kThre
     // warp-wide election per k block): with ~100+ cycles of scalar work per MMA the single
     // issuing thread, not the tensor pipe, would set the pace (128 cycles per 256x256x16).
     if (rank == 0) {
-      constexpr uint32_t idesc = make_idesc_bf16(kPairM, kPairN, 0, 0);
+      constexpr uint32_t idesc_full = make_idesc_bf16(kPairM, kPairN, 0, 0);
+      constexpr uint32_t idesc_half = make_idesc_bf16(kPairM, kPairN / 2, 0, 0);
       const uint64_t a_desc0 = make_sdesc_sw128(smem_u32(L.a), 0, 1024);
       const uint64_t b_desc0 = make_sdesc_sw128(smem_u32(L.b), 0, 1024);
       uint32_t stage = 0, phase = 0;
@@ -451,10 +486,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(SimCfg<kMode>::kThre
         if (prof) c_tempty += clock64() - t0;
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * kPairN;
+        int s_, rb_, jt_, half_;
+        decode_item(p, pi, item, s_, rb_, jt_, half_);
+        const uint32_t idesc = half_ < 0 ? idesc_full : idesc_half;
         for (int c = 0; c < n_chunks; ++c) {
           const int kb_lo = c * kSimASlots;
           const int kb_hi = min(nkb, kb_lo + kSimASlots);
-          const int key = a_key(p, item, c, n_chunks);
+          const int key = a_key(p, pi, item, c, n_chunks);
           if (key != cur_key) {
             cur_key = key;
             ready = 0;
@@ -462,8 +500,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(SimCfg<kMode>::kThre
           }
           // last use of this A generation: release each slot right after its MMAs
           int nxt_key = -2;
-          if (c + 1 < n_chunks) nxt_key = a_key(p, item, c + 1, n_chunks);
-          else if (item + 1 < it_hi) nxt_key = a_key(p, item + 1, 0, n_chunks);
+          if (c + 1 < n_chunks) nxt_key = a_key(p, pi, item, c + 1, n_chunks);
+          else if (item + 1 < it_hi) nxt_key = a_key(p, pi, item + 1, 0, n_chunks);
           const bool last_use = nxt_key != key;
           const bool last_chunk = c == n_chunks - 1;
           for (int kb = kb_lo; kb < kb_hi; ++kb) {
@@ -527,9 +565,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(SimCfg<kMode>::kThre
     const uint32_t cq = warp >> 2;        // column group (kColsW wide) of the 256-wide tile
     int it = 0;
     for (int item = it_lo; item < it_hi; ++item, ++it) {
-      int s, rb, jt;
-      decode_item(p, item, s, rb, jt);
+      int s, rb, jt, half;
+      decode_item(p, pi, item, s, rb, jt, half);
       const SimSeg& sg = p.seg[s];
+      // a half tile holds its 128 columns in TMEM columns 0..127; the warps past them idle
+      const int tile_off = half < 0 ? 0 : half * (kPairN / 2);   // first column inside the 256-wide tile
+      const bool active = static_cast<int>(cq) * kColsW < (half < 0 ? kPairN : kPairN / 2);
       const uint32_t acc = it & 1;
       const uint32_t acc_phase = (it >> 1) & 1;
       const int warp_row0 = rb * kPairM + static_cast<int>(rank) * kCtaM + static_cast<int>(q4) * 32;
@@ -538,7 +579,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(SimCfg<kMode>::kThre
       const bool warp_rows_ok = warp_row0 + 32 <= sg.rows;
       const int g0 = sg.a_row0 + warp_row0;     // global index of lane 0's anchor
       const int gi = g0 + static_cast<int>(lane);
-      const int colq = jt * kPairN + static_cast<int>(cq) * kColsW;
+      const int colq = jt * kPairN + tile_off + static_cast<int>(cq) * kColsW;
 
       float2 rstat = make_float2(0.f, 0.f);
       float rk = 0.f, rbeta = 0.f, rc = 0.f, rf = 0.f;
@@ -584,7 +625,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(SimCfg<kMode>::kThre
       if constexpr (kMode == kSimQ) {
         ps = it % kSimPSlots;
         mbar_wait(&L.pfull[ps], (it / kSimPSlots) & 1);
-        par = L.par + ps * (kSimPSlotBytes / 4) + cq * kColsW;
+        par = L.par + ps * (kSimPSlotBytes / 4) + tile_off + cq * kColsW;
         q_col_safe = 2.f * smax * bnd2 <= kClampLog2;
         // factorized form: 2^(s kappa) stays within [2^-63, 2^63] and fac within fp32 range
         q_fact = p.q_factor && __all_sync(0xffffffffu, rk * smax <= kFactMaxLog2);
@@ -594,8 +635,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(SimCfg<kMode>::kThre
       const bool row_safe = !__any_sync(0xffffffffu, row_ok && fmaf(smax, row_kap, row_beta) > kClampLog2);
       // FUSED one-exponential form: 2^(s kappa) and 2^beta stay inside [2^-63, 2^63]
       const bool fused_ok = kMode == kSimFused && __all_sync(0xffffffffu, row_kap * smax <= kFactMaxLog2);
+      if (!active) {   // half tile, columns beyond it: hand the buffer back at once
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) {
+          if (rank == 0) mbar_arrive(&L.tempty[acc]);
+          else mbar_arrive_cluster(&L.tempty[acc], 0);
+        }
+      }
 #pragma unroll 1
-      for (int h = 0; h < kChunksW; ++h) {
+      for (int h = 0; h < (active ? kChunksW : 0); ++h) {
         uint32_t rr[kMode == kSimFused ? 1 : 32];
         if constexpr (kMode != kSimFused) {
           tmem_ld_32x32b_x32(taddr + 32 * h, rr);
@@ -667,7 +716,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(SimCfg<kMode>::kThre
             const float sc = ex2_approx(rstat.y);
             const float rx = se2.x + se2.y, rzx = sye2.x + sye2.y;
             const float sxe = sc * fmaf(rstat.y, rx, rzx) + sye;
-            const int quarter = (static_cast<int>(cq) * kColsW + 32 * h) / 64;
+            const int quarter = (tile_off + static_cast<int>(cq) * kColsW + 32 * h) / 64;
             if (row_ok)
               sg.partial[static_cast<size_t>(r_loc) * (p.n_jt * 4) + jt * 4 + quarter] = make_float2(se + sc * rx, sxe);
             se2 = f2(0.f, 0.f); sye2 = f2(0.f, 0.f); se = 0.f; sye = 0.f;
@@ -711,7 +760,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(SimCfg<kMode>::kThre
       if constexpr (kMode == kSimStats) {
         const float sxe = sye2.x + sye2.y + sye;   // sum y e; the table kernel divides by kappa
         se += se2.x + se2.y;
-        if (row_ok) sg.partial[static_cast<size_t>(r_loc) * (p.n_jt * 4) + jt * 4 + cq] = make_float2(se, sxe);
+        if (row_ok && active)
+          sg.partial[static_cast<size_t>(r_loc) * (p.n_jt * 4) + jt * 4 + tile_off / 64 + cq] = make_float2(se, sxe);
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) ncl += __shfl_xor_sync(0xffffffffu, ncl, o);
         if (lane == 0 && ncl) atomicAdd(p.clamps, static_cast<unsigned long long>(ncl));
