@@ -139,7 +139,7 @@ struct LossStep {
   bool gemm_mc = false;          // FC_GEMM_MC=1: clusters of two pairs multicast the GEMM B operand
   bool fused_p1 = false;         // K == 1: row + column statistics from one S pass (FC_FUSED_P1=0: two passes)
   bool pdl = true;               // programmatic dependent launch between the step's kernels (FC_PDL=0: off)
-  bool split_tail = true;        // similarity kernels: leftover tiles as half tiles (FC_SPLIT_TAIL=0: off)
+  bool split_tail = false;       // similarity kernels: leftover tiles as half tiles (FC_SPLIT_TAIL=1; measured neutral)
   int gemm_drain = 0;            // FC_GEMM_DRAIN: stream-K unit-boundary cost in k-blocks (0: KB / 10)
   long long* dbg_buf = nullptr;   // FC_SIM_DEBUG=9 MMA-warp counters: [launch 0: pass 1, 1: pass 2][pair][8]             // FC_SIM_DEBUG perf experiments (results invalid when set)
   struct GraphEntry {

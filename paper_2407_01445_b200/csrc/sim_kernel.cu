@@ -568,9 +568,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(SimCfg<kMode>::kThre
       int s, rb, jt, half;
       decode_item(p, pi, item, s, rb, jt, half);
       const SimSeg& sg = p.seg[s];
-      // a half tile holds its 128 columns in TMEM columns 0..127; the warps past them idle
+      // a half tile holds its 128 columns in TMEM columns 0..127. FUSED / Q / RAW spread them
+      // over all column groups (half the chunks per warp); STATS keeps its 64-column row
+      // partials per warp, so there the groups past 128 columns idle
       const int tile_off = half < 0 ? 0 : half * (kPairN / 2);   // first column inside the 256-wide tile
-      const bool active = static_cast<int>(cq) * kColsW < (half < 0 ? kPairN : kPairN / 2);
+      constexpr bool kSpreadHalf = kMode != kSimStats;
+      const int cols_w = (half >= 0 && kSpreadHalf) ? kColsW / 2 : kColsW;   // this warp's columns
+      const int chunks_w = cols_w / 32;
+      const bool active = static_cast<int>(cq) * cols_w < (half < 0 ? kPairN : kPairN / 2);
       const uint32_t acc = it & 1;
       const uint32_t acc_phase = (it >> 1) & 1;
       const int warp_row0 = rb * kPairM + static_cast<int>(rank) * kCtaM + static_cast<int>(q4) * 32;
@@ -579,7 +584,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(SimCfg<kMode>::kThre
       const bool warp_rows_ok = warp_row0 + 32 <= sg.rows;
       const int g0 = sg.a_row0 + warp_row0;     // global index of lane 0's anchor
       const int gi = g0 + static_cast<int>(lane);
-      const int colq = jt * kPairN + tile_off + static_cast<int>(cq) * kColsW;
+      const int colq = jt * kPairN + tile_off + static_cast<int>(cq) * cols_w;
 
       float2 rstat = make_float2(0.f, 0.f);
       float rk = 0.f, rbeta = 0.f, rc = 0.f, rf = 0.f;
@@ -605,7 +610,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(SimCfg<kMode>::kThre
 #pragma unroll
         for (int h = 0; h < kChunksW; ++h) {
           const int jc = colq + 32 * h + static_cast<int>(lane);
-          cst_all[h] = jc < sg.cols ? sg.col_stat[jc] : f2(0.f, 0.f);
+          cst_all[h] = (h < chunks_w && jc < sg.cols) ? sg.col_stat[jc] : f2(0.f, 0.f);
         }
       }
       long long ta = eprof ? clock64() : 0;
@@ -615,7 +620,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(SimCfg<kMode>::kThre
       tc_fence_after();
       // safe_exp can only clamp if some exponent may exceed 60: |s| <= |E1|max |E2|max bounds it
       const float smax = sqrtf(bnd0 * bnd1) * 1.0001f;
-      const uint32_t taddr = tmem_base + ((q4 * 32u) << 16) + acc * kPairN + cq * kColsW;
+      const uint32_t taddr = tmem_base + ((q4 * 32u) << 16) + acc * kPairN + cq * static_cast<uint32_t>(cols_w);
       float2 se2 = f2(0.f, 0.f), sye2 = f2(0.f, 0.f);
       float se = 0.f, sye = 0.f;
       uint32_t ncl = 0;
@@ -625,7 +630,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(SimCfg<kMode>::kThre
       if constexpr (kMode == kSimQ) {
         ps = it % kSimPSlots;
         mbar_wait(&L.pfull[ps], (it / kSimPSlots) & 1);
-        par = L.par + ps * (kSimPSlotBytes / 4) + tile_off + cq * kColsW;
+        par = L.par + ps * (kSimPSlotBytes / 4) + tile_off + cq * cols_w;
         q_col_safe = 2.f * smax * bnd2 <= kClampLog2;
         // factorized form: 2^(s kappa) stays within [2^-63, 2^63] and fac within fp32 range
         q_fact = p.q_factor && __all_sync(0xffffffffu, rk * smax <= kFactMaxLog2);
@@ -644,13 +649,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(SimCfg<kMode>::kThre
         }
       }
 #pragma unroll 1
-      for (int h = 0; h < (active ? kChunksW : 0); ++h) {
+      for (int h = 0; h < (active ? chunks_w : 0); ++h) {
         uint32_t rr[kMode == kSimFused ? 1 : 32];
         if constexpr (kMode != kSimFused) {
           tmem_ld_32x32b_x32(taddr + 32 * h, rr);
           tmem_ld_wait();
         }
-        if (kMode != kSimFused && h == kChunksW - 1) {   // the tile is in registers: hand the TMEM buffer back
+        if (kMode != kSimFused && h == chunks_w - 1) {   // the tile is in registers: hand the TMEM buffer back
           tc_fence_before();
           __syncwarp();
           if (lane == 0) {
@@ -684,7 +689,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(SimCfg<kMode>::kThre
           uint32_t r32[32];
           tmem_ld_32x32b_x32(taddr + 32 * h, r32);
           tmem_ld_wait();
-          if (h == kChunksW - 1) {   // the tile is in registers: release the TMEM buffer
+          if (h == chunks_w - 1) {   // the tile is in registers: release the TMEM buffer
             tc_fence_before();
             __syncwarp();
             if (lane == 0) {
@@ -716,7 +721,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(SimCfg<kMode>::kThre
             const float sc = ex2_approx(rstat.y);
             const float rx = se2.x + se2.y, rzx = sye2.x + sye2.y;
             const float sxe = sc * fmaf(rstat.y, rx, rzx) + sye;
-            const int quarter = (tile_off + static_cast<int>(cq) * kColsW + 32 * h) / 64;
+            const int quarter = (tile_off + static_cast<int>(cq) * cols_w + 32 * h) / 64;
             if (row_ok)
               sg.partial[static_cast<size_t>(r_loc) * (p.n_jt * 4) + jt * 4 + quarter] = make_float2(se + sc * rx, sxe);
             se2 = f2(0.f, 0.f); sye2 = f2(0.f, 0.f); se = 0.f; sye = 0.f;

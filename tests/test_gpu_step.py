@@ -146,7 +146,7 @@ def test_large_table_indexing():
 
 
 @pytest.mark.parametrize("env", [{"FC_GRAPH": "0"}, {"FC_PDL": "0"}, {"FC_FUSED_P1": "0"}, {"FC_Q_FACTOR": "0"},
-                                 {"FC_SPLIT_TAIL": "0"}])
+                                 {"FC_SPLIT_TAIL": "1"}])
 def test_step_launch_modes(env, monkeypatch):
     # the same step through the non-default launch paths: direct launches (programmatic
     # dependent launches without a graph), no PDL, the two-segment pass 1 and the
