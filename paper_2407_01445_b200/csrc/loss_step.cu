@@ -137,6 +137,7 @@ struct LossStep {
   int sim_debug = 0, gemm_debug = 0;
   bool q_factor = true;          // FC_Q_FACTOR=0 forces the two-exponential Q path (A/B checks)
   bool gemm_mc = false;          // FC_GEMM_MC=1: clusters of two pairs multicast the GEMM B operand
+  int gemm_mc_clusters = 0;      // co-resident clusters of 4 (the persistent stream-K grid when gemm_mc)
   bool fused_p1 = false;         // K == 1: row + column statistics from one S pass (FC_FUSED_P1=0: two passes)
   bool pdl = true;               // programmatic dependent launch between the step's kernels (FC_PDL=0: off)
   bool split_tail = false;       // similarity kernels: leftover tiles as half tiles (FC_SPLIT_TAIL=1; measured neutral)
@@ -289,6 +290,11 @@ struct LossStep {
     if (const char* e = std::getenv("FC_SHARED_Q")) shared_q = shared_q && atoi(e) != 0;
     FC_CUDA(fc::sim_set_smem());
     FC_CUDA(fc::gemm_set_smem());
+    if (gemm_mc) {
+      FC_CUDA(fc::gemm_max_active_clusters(2, &gemm_mc_clusters));
+      gemm_mc_clusters = std::min(gemm_mc_clusters, n_sm / 4);
+      if (gemm_mc_clusters < 1) gemm_mc = false;
+    }
     // side-branch kernels run beside persistent similarity CTAs: ask for the max-shared
     // carveout so the SM configuration they land on never has to change for a pass-2 CTA
     FC_CUDA(cudaFuncSetAttribute(fc::fc_reduce_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
@@ -781,7 +787,8 @@ struct LossStep {
     }
     gp.n_tiles = (gp.n_mb[0] + gp.n_mb[1]) * gp.n_nb;
     // every unit reduce-adds into dE (zeroed on the side branch of this step)
-    const int gemm_ctas = (n_sm / (2 * gp.pairs_per_cluster)) * 2 * gp.pairs_per_cluster;
+    // persistent: exactly the clusters that co-reside (clusters of 4 pack into fewer than 148 SMs)
+    const int gemm_ctas = gemm_mc ? 4 * gemm_mc_clusters : (n_sm / 2) * 2;
     balance_units(gp, gemm_ctas / (2 * gp.pairs_per_cluster));
     CUtensorMap mX[2] = {mE2n, mE1n};
     CUtensorMap mQs[2] = {mQ[0], shared_q ? mQt : mQ[1]};

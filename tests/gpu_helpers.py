@@ -39,8 +39,10 @@ def norm_rel(a, b):
 
 
 def run_pair(variant: str, B: int, d: int, N: int, steps: int = 2, gamma: float = 0.6,
-             eps: float = 1e-14, seed: int = 0, warm: bool = True, cfg_over=None):
-    """Runs `steps` K=1 steps on the GPU and in the oracle; returns per-step (gpu, oracle)."""
+             eps: float = 1e-14, seed: int = 0, warm: bool = True, cfg_over=None, checker=None):
+    """Runs `steps` K=1 steps on the GPU and in the oracle; returns per-step (gpu, oracle).
+    `checker`: the oracle's step function (default: the C restatement, oracle.step; the
+    full-size tests pass the vectorised restatement oracle_np.step)."""
     import torch
     import paper_2407_01445_b200 as P
     ocfg = O.default_config(variant, N, **(cfg_over or {}))
@@ -56,7 +58,7 @@ def run_pair(variant: str, B: int, d: int, N: int, steps: int = 2, gamma: float 
         ids = S.ids(B, N, seed * 1000 + s)
         E1 = S.bf16_to_f32(b1).astype(np.float64)
         E2 = S.bf16_to_f32(b2).astype(np.float64)
-        ref = O.step(ocfg, st, 1, E1, E2, ids, gamma, eps)
+        ref = (checker or O.step)(ocfg, st, 1, E1, E2, ids, gamma, eps)
         de1, de2 = step.step(to_dev_bf16(b1), to_dev_bf16(b2), torch.from_numpy(ids).cuda(), gamma, eps)
         sc = step.scalars()
         views = step.local_views()

@@ -160,3 +160,40 @@ def test_oracle_matches_reference_live():
             for k in ("dE1", "dE2", "g1", "g2", "u1", "u2"):
                 np.testing.assert_allclose(a[k], b[k], rtol=1e-12, err_msg=f"{var} K{K} {k}")
             assert a["tau_new"] == b["tau_new"]
+
+
+@pytest.mark.parametrize("variant", ["fastclip_v3", "fastclip_v2", "fastclip_v1", "fastclip_v0", "openclip_mbcl",
+                                     "sogclr", "isogclr"])
+@pytest.mark.parametrize("K", [1, 2, 4])
+def test_vectorised_oracle_matches_c_oracle(variant, K):
+    # oracle/oracle_np.py (the full-size checker of tests/test_gpu_fullsize.py) against the C
+    # restatement: 3 chained steps from warm tables, every output and the updated state
+    import oracle_np as ON
+    B, d, N = 96, 24, 500
+    for tau_init in (None, 0.005):       # 0.005: the tau floor, safe_exp clamps are hit
+        over = {} if tau_init is None else dict(tau_init=tau_init)
+        cfg = O.default_config(variant, N, **over)
+        a, b = O.new_state(cfg), O.new_state(cfg)
+        a.u1[:] = b.u1[:] = S.warm_u(N, 0)
+        a.u2[:] = b.u2[:] = S.warm_u(N, 1)
+        for s in range(3):
+            b1, b2 = S.embeddings(B, d, 5 + s)
+            ids = S.ids(B, N, 5 + s)
+            E1 = S.bf16_to_f32(b1).astype(np.float64)
+            E2 = S.bf16_to_f32(b2).astype(np.float64)
+            r1 = O.step(cfg, a, K, E1, E2, ids, 0.6, 1e-14)
+            r2 = ON.step(cfg, b, K, E1, E2, ids, 0.6, 1e-14)
+            for k in ("dE1", "dE2", "g1", "g2", "u1", "u2", "gtau1", "gtau2", "gtau_local"):
+                x, y = np.asarray(r1[k]), np.asarray(r2[k])
+                assert np.max(np.abs(x - y)) <= 1e-12 * max(np.max(np.abs(x)), 1e-300), (variant, K, s, k)
+            for k in ("loss", "gtau", "tau_new"):
+                assert abs(r1[k] - r2[k]) <= 1e-12 * abs(r1[k]) + 1e-300, (variant, K, s, k)
+            assert r1["clamps_g"] == r2["clamps_g"]
+        for t in ("u1", "u2", "tau1", "tau2", "m1", "v1", "m2", "v2"):
+            x = getattr(a, t)
+            if x is not None:
+                assert np.max(np.abs(x - getattr(b, t))) <= 1e-12 * max(np.max(np.abs(x)), 1e-300), (variant, K, t)
+        if a.s1 is not None:
+            np.testing.assert_array_equal(a.s1, b.s1)
+            np.testing.assert_array_equal(a.s2, b.s2)
+        assert (a.tau, a.tau_step, a.latched) == pytest.approx((b.tau, b.tau_step, b.latched), rel=1e-12)
