@@ -162,7 +162,7 @@ struct LossStep {
   std::vector<GraphEntry> graphs;
   // optional per-phase CUDA events (bench roofline): phases of the last step
   static constexpr int kPhases = 6;
-  static constexpr int kAnchorBlock = 128;   // fc_anchor_kernel: 16 anchors (8-lane groups) per block
+  static constexpr int kAnchorBlock = 128;   // fc_anchor_kernel: 8 anchors (16-lane groups) per block
   static constexpr int kWeightsBlock = 64;   // fc_weights_kernel: thread per anchor, >= 80 blocks at B = 5120   // gatherE, prep, pass1, scalars, pass2, gemm
   bool timing = false;
   int ev_slots = 0, ev_cur = 0;        // ring of per-step event sets (no host sync between steps)
@@ -300,6 +300,12 @@ struct LossStep {
     FC_CUDA(cudaFuncSetAttribute(fc::fc_reduce_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
                                  cudaSharedmemCarveoutMaxShared));
     FC_CUDA(cudaFuncSetAttribute(fc::fc_zero_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                 cudaSharedmemCarveoutMaxShared));
+    // prep and the per-anchor kernel run while the next similarity pass's CTAs (227 KB of
+    // shared memory each) take their SMs (programmatic launch)
+    FC_CUDA(cudaFuncSetAttribute(fc::fc_prep_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                 cudaSharedmemCarveoutMaxShared));
+    FC_CUDA(cudaFuncSetAttribute(fc::fc_anchor_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
                                  cudaSharedmemCarveoutMaxShared));
     FC_CUDA(cudaFuncSetAttribute(fc::fc_indiv_update_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
                                  cudaSharedmemCarveoutMaxShared));

@@ -424,7 +424,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(SimCfg<kMode>::kThre
         // (the 128-row box then also brings 64 rows the UMMA does not read)
         const int b_row = half < 0 ? jt * kPairN + static_cast<int>(rank) * (kPairN / 2)
                                    : jt * kPairN + half * (kPairN / 2) + static_cast<int>(rank) * (kPairN / 4);
-        if constexpr (kMode == kSimQ) load_params(it);   // ahead of the tile's operands
+        // params ahead of the tile's operands, except for the pair's first tile: its operands
+        // go out first, so its MMAs run while the per-anchor kernel is still producing the
+        // parameters (the first param load is the grid-dependency wait)
+        if constexpr (kMode == kSimQ) if (it >= 1) load_params(it);
         for (int c = 0; c < n_chunks; ++c) {
           const int kb_lo = c * kSimASlots;
           const int kb_hi = min(nkb, kb_lo + kSimASlots);
@@ -459,6 +462,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(SimCfg<kMode>::kThre
             if (++stage == kStagesB) { stage = 0; phase ^= 1; }
           }
         }
+        if constexpr (kMode == kSimQ) if (it == 0) load_params(0);
       }
     }
   } else if (warp == kMmaWarp) {

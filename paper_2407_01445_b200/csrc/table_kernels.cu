@@ -31,6 +31,9 @@ namespace fc {
 // emit the pass-1 row parameters.
 __global__ void fc_prep_kernel(const __nv_bfloat16* __restrict__ e1, const __nv_bfloat16* __restrict__ e2,
                                StepArgs a, double gamma, double eps) {
+  // pass 1 (programmatic launch) may take SMs now: its operand loads and MMAs do not read
+  // anything prep writes; its epilogue waits for this grid (griddepcontrol.wait)
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const int w = (blockIdx.x * blockDim.x + threadIdx.x) / 32;
   const int lane = threadIdx.x & 31;
   if (a.dbg && threadIdx.x == 0) {   // debug timeline: first entry / last exit of the grid

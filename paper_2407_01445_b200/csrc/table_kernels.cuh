@@ -27,7 +27,7 @@ struct StepResult {
 };
 
 // lanes per anchor in fc_anchor_kernel (partial reduction width; the leader runs the fp64 chain)
-constexpr int kAnchorLanes = 8;
+constexpr int kAnchorLanes = 16;
 
 struct StepArgs {
   // shapes / config

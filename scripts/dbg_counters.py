@@ -65,7 +65,8 @@ print('  pass2: first entry', f(tls[1][:, 0].min()), 'last entry', f(tls[1][:, 0
 if os.environ.get('FC_GEMM_DEBUG') in ('9', '10'):
     print('  gemm : first entry', f(g[:, 11].min()), 'last entry', f(g[:, 11].max()), 'epi end min', f(g[:, 10].min()), 'epi end max', f(g[:, 10].max()))
 an = out[2 * R + 160 * 16:2 * R + 160 * 16 + 640 * 8].reshape(640, 8)
-print('  anchor: entry', f(an[:, 0].min()), '..', f(an[:, 0].max()), 'wait done', f(an[:, 1].min()), '..', f(an[:, 1].max()),
-      'partials reduced', f(an[:, 2].min()), '..', f(an[:, 2].max()), 'fp64 done', f(an[:, 3].min()), '..', f(an[:, 3].max()),
-      'exit', f(an[:, 4].min()), '..', f(an[:, 4].max()))
+an = an[an[:, 0] != 0]
+pc = lambda x: [f(v) for v in np.percentile(x, [0, 10, 50, 90, 100])]
+print(f'  anchor ({len(an)} blocks) [min p10 p50 p90 max]: entry', pc(an[:, 0]), 'wait done', pc(an[:, 1]),
+      'partials reduced', pc(an[:, 2]), 'fp64 done', pc(an[:, 3]), 'exit', pc(an[:, 4]))
 print('  prep: first entry', f(out[2 * R + 160 * 16 + 8 * 640]), 'last exit', f(out[2 * R + 160 * 16 + 8 * 640 + 1]))
