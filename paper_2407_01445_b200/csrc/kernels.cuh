@@ -25,7 +25,11 @@ constexpr int kSimEpiWarps = 16;   // 4 per TMEM lane quarter, 64 columns each
 constexpr int kSimThreads = (2 + kSimEpiWarps) * 32;
 constexpr int kSimPSlots = 3;      // column-parameter slots (Q pass): kappa, beta, coef, fac x 256
 constexpr int kSimPSlotBytes = 4 * kPairN * 4;   // kappa, beta, coef, fac
-constexpr int kSimSmemStats = kSimASlots * kStageBytesA + kSimStagesStats * kStageBytesB + kSimPSlots * kSimPSlotBytes;
+// STATS / FUSED / RAW: the parameter region doubles as the fused pass's column-sum exchange,
+// [tile parity][column group][chunk][lane quarter][32] float2
+constexpr int kSimRedBytes = 2 * 2 * 4 * 4 * 32 * 8;
+constexpr int kSimParRedBytes = kSimRedBytes > kSimPSlots * kSimPSlotBytes ? kSimRedBytes : kSimPSlots * kSimPSlotBytes;
+constexpr int kSimSmemStats = kSimASlots * kStageBytesA + kSimStagesStats * kStageBytesB + kSimParRedBytes;
 constexpr int kSimSmemQ = kSimASlots * kStageBytesA + kSimStagesQ * kStageBytesB + kSimPSlots * kSimPSlotBytes +
                           kSimEpiWarps * kSimStageOutQ;
 constexpr int kSimSmemBytes = (kSimSmemStats > kSimSmemQ ? kSimSmemStats : kSimSmemQ) + 1024 + 512;
@@ -75,8 +79,9 @@ struct SimParams {
   // gradient GEMM later accumulates into with TMA reduce-add
   float4* zero_a; float4* zero_b;          // nullptr: nothing to zero
   long long zero_n4;                       // float4 count of each
-  // FUSED: column statistics {sum e, sum y e} per (row slot = 32-row quarter of a pair tile,
-  // column), laid out [cols / 32][n_slots][32]; fuse_fast enables the one-exponential path
+  // FUSED: column statistics {sum e, sum y e} per (row slot = one CTA of a pair row block,
+  // column), laid out [cols / 32][n_slots][32] with n_slots = 2 per pair row block (the CTA's
+  // four 32-row warp sums are added in shared memory); fuse_fast enables the one-exponential path
   float2* col_partial;
   int n_slots;
   int fuse_fast;

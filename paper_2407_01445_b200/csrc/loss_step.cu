@@ -239,8 +239,8 @@ struct LossStep {
     diag = dalloc<float>(B);
     rowstat = dalloc<float2>(2 * static_cast<size_t>(Bl));
     partial = dalloc<float2>(2 * static_cast<size_t>(Bl) * n_jt * 4);
-    if (K == 1)   // [ceil(B/32)][n_slots][32]: 256-byte warp stores, 32-byte reads per 4 anchors
-      col_partial = dalloc<float2>(static_cast<size_t>((Bl + fc::kPairM - 1) / fc::kPairM) * 8 * ((B + 31) / 32 * 32));
+    if (K == 1)   // [ceil(B/32)][n_slots = 2 per pair row block][32]: 256-byte warp stores
+      col_partial = dalloc<float2>(static_cast<size_t>((Bl + fc::kPairM - 1) / fc::kPairM) * 2 * ((B + 31) / 32 * 32));
     clamps = dalloc<unsigned long long>(1);
     bounds = dalloc<float>(4 * fc::kMaxPeers);   // one {norm1, norm2, kappa, -} slot per rank
     FC_CUDA(cudaMemset(bounds, 0, 4 * fc::kMaxPeers * sizeof(float)));
@@ -683,7 +683,7 @@ struct LossStep {
       sp.n_items = sp.n_rb[0] * n_jt;
       sp.seg[0].col_stat = a.rowstat_C;
       sp.col_partial = col_partial;
-      sp.n_slots = sp.n_rb[0] * 8;
+      sp.n_slots = sp.n_rb[0] * 2;   // one column partial per CTA of each pair row block
       sp.fuse_fast = indiv ? 0 : 1;
       a.col_partial = col_partial;
       a.col_slots = sp.n_slots;

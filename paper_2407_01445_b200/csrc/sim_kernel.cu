@@ -47,7 +47,8 @@ __device__ __forceinline__ SmemLayout carve(uint8_t* base) {
   L.b = p + kSimASlots * kStageBytesA;
   L.qout = L.b + kStagesB * kStageBytesB;
   L.par = reinterpret_cast<float*>(L.qout + (kStagesB == kSimStagesQ ? kSimEpiWarps * kSimStageOutQ : 0));
-  uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(L.par) + kSimPSlots * kSimPSlotBytes);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(L.par) +
+                                               (kStagesB == kSimStagesQ ? kSimPSlots * kSimPSlotBytes : kSimParRedBytes));
   L.full = bars;
   L.empty = L.full + kStagesB;
   L.afull = L.empty + kStagesB;
@@ -644,6 +645,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(SimCfg<kMode>::kThre
       const bool row_safe = !__any_sync(0xffffffffu, row_ok && fmaf(smax, row_kap, row_beta) > kClampLog2);
       // FUSED one-exponential form: 2^(s kappa) and 2^beta stay inside [2^-63, 2^63]
       const bool fused_ok = kMode == kSimFused && __all_sync(0xffffffffu, row_kap * smax <= kFactMaxLog2);
+      // FUSED: [chunk][q4][32] column sums of this column group for the tile (parity buffer)
+      float2* red = reinterpret_cast<float2*>(L.par) + ((it & 1) * 2 + static_cast<int>(cq)) * (4 * 4 * 32);
       if (!active) {   // half tile, columns beyond it: hand the buffer back at once
         tc_fence_before();
         __syncwarp();
@@ -718,8 +721,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(SimCfg<kMode>::kThre
             cye = sc * fmaf(cst.y, ce, cye);
             ce = sc * ce;
           }
-          if (jc < sg.cols)
-            p.col_partial[(static_cast<size_t>(col0 >> 5) * p.n_slots + (rb * 8 + rank * 4 + q4)) * 32 + lane] = f2(ce, cye);
+          // this warp's 32-row column sums -> shared memory; the tile's four lane-quarter warps
+          // of this column group combine them after the chunk loop
+          red[(h * 4 + static_cast<int>(q4)) * 32 + lane] = f2(ce, cye);
           if (h & 1) {   // 64 columns done: one row partial per (row, column quarter)
             // fast-path row raw sums {sum x, sum z x} -> e = 2^beta_i x, y e = (z + beta_i) e
             const float sc = ex2_approx(rstat.y);
@@ -757,6 +761,27 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(SimCfg<kMode>::kThre
               tma_store_2d(s ? &mapQo1 : &mapQo0, stg, col0, warp_row0);
               bulk_commit();
             }
+          }
+        }
+      }
+      if constexpr (kMode == kSimFused) {
+        // column partials: the four lane-quarter warps of the column group add their 32-row sums
+        // in fixed order (q4 = 0..3), warp q4 taking chunk q4 -> one partial per (CTA, column),
+        // a quarter of the partials the per-anchor kernel reads. One named barrier per tile;
+        // the buffer alternates with the tile parity (the next tile's barrier orders the reuse).
+        if (active) {
+          named_bar_sync(1 + cq, 128);
+          if (static_cast<int>(q4) < chunks_w) {
+            float2 v = red[(q4 * 4 + 0) * 32 + lane];
+#pragma unroll
+            for (int q = 1; q < 4; ++q) {
+              const float2 w = red[(q4 * 4 + q) * 32 + lane];
+              v.x += w.x;
+              v.y += w.y;
+            }
+            const int col0 = colq + 32 * static_cast<int>(q4);
+            if (col0 + static_cast<int>(lane) < sg.cols)
+              p.col_partial[(static_cast<size_t>(col0 >> 5) * p.n_slots + (rb * 2 + rank)) * 32 + lane] = v;
           }
         }
       }

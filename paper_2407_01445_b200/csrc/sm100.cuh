@@ -198,6 +198,10 @@ __device__ __forceinline__ void tmem_ld_32x32b_x16(uint32_t taddr, uint32_t (&r)
         "=r"(r[14]), "=r"(r[15])
       : "r"(taddr));
 }
+// named barrier `id` (1..15) over `n` threads (a multiple of 32) of this CTA
+__device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t n) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
 // Programmatic dependent launch: a kernel launched with programmatic stream serialization may
 // start while its predecessor drains; griddep_wait() blocks until the predecessor grid has
 // completed and its writes are visible (a no-op for a normally launched kernel).
