@@ -134,11 +134,20 @@ __device__ __forceinline__ void store_params(const StepArgs& a, int i, const Anc
   a.kap2[i] = p.k2; a.bet2[i] = b2; a.coef2[i] = c2; a.fac2[i] = c2 * exp2f(b2);
 }
 
-// Local anchor: tau-gradient and loss terms (engine.cpp:198-266, losses.cpp:126-180); v2 writes
-// its per-anchor tau gradients.
+// The four logarithms of an anchor's tau-gradient / loss terms, one per lane of its group:
+// lane k of the group evaluates log(arg_k) with arg = {eps + u1, eps + u2, e + g1, e + g2}
+// (e = 1/(B-1) for MBCL, eps otherwise).
+__device__ __forceinline__ double log_arg(const StepArgs& a, int k, double u1, double u2, double g1, double g2,
+                                          double eps) {
+  const double e = a.variant == 0 ? 1.0 / static_cast<double>(a.B - 1) : eps;
+  return k == 0 ? eps + u1 : k == 1 ? eps + u2 : k == 2 ? e + g1 : e + g2;
+}
+
+// Local anchor: tau-gradient and loss terms (engine.cpp:198-266, losses.cpp:126-180) from the
+// precomputed logs lu = log(eps + u), lg = log(e + g); v2 writes its per-anchor tau gradients.
 __device__ __forceinline__ void local_terms(const StepArgs& a, int r, const AnchorParams& p, double u1, double u2,
-                                            double g1, double g2, double dx1, double dx2, double eps, double& ta,
-                                            double& tb, double& tl) {
+                                            double g1, double g2, double dx1, double dx2, double eps, double lu1,
+                                            double lu2, double lg1, double lg2, double& ta, double& tb, double& tl) {
   const double t1 = p.t1, t2 = p.t2;
   const double inv = 1.0 / static_cast<double>(a.B - 1);
   const double ds1 = (-(dx1 / (t1 * t1))) * inv;   // engine.cpp:198-205
@@ -146,16 +155,16 @@ __device__ __forceinline__ void local_terms(const StepArgs& a, int r, const Anch
   if (a.variant == 0) {
     const double c = inv;
     ta = ds1 / (c + g1) + ds2 / (c + g2);                 // grad_tau_mbcl (engine.cpp:261-266)
-    tl = log(c + g1) + log(c + g2);                       // eval_mbcl (losses.cpp:168-180)
+    tl = lg1 + lg2;                                       // eval_mbcl (losses.cpp:168-180)
   } else if (a.individual) {
     const double inv_n = 1.0 / static_cast<double>(a.n_train);   // engine.cpp:240-259
-    a.gt1[r] = inv_n * (log(eps + u1) + a.rho + t1 * ds1 / (eps + u1));
-    a.gt2[r] = inv_n * (log(eps + u2) + a.rho + t2 * ds2 / (eps + u2));
-    tl = t1 * (log(eps + g1) + a.rho) + t2 * (log(eps + g2) + a.rho);  // eval_rgcl
+    a.gt1[r] = inv_n * (lu1 + a.rho + t1 * ds1 / (eps + u1));
+    a.gt2[r] = inv_n * (lu2 + a.rho + t2 * ds2 / (eps + u2));
+    tl = t1 * (lg1 + a.rho) + t2 * (lg2 + a.rho);          // eval_rgcl
   } else {
     ta = ds1 / (eps + u1) + ds2 / (eps + u2);             // grad_tau_unscaled (engine.cpp:208-224)
-    tb = log(eps + u1) + log(eps + u2);                   // grad_tau_margin logs (engine.cpp:226-238)
-    tl = log(eps + g1) + log(eps + g2);                   // eval_gcl (losses.cpp:126-138)
+    tb = lu1 + lu2;                                       // grad_tau_margin logs (engine.cpp:226-238)
+    tl = lg1 + lg2;                                       // eval_gcl (losses.cpp:126-138)
   }
 }
 
@@ -199,11 +208,17 @@ __device__ __forceinline__ void anchor_work(const StepArgs& a, int r, int sub, d
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     a.dbg[blockIdx.x * 8 + 2] = t;
   }
+  // every lane of the group holds the sums: g, u and the weights are evaluated redundantly, and
+  // the four logarithms of the anchor's terms run on four lanes at once
+  const TableVals v = table_math(a, s1, x1, s2, x2, kr, kc, uo1, uo2, gamma);
+  const double lg = log(log_arg(a, sub & 3, v.u1, v.u2, v.g1, v.g2, eps));
+  const int base = (threadIdx.x & 31) & ~(kGroup - 1);
+  const double lu1 = __shfl_sync(0xffffffffu, lg, base + 0), lu2 = __shfl_sync(0xffffffffu, lg, base + 1);
+  const double lg1 = __shfl_sync(0xffffffffu, lg, base + 2), lg2 = __shfl_sync(0xffffffffu, lg, base + 3);
   if (sub == 0 && valid) {
-    const TableVals v = table_math(a, s1, x1, s2, x2, kr, kc, uo1, uo2, gamma);
     const AnchorParams p = anchor_params(a, v.u1, v.u2, t1, t2, tau, eps);
     kmax = fmaxf(kmax, fmaxf(p.k1, p.k2));
-    local_terms(a, r, p, v.u1, v.u2, v.g1, v.g2, v.dx1, v.dx2, eps, ta, tb, tl);
+    local_terms(a, r, p, v.u1, v.u2, v.g1, v.g2, v.dx1, v.dx2, eps, lu1, lu2, lg1, lg2, ta, tb, tl);
     a.rcoef[r] = static_cast<float>(p.c1 * s1 + p.c2 * s2);
     store_params(a, a.row0 + r, p, s_ii);
     a.sum1[r] = s1; a.dx1[r] = v.dx1; a.sum2[r] = s2; a.dx2[r] = v.dx2;
