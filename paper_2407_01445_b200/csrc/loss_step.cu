@@ -979,9 +979,12 @@ int fc_step_scalars_get(void* ctx, fc_step_scalars* out) {
   out->tau = s->result_h->tau;
   out->exp_clamps = s->result_h->clamps;
   out->latched = s->result_h->latched;
-  if (s->result_h->err) {
-    g_last_error = "non-finite temperature gradient";
-    return s->result_h->err;
+  if (const int e = s->result_h->err) {   // device-detected failures of the step (sticky)
+    g_last_error = e == FC_ERR_SHAPE ? "ids: dataset index out of range [0, n_train) (UTable::update, state.cpp:46)"
+                 : e == FC_ERR_NUMERIC ? "non-finite temperature gradient (optimizers.cpp:67)"
+                 : e == FC_ERR_NCCL ? "peer all-gather handshake timed out (a rank stopped stepping)"
+                 : "device-side step failure";
+    return e;
   }
   return FC_OK;
 }

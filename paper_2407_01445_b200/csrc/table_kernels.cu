@@ -67,7 +67,11 @@ __global__ void fc_prep_kernel(const __nv_bfloat16* __restrict__ e1, const __nv_
     xs[i] = v < nv ? __ldg(x4 + v) : make_uint4(0u, 0u, 0u, 0u);
     ys[i] = v < nv ? __ldg(y4 + v) : make_uint4(0u, 0u, 0u, 0u);
   }
-  const int id = lead ? a.ids[r] : 0;
+  int id = lead ? a.ids[r] : 0;
+  if (lead && (id < 0 || id >= a.n_train)) {   // UTable::update range check (state.cpp:46)
+    atomicExch(a.err, 2);                       // ShapeError; the table is not touched at this id
+    id = 0;
+  }
   float acc = 0.f, n1 = 0.f, n2 = 0.f;
   auto accum = [&](const uint4& x, const uint4& y) {
     const uint32_t xx[4] = {x.x, x.y, x.z, x.w};
@@ -154,8 +158,8 @@ __global__ void fc_weights_kernel(StepArgs a) {
     const double* blk = a.recv + static_cast<size_t>(k) * a.pstride;
     const double u1 = blk[r], u2 = blk[a.Bl + r];
     const double t1 = blk[2 * a.Bl + r], t2 = blk[3 * a.Bl + r];
-    if (a.track_u && k != a.rank) {   // keep this rank's full u replica equal to the shared UTable
-      const int id = static_cast<int>(blk[4 * a.Bl + r]);
+    const int id = static_cast<int>(blk[4 * a.Bl + r]);
+    if (a.track_u && k != a.rank && id >= 0 && id < a.n_train) {   // keep this rank's u replica equal to the UTable
       a.u1_tab[id] = u1;
       a.u2_tab[id] = u2;
     }
@@ -315,6 +319,7 @@ __global__ void fc_indiv_update_kernel(StepArgs a) {
   const int r = i % a.Bl;
   const double* blk = a.recv + static_cast<size_t>(k) * a.pstride;
   const int id = static_cast<int>(blk[4 * a.Bl + r]);
+  if (id < 0 || id >= a.n_train) return;   // rejected by its owner's prep (ShapeError)
   const double gts[2] = {blk[5 * a.Bl + r], blk[6 * a.Bl + r]};
   double* taus[2] = {a.tau1_tab, a.tau2_tab};
   double* ms[2] = {a.m1_tab, a.m2_tab};

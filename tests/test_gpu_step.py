@@ -157,3 +157,28 @@ def test_step_launch_modes(env, monkeypatch):
         res, _, _, _ = run_pair(variant, B=320, d=96, N=4000, steps=3, seed=17)
         for i, (got, ref) in enumerate(res):
             _check(got, ref, f"{env} {variant} step {i}")
+
+
+@pytest.mark.parametrize("variant", ["fastclip_v3", "fastclip_v2"])
+def test_out_of_range_id_is_a_shape_error(variant):
+    # UTable::update rejects an index outside [0, N) with ShapeError (state.cpp:46): the step
+    # reports FC_ERR_SHAPE at the scalar readback and never writes the tables out of bounds
+    import torch
+    import paper_2407_01445_b200 as P
+    N, B, d = 3000, 128, 64
+    ocfg = O.default_config(variant, N)
+    step = P.LossStep(gpu_cfg(ocfg, d, B))
+    u0 = S.warm_u(N, 3)
+    step.load_tables(u1=u0, u2=u0)
+    b1, b2 = S.embeddings(B, d, 4)
+    ids = S.ids(B, N, 4)
+    ids[7] = N          # one past the table
+    ids[9] = -5
+    step.step(to_dev_bf16(b1), to_dev_bf16(b2), torch.from_numpy(ids).cuda(), 0.6, 1e-14)
+    with pytest.raises(P.FastclipError) as e:
+        step.scalars()
+    assert e.value.code == 2
+    u = step.tables()["u1"]
+    ok = np.ones(N, bool)
+    ok[ids[(ids >= 0) & (ids < N)]] = False
+    np.testing.assert_array_equal(u[ok], u0[ok])   # untouched entries identical
