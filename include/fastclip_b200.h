@@ -123,7 +123,11 @@ int fc_destroy(void* ctx);
  * temperature_step / IndividualTemp::update (optimizers.cpp:77-83, state.cpp:124-131). */
 int fc_loss_step(void* ctx, const fc_step_in* in, fc_step_out* out, void* stream);
 
-/* Waits for the last step and returns its scalars. */
+/* Waits for the last step and returns its scalars. Failures the device detects during a step
+ * are returned here and stay set for the context (the reference throws and the run ends):
+ * FC_ERR_SHAPE for an id outside [0, n_train) (state.cpp:46; the table is never written at
+ * such an id), FC_ERR_NUMERIC for a non-finite tau gradient (optimizers.cpp:67), FC_ERR_NCCL
+ * when a peer all-gather handshake times out (a rank stopped stepping). */
 int fc_step_scalars_get(void* ctx, fc_step_scalars* out);
 
 /* Per-anchor views of the last step for the local rows (host fp64 [Bl] each, may be NULL):
