@@ -135,6 +135,7 @@ struct PeerGather {
   unsigned long long* my_flag;        // local flag array [world]
   unsigned* ticket;                   // local grid-completion ticket
   int* err;
+  long long* dbg;                     // debug: globaltimer stamps {entry, stores done, flags out, peers in}
 };
 cudaError_t launch_peer_gather(const PeerGather& g, int blocks, cudaStream_t s);
 void* peer_gather_kernel_fn();

@@ -286,6 +286,10 @@ struct LossStep {
     if (const char* e = std::getenv("FC_FUSED_P1")) fused_p1 = fused_p1 && atoi(e) != 0;
     if (const char* e = std::getenv("FC_GEMM_DEBUG")) gemm_debug = atoi(e);
     if (sim_debug == 9 || gemm_debug >= 9) dbg_buf = dalloc<long long>(2 * 2688 + 160 * 16 + 8192);
+    if (dbg_buf && use_peer) {   // FC_SIM_DEBUG=9: gather stamps after the anchor / prep stamps
+      pg_e.dbg = dbg_buf + 2 * 2688 + 160 * 16 + 6000;
+      pg_p.dbg = pg_e.dbg + 4;
+    }
     if (debug_sync) use_graph = false;
     if (const char* e = std::getenv("FC_SHARED_Q")) shared_q = shared_q && atoi(e) != 0;
     FC_CUDA(fc::sim_set_smem());

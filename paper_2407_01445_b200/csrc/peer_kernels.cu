@@ -5,8 +5,9 @@
 // NCCL at creation). One kernel per gather: its CTAs store this rank's slice straight into
 // every rank's destination buffer over NVLink (16-byte stores, grid-strided), the last CTA to
 // finish (device-scope ticket) publishes a per-step sequence number into each peer's flag slot
-// for this rank (system-scope release) and then waits until every rank's flag in the LOCAL
-// flag array carries the same sequence number (system-scope acquire). The kernel therefore
+// for this rank (one system-scope release fence, then relaxed flag stores back to back) and
+// then waits until every rank's flag in the LOCAL flag array carries the same sequence number
+// (relaxed polling, then a system-scope acquire fence). The kernel therefore
 // completes only when the whole gathered buffer is in local HBM -- a stream-ordered all-gather
 // with no NCCL launch and no proxy thread (~20-30 us per NCCL gather on this system vs a few
 // microseconds of NVLink traffic for the payload and ~2.6 MB embedding slices).
@@ -20,18 +21,30 @@ namespace fc {
 
 namespace {
 
-__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
-  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+__device__ __forceinline__ void st_relaxed_sys(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
-__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
+__device__ __forceinline__ unsigned long long ld_relaxed_sys(const unsigned long long* p) {
   unsigned long long v;
-  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
   return v;
 }
 
+// release/acquire fence at system scope: orders this thread's (and, cumulatively, the CTA's
+// barrier-ordered) prior stores before its later ones for every observer, without the
+// sequential-consistency cost of fence.sc.sys (__threadfence_system)
+__device__ __forceinline__ void fence_acq_rel_sys() { asm volatile("fence.acq_rel.sys;" ::: "memory"); }
+
 }  // namespace
 
+__device__ __forceinline__ long long gtimer() {
+  long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
 __global__ void __launch_bounds__(256) peer_gather_kernel(PeerGather g) {
+  if (g.dbg && blockIdx.x == 0 && threadIdx.x == 0) g.dbg[0] = gtimer();
   // ---- this rank's slices -> every rank's destination (row offset rank * bytes) ----
   const size_t stride = static_cast<size_t>(gridDim.x) * blockDim.x;
   for (int t = 0; t < g.n_src; ++t) {
@@ -48,19 +61,24 @@ __global__ void __launch_bounds__(256) peer_gather_kernel(PeerGather g) {
   __shared__ bool last;
   __syncthreads();
   if (threadIdx.x == 0) {
-    __threadfence_system();   // this CTA's peer stores are visible system-wide
+    fence_acq_rel_sys();      // this CTA's peer stores (ordered by the barrier) before the ticket
     const unsigned ticket = atomicAdd(g.ticket, 1u);
     last = ticket == gridDim.x - 1;
   }
   __syncthreads();
   if (!last || threadIdx.x != 0) return;
   *g.ticket = 0u;             // re-arm for the next gather (stream order)
-  __threadfence_system();
-  for (int k = 0; k < g.world; ++k) st_release_sys(g.peer_flag[k] + g.rank, g.seq);
+  if (g.dbg) g.dbg[1] = gtimer();
+  // one release fence orders every CTA's stores (acquired through the ticket) before all the
+  // flag stores, which then go out back to back (a release per store would serialise them
+  // behind one NVLink round trip each)
+  fence_acq_rel_sys();
+  for (int k = 0; k < g.world; ++k) st_relaxed_sys(g.peer_flag[k] + g.rank, g.seq);
+  if (g.dbg) g.dbg[2] = gtimer();
   // wait for every rank's slice (bounded: a dead peer must not hang the GPU)
   for (int k = 0; k < g.world; ++k) {
     long long spins = 0;
-    while (ld_acquire_sys(g.my_flag + k) < g.seq) {
+    while (ld_relaxed_sys(g.my_flag + k) < g.seq) {
       __nanosleep(64);
       if (++spins > (1ll << 26)) {   // ~seconds: report instead of spinning forever
         *g.err = 12;                  // NcclError-class failure (collective aborted)
@@ -68,6 +86,8 @@ __global__ void __launch_bounds__(256) peer_gather_kernel(PeerGather g) {
       }
     }
   }
+  fence_acq_rel_sys();        // acquire: the peers' slices are read only after their flags
+  if (g.dbg) g.dbg[3] = gtimer();
 }
 
 cudaError_t launch_peer_gather(const PeerGather& g, int blocks, cudaStream_t s) {

@@ -1,0 +1,2 @@
+timeout -s KILL 400 python -m pytest tests/test_gpu_multirank.py -q -x --timeout 300 2>&1 | grep -E "^E |passed|failed" | head -5
+bash scripts/gpu_mr_timeline.sh | grep "rep 2"
