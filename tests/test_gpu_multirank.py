@@ -1,9 +1,9 @@
-"""Multi-GPU parity (K = 2 ranks, one process per GPU, NCCL): every rank runs the B200 step on
+"""Multi-GPU parity (K = 2 and 4 ranks, one process per GPU): every rank runs the B200 step on
 its contiguous slice of the global batch (trainer.cpp:231-241) and the rank outputs must equal
-the K = 2 oracle replay of trainer.cpp:427-589 on the whole batch -- the gathered-embedding
+the K-rank oracle replay of trainer.cpp:427-589 on the whole batch -- the gathered-embedding
 rows of dE, the all-reduced G_tau and tau update, the exact batch loss and, for the
-individual-temperature variants, the replicated IndividualTemp tables. Needs >= 2 GPUs
-(`gpurun --gpus 2`); skipped otherwise."""
+individual-temperature variants, the replicated IndividualTemp tables. Needs >= K GPUs
+(`gpurun --gpus 2` / `--gpus 4`); skipped otherwise."""
 import os
 import socket
 
@@ -15,9 +15,6 @@ from paper_2407_01445_b200 import synthetic as S
 
 pytestmark = pytest.mark.gpu
 
-K = 2
-
-
 def _free_port():
     s = socket.socket()
     s.bind(("127.0.0.1", 0))
@@ -26,7 +23,7 @@ def _free_port():
     return p
 
 
-def _worker(rank, variant, B, d, N, steps, nccl_id, q):
+def _worker(rank, K, variant, B, d, N, steps, nccl_id, q):
     import torch
     import paper_2407_01445_b200 as P
     from gpu_helpers import gpu_cfg, to_dev_bf16
@@ -56,7 +53,7 @@ def _worker(rank, variant, B, d, N, steps, nccl_id, q):
         q.put((rank, None, None, repr(e)))
 
 
-def _run(variant, B, d, N, steps):
+def _run(K, variant, B, d, N, steps):
     import torch
     import torch.multiprocessing as mp
     import paper_2407_01445_b200 as P
@@ -65,7 +62,7 @@ def _run(variant, B, d, N, steps):
     nccl_id = P.nccl_unique_id()
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    procs = [ctx.Process(target=_worker, args=(r, variant, B, d, N, steps, nccl_id, q)) for r in range(K)]
+    procs = [ctx.Process(target=_worker, args=(r, K, variant, B, d, N, steps, nccl_id, q)) for r in range(K)]
     for p in procs:
         p.start()
     res = {}
@@ -76,7 +73,7 @@ def _run(variant, B, d, N, steps):
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
-    # oracle: K = 2 replay on the whole batch
+    # oracle: K-rank replay on the whole batch
     ocfg = O.default_config(variant, N)
     st = O.new_state(ocfg)
     st.u1[:] = S.warm_u(N, 0)
@@ -98,10 +95,11 @@ def _norm_rel(a, b):
     return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
 
 
-@pytest.mark.parametrize("variant", ["fastclip_v3", "fastclip_v2", "fastclip_v1"])
-def test_two_ranks_match_oracle(variant):
-    B, d, N, steps = 512, 128, 4096, 2
-    res, refs, st = _run(variant, B, d, N, steps)
+@pytest.mark.parametrize("K,variant", [(2, "fastclip_v3"), (2, "fastclip_v2"), (2, "fastclip_v1"),
+                                       (4, "fastclip_v3"), (4, "fastclip_v2"), (4, "fastclip_v0")])
+def test_ranks_match_oracle(K, variant):
+    B, d, N, steps = 1024 if K == 4 else 512, 128, 8192, 2
+    res, refs, st = _run(K, variant, B, d, N, steps)
     Bl = B // K
     for s in range(steps):
         ref = refs[s]
