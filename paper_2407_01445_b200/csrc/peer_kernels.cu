@@ -50,11 +50,23 @@ __global__ void __launch_bounds__(256) peer_gather_kernel(PeerGather g) {
   for (int t = 0; t < g.n_src; ++t) {
     const size_t n16 = g.bytes[t] / 16;
     const uint4* src = reinterpret_cast<const uint4*>(g.src[t]);
-    for (size_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n16; i += stride) {
-      const uint4 v = src[i];
+    // four independent 16-byte loads in flight per thread before the stores: the copy is
+    // load-latency bound otherwise (one L2/HBM round trip per grid-stride step)
+    constexpr int kU = 4;
+    for (size_t i0 = blockIdx.x * blockDim.x + threadIdx.x; i0 < n16; i0 += kU * stride) {
+      uint4 v[kU];
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const size_t i = i0 + u * stride;
+        v[u] = i < n16 ? src[i] : make_uint4(0u, 0u, 0u, 0u);
+      }
 #pragma unroll 1
-      for (int k = 0; k < g.world; ++k)
-        reinterpret_cast<uint4*>(g.dst[t][k] + static_cast<size_t>(g.rank) * g.bytes[t])[i] = v;
+      for (int k = 0; k < g.world; ++k) {
+        uint4* dst = reinterpret_cast<uint4*>(g.dst[t][k] + static_cast<size_t>(g.rank) * g.bytes[t]);
+#pragma unroll
+        for (int u = 0; u < kU; ++u)
+          if (i0 + u * stride < n16) dst[i0 + u * stride] = v[u];
+      }
     }
   }
   // ---- grid completion: the last CTA publishes and waits ----

@@ -119,3 +119,18 @@ def test_ranks_match_oracle(K, variant):
         for name in names:
             got, ref_tab = tabs[name], getattr(st, name)
             assert np.max(np.abs(got - ref_tab) / np.maximum(np.abs(ref_tab), 1e-300)) < 1e-3, (variant, r, name)
+
+
+def test_nccl_fallback_matches_oracle(monkeypatch):
+    # FC_PEER=0: the NCCL all-gather / all-reduce path (used when GPUs cannot map each other's
+    # memory) gives the same results
+    monkeypatch.setenv("FC_PEER", "0")
+    B, d, N, steps = 512, 128, 8192, 2
+    res, refs, st = _run(2, "fastclip_v3", B, d, N, steps)
+    Bl = B // 2
+    for s in range(steps):
+        for r in range(2):
+            got, ref = res[r][0][s], refs[s]
+            assert _norm_rel(got["dE1"], ref["dE1"][r * Bl:(r + 1) * Bl]) < 2e-3
+            assert _norm_rel(got["dE2"], ref["dE2"][r * Bl:(r + 1) * Bl]) < 2e-3
+            assert _rel(got["loss"], ref["loss"]) < 1e-3 and _rel(got["tau"], ref["tau_new"]) < 1e-3
