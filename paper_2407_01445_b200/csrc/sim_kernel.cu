@@ -215,6 +215,45 @@ __device__ __forceinline__ void fused_fast(const uint32_t (&r)[32], float kap, f
   transpose_reduce2(x, zx, lane, cx, czx);
 }
 
+// 16-column version: the xor-halving over lane bits 3..0 leaves column (lane & 15)'s sum over
+// the 16 rows of the lane's half-warp, one more xor-16 step adds the other half (both lanes of
+// a pair then hold the full 32-row column sum).
+__device__ __forceinline__ void transpose_reduce2_16(float (&v)[16], float (&u)[16], uint32_t lane, float& sv,
+                                                     float& su) {
+#pragma unroll
+  for (int w = 8; w >= 1; w >>= 1) {
+    const bool upper = (lane & w) != 0;
+#pragma unroll
+    for (int k = 0; k < w; ++k) {
+      const float sv_ = upper ? v[k] : v[k + w];
+      const float kv = upper ? v[k + w] : v[k];
+      const float su_ = upper ? u[k] : u[k + w];
+      const float ku = upper ? u[k + w] : u[k];
+      v[k] = kv + __shfl_xor_sync(0xffffffffu, sv_, w);
+      u[k] = ku + __shfl_xor_sync(0xffffffffu, su_, w);
+    }
+  }
+  sv = v[0] + __shfl_xor_sync(0xffffffffu, v[0], 16);
+  su = u[0] + __shfl_xor_sync(0xffffffffu, u[0], 16);
+}
+
+__device__ __forceinline__ void fused_fast16(const uint32_t (&r)[16], float kap, float2& rx, float2& rzx, uint32_t lane,
+                                             float& cx, float& czx) {
+  const float2 k2 = f2(kap, kap);
+  float x[16], zx[16];
+#pragma unroll
+  for (int k = 0; k < 16; k += 2) {
+    const float2 z = __fmul2_rn(f2(__uint_as_float(r[k]), __uint_as_float(r[k + 1])), k2);
+    const float2 e = f2(ex2_approx(z.x), ex2_approx(z.y));
+    const float2 ze = __fmul2_rn(z, e);
+    rx = __fadd2_rn(rx, e);
+    rzx = __fadd2_rn(rzx, ze);
+    x[k] = e.x; x[k + 1] = e.y;
+    zx[k] = ze.x; zx[k + 1] = ze.y;
+  }
+  transpose_reduce2_16(x, zx, lane, cx, czx);
+}
+
 // FUSED exact path for one 8-column piece (rare: diagonal / ragged / clamp-capable chunks):
 // both exponentials with the safe_exp clamp, masks and clamp counts; the lanes of quarter q of
 // the warp get their column's exact {sum e, sum y e}.
@@ -311,7 +350,7 @@ __device__ __forceinline__ void q_chunk(const uint32_t (&r)[32], float rk, float
 // per-chunk working set (two 32-column transposes) fits the register file; the others run 16.
 template <int kMode>
 struct SimCfg {
-  static constexpr int kEpi = kMode == kSimFused ? 8 : kSimEpiWarps;
+  static constexpr int kEpi = kSimEpiWarps;
   static constexpr int kThreads = (kEpi + 2) * 32;
   static constexpr int kColsW = kPairN / (kEpi / 4);   // columns per epilogue warp
   static constexpr int kChunksW = kColsW / 32;
@@ -577,7 +616,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(SimCfg<kMode>::kThre
       // over all column groups (half the chunks per warp); STATS keeps its 64-column row
       // partials per warp, so there the groups past 128 columns idle
       const int tile_off = half < 0 ? 0 : half * (kPairN / 2);   // first column inside the 256-wide tile
-      constexpr bool kSpreadHalf = kMode != kSimStats;
+      constexpr bool kSpreadHalf = kMode != kSimStats && kMode != kSimFused;
       const int cols_w = (half >= 0 && kSpreadHalf) ? kColsW / 2 : kColsW;   // this warp's columns
       const int chunks_w = cols_w / 32;
       const bool active = static_cast<int>(cq) * cols_w < (half < 0 ? kPairN : kPairN / 2);
@@ -646,7 +685,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(SimCfg<kMode>::kThre
       // FUSED one-exponential form: 2^(s kappa) and 2^beta stay inside [2^-63, 2^63]
       const bool fused_ok = kMode == kSimFused && __all_sync(0xffffffffu, row_kap * smax <= kFactMaxLog2);
       // FUSED: [chunk][q4][32] column sums of this column group for the tile (parity buffer)
-      float2* red = reinterpret_cast<float2*>(L.par) + ((it & 1) * 2 + static_cast<int>(cq)) * (4 * 4 * 32);
+      float2* red = reinterpret_cast<float2*>(L.par) + ((it & 1) * (kEpi / 4) + static_cast<int>(cq)) * (kChunksW * 4 * 32);
       if (!active) {   // half tile, columns beyond it: hand the buffer back at once
         tc_fence_before();
         __syncwarp();
@@ -693,27 +732,44 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(SimCfg<kMode>::kThre
             if (h == q) cst = cst_all[q];
           const bool col_safe = !__any_sync(0xffffffffu, jc < sg.cols && fmaf(smax, cst.x, cst.y) > kClampLog2);
           const bool fast = p.fuse_fast && interior && warp_rows_ok && row_safe && col_safe && fused_ok;
-          uint32_t r32[32];
-          tmem_ld_32x32b_x32(taddr + 32 * h, r32);
-          tmem_ld_wait();
-          if (h == chunks_w - 1) {   // the tile is in registers: release the TMEM buffer
+          auto release_tmem = [&]() {   // the tile is in registers: release the TMEM buffer
             tc_fence_before();
             __syncwarp();
             if (lane == 0) {
               if (rank == 0) mbar_arrive(&L.tempty[acc]);
               else mbar_arrive_cluster(&L.tempty[acc], 0);
             }
-          }
+          };
           float ce = 0.f, cye = 0.f;
           if (fast) {
-            fused_fast(r32, rstat.x, se2, sye2, lane, ce, cye);
+            // two 16-column halves (x / z x of 16 columns stay within the 16-warp register
+            // budget); lanes 0-15 keep the first half's column sums, lanes 16-31 the second's
+            float c0x, c0zx, c1x, c1zx;
+            uint32_t r16[16];
+            tmem_ld_32x32b_x16(taddr + 32 * h, r16);
+            tmem_ld_wait();
+            fused_fast16(r16, rstat.x, se2, sye2, lane, c0x, c0zx);
+            tmem_ld_32x32b_x16(taddr + 32 * h + 16, r16);
+            tmem_ld_wait();
+            if (h == chunks_w - 1) release_tmem();
+            fused_fast16(r16, rstat.x, se2, sye2, lane, c1x, c1zx);
+            ce = lane < 16 ? c0x : c1x;
+            cye = lane < 16 ? c0zx : c1zx;
           } else {
+#pragma unroll 1
+            for (int hh = 0; hh < 2; ++hh) {
+              uint32_t r16[16];
+              tmem_ld_32x32b_x16(taddr + 32 * h + 16 * hh, r16);
+              tmem_ld_wait();
+              if (hh == 1 && h == chunks_w - 1) release_tmem();
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              uint32_t r8[8];
+              for (int q = 0; q < 2; ++q) {
+                uint32_t r8[8];
 #pragma unroll
-              for (int k = 0; k < 8; ++k) r8[k] = r32[8 * q + k];
-              fused_masked(r8, rstat, sg.col_stat, col0 + 8 * q, sg.cols, gi, row_ok, lane, q, se, sye, ncl, ce, cye);
+                for (int k = 0; k < 8; ++k) r8[k] = r16[8 * q + k];
+                fused_masked(r8, rstat, sg.col_stat, col0 + 16 * hh + 8 * q, sg.cols, gi, row_ok, lane, 2 * hh + q, se,
+                             sye, ncl, ce, cye);
+              }
             }
           }
           if (fast) {   // raw {sum x, sum z x} -> {sum e, sum y e} with 2^beta_j (|beta_j| <= 63)
