@@ -136,8 +136,10 @@ struct PeerGather {
   unsigned* ticket;                   // local grid-completion ticket
   int* err;
   long long* dbg;                     // debug: globaltimer stamps {entry, stores done, flags out, peers in}
+  int early_trigger;                  // release the next (programmatic) kernel at entry: it only
+                                      // reads the gathered data after griddepcontrol.wait
 };
-cudaError_t launch_peer_gather(const PeerGather& g, int blocks, cudaStream_t s);
+cudaError_t launch_peer_gather(const PeerGather& g, int blocks, int threads, cudaStream_t s);
 void* peer_gather_kernel_fn();
 
 enum SimMode { kSimStats = 0, kSimQ = 1, kSimRaw = 2, kSimFused = 3 };

@@ -311,6 +311,8 @@ struct LossStep {
                                  cudaSharedmemCarveoutMaxShared));
     FC_CUDA(cudaFuncSetAttribute(fc::fc_anchor_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
                                  cudaSharedmemCarveoutMaxShared));
+    FC_CUDA(cudaFuncSetAttribute(fc::peer_gather_kernel_fn(), cudaFuncAttributePreferredSharedMemoryCarveout,
+                                 cudaSharedmemCarveoutMaxShared));
     FC_CUDA(cudaFuncSetAttribute(fc::fc_indiv_update_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
                                  cudaSharedmemCarveoutMaxShared));
     mQ[0] = make_map(q, ldq, Bl, static_cast<uint64_t>(ldq) * 2, 64, 128);
@@ -640,7 +642,7 @@ struct LossStep {
         g.src[0] = reinterpret_cast<const uint8_t*>(E1);
         g.src[1] = reinterpret_cast<const uint8_t*>(E2);
         g.seq = seq;
-        FC_CUDA(fc::launch_peer_gather(g, n_sm, st));
+        FC_CUDA(fc::launch_peer_gather(g, n_sm, 256, st));
       } else {
         FC_NCCL(ncclGroupStart());
         FC_NCCL(ncclAllGather(E1, e1g, static_cast<size_t>(Bl) * d * 2, ncclUint8, comm, st));
@@ -723,7 +725,11 @@ struct LossStep {
         // other ranks' ids follows on the side branch)
         fc::PeerGather g = pg_p;
         g.seq = seq;
-        FC_CUDA(fc::launch_peer_gather(g, 64, st));
+        // pass 2 (programmatic launch) takes its SMs while the payload moves: its first tile's
+        // operands and MMAs need only E; parameters are loaded after griddepcontrol.wait.
+        // 128-thread blocks fit beside a pass-2 CTA's register file
+        g.early_trigger = pdl && !timing ? 1 : 0;
+        FC_CUDA(fc::launch_peer_gather(g, 128, 128, st));
       } else {
         FC_NCCL(ncclAllGather(send, recv, static_cast<size_t>(pstride), ncclFloat64, comm, st));
         a.weights_replica_only = 0;

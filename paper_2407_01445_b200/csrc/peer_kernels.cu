@@ -45,6 +45,7 @@ __device__ __forceinline__ long long gtimer() {
 
 __global__ void __launch_bounds__(256) peer_gather_kernel(PeerGather g) {
   if (g.dbg && blockIdx.x == 0 && threadIdx.x == 0) g.dbg[0] = gtimer();
+  if (g.early_trigger) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   // ---- this rank's slices -> every rank's destination (row offset rank * bytes) ----
   const size_t stride = static_cast<size_t>(gridDim.x) * blockDim.x;
   for (int t = 0; t < g.n_src; ++t) {
@@ -102,8 +103,8 @@ __global__ void __launch_bounds__(256) peer_gather_kernel(PeerGather g) {
   if (g.dbg) g.dbg[3] = gtimer();
 }
 
-cudaError_t launch_peer_gather(const PeerGather& g, int blocks, cudaStream_t s) {
-  peer_gather_kernel<<<blocks, 256, 0, s>>>(g);
+cudaError_t launch_peer_gather(const PeerGather& g, int blocks, int threads, cudaStream_t s) {
+  peer_gather_kernel<<<blocks, threads, 0, s>>>(g);
   return cudaGetLastError();
 }
 
