@@ -138,8 +138,10 @@ struct PeerGather {
   long long* dbg;                     // debug: globaltimer stamps {entry, stores done, flags out, peers in}
   int early_trigger;                  // release the next (programmatic) kernel at entry: it only
                                       // reads the gathered data after griddepcontrol.wait
+  int wait_src;                       // programmatic launch: sources >= wait_src are written by the
+                                      // preceding kernel (griddepcontrol.wait first); -1: none
 };
-cudaError_t launch_peer_gather(const PeerGather& g, int blocks, int threads, cudaStream_t s);
+cudaError_t launch_peer_gather(const PeerGather& g, int blocks, int threads, cudaStream_t s, bool pdl = false);
 void* peer_gather_kernel_fn();
 
 enum SimMode { kSimStats = 0, kSimQ = 1, kSimRaw = 2, kSimFused = 3 };

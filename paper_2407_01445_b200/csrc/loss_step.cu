@@ -642,7 +642,11 @@ struct LossStep {
         g.src[0] = reinterpret_cast<const uint8_t*>(E1);
         g.src[1] = reinterpret_cast<const uint8_t*>(E2);
         g.seq = seq;
-        FC_CUDA(fc::launch_peer_gather(g, n_sm, 256, st));
+        // programmatic launch after the local prep: the E slices go out while prep runs; the
+        // bounds slot (source 2, prep's norm maxima) is sent after griddepcontrol.wait. Pass 1
+        // waits for this grid, which completes only after prep did.
+        g.wait_src = 2;
+        FC_CUDA(fc::launch_peer_gather(g, n_sm, 256, st, pdl && !timing));
       } else {
         FC_NCCL(ncclGroupStart());
         FC_NCCL(ncclAllGather(E1, e1g, static_cast<size_t>(Bl) * d * 2, ncclUint8, comm, st));
@@ -729,6 +733,7 @@ struct LossStep {
         // operands and MMAs need only E; parameters are loaded after griddepcontrol.wait.
         // 128-thread blocks fit beside a pass-2 CTA's register file
         g.early_trigger = pdl && !timing ? 1 : 0;
+        g.wait_src = -1;
         FC_CUDA(fc::launch_peer_gather(g, 128, 128, st));
       } else {
         FC_NCCL(ncclAllGather(send, recv, static_cast<size_t>(pstride), ncclFloat64, comm, st));

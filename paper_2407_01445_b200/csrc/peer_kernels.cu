@@ -49,6 +49,7 @@ __global__ void __launch_bounds__(256) peer_gather_kernel(PeerGather g) {
   // ---- this rank's slices -> every rank's destination (row offset rank * bytes) ----
   const size_t stride = static_cast<size_t>(gridDim.x) * blockDim.x;
   for (int t = 0; t < g.n_src; ++t) {
+    if (t == g.wait_src) asm volatile("griddepcontrol.wait;" ::: "memory");   // the predecessor's outputs
     const size_t n16 = g.bytes[t] / 16;
     const uint4* src = reinterpret_cast<const uint4*>(g.src[t]);
     // four independent 16-byte loads in flight per thread before the stores: the copy is
@@ -103,9 +104,18 @@ __global__ void __launch_bounds__(256) peer_gather_kernel(PeerGather g) {
   if (g.dbg) g.dbg[3] = gtimer();
 }
 
-cudaError_t launch_peer_gather(const PeerGather& g, int blocks, int threads, cudaStream_t s) {
-  peer_gather_kernel<<<blocks, threads, 0, s>>>(g);
-  return cudaGetLastError();
+cudaError_t launch_peer_gather(const PeerGather& g, int blocks, int threads, cudaStream_t s, bool pdl) {
+  cudaLaunchConfig_t cfg{};
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
+  cfg.gridDim = dim3(blocks, 1, 1);
+  cfg.blockDim = dim3(threads, 1, 1);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = s;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, peer_gather_kernel, g);
 }
 
 void* peer_gather_kernel_fn() { return reinterpret_cast<void*>(peer_gather_kernel); }
