@@ -75,10 +75,6 @@ struct SimParams {
   int n_bounds;                // the maxima over G are the max over the slots (clamp-free fast paths)
   int q_factor;                // Q: one shared temperature -> factorized single-exponential fast path
   int split_tail;              // leftover tiles (T mod pairs) run as 256 x 128 halves on twice the pairs
-  // STATS pass prologue (idle epilogue warps): zero the step's gradient outputs, which the
-  // gradient GEMM later accumulates into with TMA reduce-add
-  float4* zero_a; float4* zero_b;          // nullptr: nothing to zero
-  long long zero_n4;                       // float4 count of each
   // FUSED: column statistics {sum e, sum y e} per (row slot = one CTA of a pair row block,
   // column), laid out [cols / 32][n_slots][32] with n_slots = 2 per pair row block (the CTA's
   // four 32-row warp sums are added in shared memory); fuse_fast enables the one-exponential path

@@ -681,7 +681,6 @@ struct LossStep {
     sp.n_bounds = K;
     sp.debug = sim_debug;
     sp.split_tail = split_tail ? 1 : 0;
-    sp.zero_a = sp.zero_b = nullptr;
     if (sim_debug == 9) sp.dbg_out = dbg_buf;
     CUtensorMap mA[2] = {mE1k, mE2k}, mB[2] = {mE2k, mE1k};
     mark(2, st);
@@ -779,7 +778,6 @@ struct LossStep {
     }
     if (sim_debug == 9) sp.dbg_out = dbg_buf + 2688;
     sp.q_factor = (!indiv && q_factor) ? 1 : 0;   // one shared temperature: single-exponential Q
-    sp.zero_a = sp.zero_b = nullptr;
     FC_CUDA(fc::launch_sim(fc::kSimQ, sp, mA, mB, mQo, pair_grid(sp.n_items), st, nullptr, pdl && !timing));
 
     // ---- pass 2b: dE = c (Q' E - r o E_local) ----

@@ -175,49 +175,9 @@ __device__ __forceinline__ float transpose_reduce(float (&v)[N], uint32_t lane) 
   return v[0];
 }
 
-// Two arrays reduced in lock-step (twice the independent shuffles per halving step).
-__device__ __forceinline__ void transpose_reduce2(float (&v)[32], float (&u)[32], uint32_t lane, float& sv, float& su) {
-#pragma unroll
-  for (int w = 16; w >= 1; w >>= 1) {
-    const bool upper = (lane & w) != 0;
-#pragma unroll
-    for (int k = 0; k < w; ++k) {
-      const float sv_ = upper ? v[k] : v[k + w];
-      const float kv = upper ? v[k + w] : v[k];
-      const float su_ = upper ? u[k] : u[k + w];
-      const float ku = upper ? u[k + w] : u[k];
-      v[k] = kv + __shfl_xor_sync(0xffffffffu, sv_, w);
-      u[k] = ku + __shfl_xor_sync(0xffffffffu, su_, w);
-    }
-  }
-  sv = v[0];
-  su = u[0];
-}
-
-// FUSED fast path (one temperature, no clamp possible, no diagonal / ragged element in the
-// chunk): x = 2^(s kappa) once per element serves the row (R) and the column (C) statistics,
-// e_row = 2^beta_i x, e_col = 2^beta_j x. Row raw sums {sum x, sum z x} (z = s kappa)
-// accumulate per thread; lane c gets column c's raw sums from the transposed reductions.
-__device__ __forceinline__ void fused_fast(const uint32_t (&r)[32], float kap, float2& rx, float2& rzx, uint32_t lane,
-                                           float& cx, float& czx) {
-  const float2 k2 = f2(kap, kap);
-  float x[32], zx[32];
-#pragma unroll
-  for (int k = 0; k < 32; k += 2) {
-    const float2 z = __fmul2_rn(f2(__uint_as_float(r[k]), __uint_as_float(r[k + 1])), k2);
-    const float2 e = f2(ex2_approx(z.x), ex2_approx(z.y));
-    const float2 ze = __fmul2_rn(z, e);
-    rx = __fadd2_rn(rx, e);
-    rzx = __fadd2_rn(rzx, ze);
-    x[k] = e.x; x[k + 1] = e.y;
-    zx[k] = ze.x; zx[k + 1] = ze.y;
-  }
-  transpose_reduce2(x, zx, lane, cx, czx);
-}
-
-// 16-column version: the xor-halving over lane bits 3..0 leaves column (lane & 15)'s sum over
-// the 16 rows of the lane's half-warp, one more xor-16 step adds the other half (both lanes of
-// a pair then hold the full 32-row column sum).
+// Column sums of two 32 x 16 register tiles in lock-step (lane = row): the xor-halving over
+// lane bits 3..0 leaves column (lane & 15)'s sum over the 16 rows of the lane's half-warp, one
+// more xor-16 step adds the other half (both lanes of a pair then hold the full column sum).
 __device__ __forceinline__ void transpose_reduce2_16(float (&v)[16], float (&u)[16], uint32_t lane, float& sv,
                                                      float& su) {
 #pragma unroll
@@ -237,6 +197,10 @@ __device__ __forceinline__ void transpose_reduce2_16(float (&v)[16], float (&u)[
   su = u[0] + __shfl_xor_sync(0xffffffffu, u[0], 16);
 }
 
+// FUSED fast path (one temperature, no clamp possible, no diagonal / ragged element in the
+// chunk): x = 2^(s kappa) once per element serves the row (R) and the column (C) statistics,
+// e_row = 2^beta_i x, e_col = 2^beta_j x. Row raw sums {sum x, sum z x} (z = s kappa)
+// accumulate per thread; lane c (c < 16) or c + 16 (c >= 16) gets that column's raw sums of the 16-column half.
 __device__ __forceinline__ void fused_fast16(const uint32_t (&r)[16], float kap, float2& rx, float2& rzx, uint32_t lane,
                                              float& cx, float& czx) {
   const float2 k2 = f2(kap, kap);
@@ -590,18 +554,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(SimCfg<kMode>::kThre
   } else {
     // ===================== epilogue (both CTAs) =====================
     griddep_wait();   // row / column parameters and bounds come from the preceding kernel
-    if constexpr (kStatsLike) {
-      // While the first tiles load and multiply (two TMEM buffers of slack), the epilogue
-      // warps zero this CTA's slice of the gradient outputs for the GEMM of this step.
-      if (p.zero_a) {
-        const long long nthr = static_cast<long long>(gridDim.x) * kEpi * 32;
-        const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
-        for (long long g = blockIdx.x * (kEpi * 32) + threadIdx.x; g < p.zero_n4; g += nthr) {
-          p.zero_a[g] = z;
-          p.zero_b[g] = z;
-        }
-      }
-    }
     const uint32_t q4 = warp & 3;               // TMEM lane quarter accessible to this warp
     long long e_wait = 0, e_ld = 0, e_math = 0, e_t0 = clock64(), e_g0 = 0;
     const bool eprof = p.debug == 9 && warp == 5;
