@@ -161,6 +161,19 @@ int fc_kernels_per_step(void* ctx);
 int fc_debug_similarity(const void* a, const void* b, int32_t rows, int32_t cols, int32_t dim,
                         float* out, void* stream);
 
+/* Per-function entry point for parity / a stateless caller: engine::g_values
+ * (engine.cpp:151-176) and, when dsum1/dsum2 are non-NULL, engine::dtau_sums (engine.cpp:182-204)
+ * for the local slice [local_begin, local_begin + local_count) of a global batch, computed by the
+ * step's tcgen05 pass-1 kernel. e1g/e2g: (device) bf16 [batch x dim]; t1/t2_local: (device) fp64
+ * [local_count] (tau^t of the local anchors; dtau_sums' t is the same per-anchor value,
+ * engine.cpp:198-199); outputs (device) fp64 [local_count]; clamps: (device, may be NULL) the
+ * number of safe_exp clamps among the evaluated exponentials (losses.cpp:10). Asynchronous on
+ * `stream`. Errors: FC_ERR_DEGENERATE_BATCH (batch < 2), FC_ERR_SHAPE (slice outside the batch,
+ * engine.cpp:11-19), FC_ERR_UNSUPPORTED (dim % 8 != 0). */
+int fc_g_values(const void* e1g, const void* e2g, int32_t batch, int32_t dim, const double* t1_local,
+                const double* t2_local, int32_t local_begin, int32_t local_count, double* g1, double* g2,
+                double* dsum1, double* dsum2, uint64_t* clamps, void* stream);
+
 const char* fc_last_error(void);
 
 #ifdef __cplusplus

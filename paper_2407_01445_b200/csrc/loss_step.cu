@@ -1162,4 +1162,74 @@ int fc_debug_similarity(const void* a, const void* b, int32_t rows, int32_t cols
   });
 }
 
+// engine::g_values (engine.cpp:151-176) and engine::dtau_sums (engine.cpp:182-204) for the
+// local slice [local_begin, local_begin + local_count) of a global batch, on the step's pass-1
+// kernel (segments R = S[L,G] and C = S^T[L,G], safe_exp in the log2 domain). Stateless:
+// workspaces come from the stream-ordered allocator and are released on the same stream.
+int fc_g_values(const void* e1g, const void* e2g, int32_t batch, int32_t dim, const double* t1_local,
+                const double* t2_local, int32_t local_begin, int32_t local_count, double* g1, double* g2,
+                double* dsum1, double* dsum2, uint64_t* clamps, void* stream) {
+  return guarded([&] {
+    if (batch < 2) throw FcError{FC_ERR_DEGENERATE_BATCH, "g_values: global batch must have >= 2 pairs"};
+    if (local_begin < 0 || local_count <= 0 || local_begin + local_count > batch)
+      throw FcError{FC_ERR_SHAPE, "g_values: local slice outside the global batch"};
+    if (dim < 8 || dim % 8 != 0) throw FcError{FC_ERR_UNSUPPORTED, "dim must be a positive multiple of 8"};
+    if (!e1g || !e2g || !t1_local || !t2_local || !g1 || !g2 || (!dsum1) != (!dsum2))
+      throw FcError{FC_ERR_SHAPE, "g_values: null pointer"};
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const int B = batch, d = dim, lo = local_begin, cnt = local_count;
+    const int n_jt = (B + fc::kPairN - 1) / fc::kPairN;
+    const int nparts = n_jt * 4;
+    const size_t part_bytes = static_cast<size_t>(cnt) * nparts * sizeof(float2);
+    uint8_t* ws = nullptr;
+    const size_t ws_bytes = 2 * part_bytes + 2 * cnt * sizeof(float2) + 64;
+    FC_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&ws), ws_bytes, st));
+    float2* pR = reinterpret_cast<float2*>(ws);
+    float2* pC = reinterpret_cast<float2*>(ws + part_bytes);
+    float2* rsR = reinterpret_cast<float2*>(ws + 2 * part_bytes);
+    float2* rsC = rsR + cnt;
+    float* bnd = reinterpret_cast<float*>(rsC + cnt);
+    unsigned long long* ncl = reinterpret_cast<unsigned long long*>(bnd + 4);
+    FC_CUDA(cudaMemsetAsync(bnd, 0, 4 * sizeof(float) + sizeof(unsigned long long), st));
+    fc::fc_rows_kernel<<<(B * 32 + 127) / 128, 128, 0, st>>>(static_cast<const __nv_bfloat16*>(e1g),
+                                                            static_cast<const __nv_bfloat16*>(e2g), B, d, lo, cnt,
+                                                            t1_local, t2_local, rsR, rsC, bnd);
+    FC_CUDA(cudaGetLastError());
+    const uint64_t rb = static_cast<uint64_t>(d) * 2;
+    CUtensorMap m1 = make_map(e1g, d, B, rb, 64, 128), m2 = make_map(e2g, d, B, rb, 64, 128);
+    fc::SimParams sp{};
+    sp.nseg = 2;
+    sp.d = d;
+    sp.n_jt = n_jt;
+    for (int s = 0; s < 2; ++s) {
+      fc::SimSeg& g = sp.seg[s];
+      g.rows = cnt;
+      g.a_row0 = lo;
+      g.cols = B;
+      g.row_stat = s ? rsC : rsR;
+      g.partial = s ? pC : pR;
+      sp.n_rb[s] = (cnt + fc::kPairM - 1) / fc::kPairM;
+    }
+    sp.n_items = (sp.n_rb[0] + sp.n_rb[1]) * n_jt;
+    sp.clamps = ncl;
+    sp.bounds = bnd;
+    sp.n_bounds = 1;
+    int dev = 0;
+    FC_CUDA(cudaGetDevice(&dev));
+    static bool smem_set = false;
+    if (!smem_set) {
+      FC_CUDA(fc::sim_set_smem());
+      smem_set = true;
+    }
+    CUtensorMap mA[2] = {m1, m2}, mB[2] = {m2, m1};
+    const int pairs = std::max(1, std::min(sm_count(dev) / 2, sp.n_items));
+    FC_CUDA(fc::launch_sim(fc::kSimStats, sp, mA, mB, nullptr, pairs * 2, st, nullptr));
+    fc::fc_gsum_kernel<<<(cnt + 127) / 128, 128, 0, st>>>(pR, pC, nparts, cnt, B, rsR, rsC, t1_local, t2_local, g1, g2,
+                                                         dsum1, dsum2);
+    FC_CUDA(cudaGetLastError());
+    if (clamps) FC_CUDA(cudaMemcpyAsync(clamps, ncl, sizeof(uint64_t), cudaMemcpyDeviceToDevice, st));
+    FC_CUDA(cudaFreeAsync(ws, st));
+  });
+}
+
 }  // extern "C"

@@ -345,3 +345,69 @@ __global__ void fc_indiv_update_kernel(StepArgs a) {
 }
 
 }  // namespace fc
+
+namespace fc {
+
+// ---- stateless engine entry points (fc_g_values): engine::g_values + dtau_sums ----
+
+// Warp per global row w of [0, B): norm maxima of E1 / E2 rows into bounds[0..1] (the
+// similarity kernel's clamp-free fast-path test); rows of the local slice [lo, lo + cnt) also
+// get S_ww and their pass-1 row parameters {kappa = log2(e)/t, beta = -S_ww kappa} at the
+// caller's temperatures (engine.cpp:151-176 takes t per local anchor).
+__global__ void fc_rows_kernel(const __nv_bfloat16* __restrict__ e1, const __nv_bfloat16* __restrict__ e2, int B,
+                               int d, int lo, int cnt, const double* __restrict__ t1, const double* __restrict__ t2,
+                               float2* rowstat_R, float2* rowstat_C, float* bounds) {
+  const int w = (blockIdx.x * blockDim.x + threadIdx.x) / 32;
+  const int lane = threadIdx.x & 31;
+  float acc = 0.f, n1 = 0.f, n2 = 0.f;
+  if (w < B) {
+    const __nv_bfloat162* x = reinterpret_cast<const __nv_bfloat162*>(e1 + static_cast<size_t>(w) * d);
+    const __nv_bfloat162* y = reinterpret_cast<const __nv_bfloat162*>(e2 + static_cast<size_t>(w) * d);
+    for (int k = lane; k < d / 2; k += 32) {
+      const float2 fx = __bfloat1622float2(x[k]), fy = __bfloat1622float2(y[k]);
+      acc = fmaf(fx.x, fy.x, fmaf(fx.y, fy.y, acc));
+      n1 = fmaf(fx.x, fx.x, fmaf(fx.y, fx.y, n1));
+      n2 = fmaf(fy.x, fy.x, fmaf(fy.y, fy.y, n2));
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    n1 += __shfl_xor_sync(0xffffffffu, n1, o);
+    n2 += __shfl_xor_sync(0xffffffffu, n2, o);
+  }
+  if (lane != 0 || w >= B) return;
+  atomicMax(reinterpret_cast<int*>(bounds) + 0, __float_as_int(n1));   // non-negative floats order like ints
+  atomicMax(reinterpret_cast<int*>(bounds) + 1, __float_as_int(n2));
+  const int r = w - lo;
+  if (r < 0 || r >= cnt) return;
+  const float k1 = static_cast<float>(kLog2eD / t1[r]), k2 = static_cast<float>(kLog2eD / t2[r]);
+  rowstat_R[r] = make_float2(k1, -acc * k1);
+  rowstat_C[r] = make_float2(k2, -acc * k2);
+}
+
+// Thread per local row: fixed-order fp64 sum of the row's pass-1 partials of both segments ->
+// g = sum e / (B-1) (engine.cpp:176) and dsum = -(sum (s - S_ii) e) / (t^2 (B-1))
+// (engine.cpp:198-205; pass 1 accumulates y e with y = (s - S_ii) kappa).
+__global__ void fc_gsum_kernel(const float2* __restrict__ pR, const float2* __restrict__ pC, int nparts, int cnt,
+                               int B, const float2* __restrict__ rsR, const float2* __restrict__ rsC,
+                               const double* __restrict__ t1, const double* __restrict__ t2, double* g1, double* g2,
+                               double* ds1, double* ds2) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= cnt) return;
+  double s1 = 0.0, x1 = 0.0, s2 = 0.0, x2 = 0.0;
+  for (int q = 0; q < nparts; ++q) {
+    const float2 a = pR[static_cast<size_t>(r) * nparts + q], b = pC[static_cast<size_t>(r) * nparts + q];
+    s1 += a.x; x1 += a.y; s2 += b.x; x2 += b.y;
+  }
+  const double inv = 1.0 / static_cast<double>(B - 1);
+  g1[r] = s1 * inv;
+  g2[r] = s2 * inv;
+  if (ds1) {
+    const double d1 = x1 / static_cast<double>(rsR[r].x), d2 = x2 / static_cast<double>(rsC[r].x);
+    ds1[r] = (-(d1 / (t1[r] * t1[r]))) * inv;
+    ds2[r] = (-(d2 / (t2[r] * t2[r]))) * inv;
+  }
+}
+
+}  // namespace fc

@@ -90,5 +90,12 @@ __global__ void fc_anchor_kernel(StepArgs a);
 __global__ void fc_zero_kernel(float4* a0, float4* a1, long long n4);
 __global__ void fc_reduce_kernel(StepArgs a);
 __global__ void fc_indiv_update_kernel(StepArgs a);
+__global__ void fc_rows_kernel(const __nv_bfloat16* __restrict__ e1, const __nv_bfloat16* __restrict__ e2, int B,
+                               int d, int lo, int cnt, const double* __restrict__ t1, const double* __restrict__ t2,
+                               float2* rowstat_R, float2* rowstat_C, float* bounds);
+__global__ void fc_gsum_kernel(const float2* __restrict__ pR, const float2* __restrict__ pC, int nparts, int cnt,
+                               int B, const float2* __restrict__ rsR, const float2* __restrict__ rsC,
+                               const double* __restrict__ t1, const double* __restrict__ t2, double* g1, double* g2,
+                               double* ds1, double* ds2);
 
 }  // namespace fc

@@ -102,6 +102,7 @@ def lib():
         L.fc_set_phase_timing.argtypes = [P, I32]
         L.fc_phase_times.argtypes = [P, I32, C.POINTER(C.c_float), I32]
         L.fc_debug_similarity.argtypes = [P, P, I32, I32, I32, P, P]
+        L.fc_g_values.argtypes = [P, P, I32, I32, P, P, I32, I32, P, P, P, P, P, P]
         L.fc_last_error.restype = C.c_char_p
         _lib = L
     return _lib
@@ -111,7 +112,7 @@ EXPORTED = [
     "fc_config_defaults", "fc_gamma_at", "fc_epsilon_at", "fc_nccl_unique_id", "fc_create",
     "fc_destroy", "fc_loss_step", "fc_step_scalars_get", "fc_local_views", "fc_table_download",
     "fc_table_upload", "fc_tau_state_get", "fc_tau_state_set", "fc_kernels_per_step",
-    "fc_debug_similarity", "fc_last_error", "fc_set_phase_timing", "fc_phase_times",
+    "fc_debug_similarity", "fc_last_error", "fc_set_phase_timing", "fc_phase_times", "fc_g_values",
 ]
 PHASES = ["allgather_e", "prep", "pass1_stats", "tables_tau", "pass2_q", "grad_gemm"]
 
@@ -269,6 +270,31 @@ class LossStep:
 
     def set_tau_state(self, tau: float, m: float = 0.0, v: float = 0.0, step: int = 0, latched: int = 0):
         _check(lib().fc_tau_state_set(self._h, tau, m, v, step, latched))
+
+
+def g_values(e1g, e2g, t1_local, t2_local, local_begin: int, local_count: int, dtau_sums: bool = True):
+    """engine::g_values (engine.cpp:151-176) [+ engine::dtau_sums (engine.cpp:182-204)] for the
+    local slice [local_begin, local_begin + local_count) of the global batch (e1g / e2g: CUDA bf16
+    [B, d]; t1/t2_local: CUDA fp64 [local_count]) through the step's tcgen05 pass-1 kernel.
+    Returns {"g1", "g2"[, "dsum1", "dsum2"], "clamps"} (CUDA fp64 tensors, clamps a Python int)."""
+    import torch
+    B, d = e1g.shape
+    for name, x in (("e1g", e1g), ("e2g", e2g)):
+        if x.dtype != torch.bfloat16 or not x.is_cuda or not x.is_contiguous() or tuple(x.shape) != (B, d):
+            raise FastclipError(2, f"{name} must be a contiguous CUDA bf16 tensor of shape ({B}, {d})")
+    t1 = t1_local.to(device=e1g.device, dtype=torch.float64).contiguous()
+    t2 = t2_local.to(device=e1g.device, dtype=torch.float64).contiguous()
+    if t1.numel() != local_count or t2.numel() != local_count:
+        raise FastclipError(2, f"t1/t2_local must have {local_count} entries")
+    out = {k: torch.empty(local_count, device=e1g.device, dtype=torch.float64)
+           for k in (("g1", "g2", "dsum1", "dsum2") if dtau_sums else ("g1", "g2"))}
+    ncl = torch.zeros(1, device=e1g.device, dtype=torch.int64)
+    stream = torch.cuda.current_stream(e1g.device)
+    _check(lib().fc_g_values(_dptr(e1g), _dptr(e2g), B, d, _dptr(t1), _dptr(t2), int(local_begin), int(local_count),
+                             _dptr(out["g1"]), _dptr(out["g2"]), _dptr(out["dsum1"]) if dtau_sums else None,
+                             _dptr(out["dsum2"]) if dtau_sums else None, _dptr(ncl), C.c_void_p(stream.cuda_stream)))
+    out["clamps"] = int(ncl.item())
+    return out
 
 
 def debug_similarity(a, b):

@@ -1,0 +1,68 @@
+"""Per-function entry point fc_g_values (engine::g_values, engine.cpp:151-176, and
+engine::dtau_sums, engine.cpp:182-204) on the step's tcgen05 pass-1 kernel vs the oracle's
+oc_g_values / oc_dtau_sums on the same bf16 inputs: max relative error <= 1e-3, clamp counts
+equal to the oracle's (within the fp32-vs-fp64 rounding of exponents that sit on the clamp)."""
+import ctypes as C
+
+import numpy as np
+import pytest
+
+import oracle as O
+from gpu_helpers import to_dev_bf16
+from paper_2407_01445_b200 import synthetic as S
+
+pytestmark = pytest.mark.gpu
+
+
+def _oracle(E1, E2, t1, t2, lo, cnt):
+    L = O.lib("oracle")
+    DP = C.POINTER(C.c_double)
+    for f in ("oc_g_values", "oc_dtau_sums"):
+        getattr(L, f).argtypes = [C.c_int, C.c_int, DP, DP, DP, DP, C.c_int, C.c_int, DP, DP]
+    B, d = E1.shape
+    p = lambda a: a.ctypes.data_as(DP)
+    g1, g2, d1, d2 = (np.zeros(cnt) for _ in range(4))
+    L.oc_reset_exp_clamp_count()
+    assert L.oc_g_values(B, d, p(E1), p(E2), p(t1), p(t2), lo, cnt, p(g1), p(g2)) == 0
+    clamps = L.oc_exp_clamp_count()
+    # dtau_sums indexes t by the GLOBAL row (engine.cpp:198-199): pass t over G with the local
+    # slice's values at [lo, lo + cnt)
+    T1, T2 = np.ones(B), np.ones(B)
+    T1[lo:lo + cnt], T2[lo:lo + cnt] = t1, t2
+    assert L.oc_dtau_sums(B, d, p(E1), p(E2), p(T1), p(T2), lo, cnt, p(d1), p(d2)) == 0
+    return dict(g1=g1, g2=g2, dsum1=d1, dsum2=d2, clamps=clamps)
+
+
+def _rel(a, b):
+    return float(np.max(np.abs(a - b) / np.maximum(np.abs(b), 1e-300)))
+
+
+@pytest.mark.parametrize("B,d,lo,cnt,tmin,tmax", [
+    (600, 200, 128, 256, 0.02, 0.1),     # ragged B, a slice in the middle, individual temperatures
+    (512, 128, 0, 512, 0.07, 0.07),      # the whole batch at one temperature (K = 1 shape)
+    (384, 64, 300, 84, 0.005, 0.01),     # tau near the floor: safe_exp clamps are hit
+])
+def test_g_values_match_oracle(B, d, lo, cnt, tmin, tmax):
+    import torch
+    import paper_2407_01445_b200 as P
+    b1, b2 = S.embeddings(B, d, 31)
+    rng = np.random.default_rng(5)
+    t1 = rng.uniform(tmin, tmax, cnt)
+    t2 = rng.uniform(tmin, tmax, cnt)
+    got = P.g_values(to_dev_bf16(b1), to_dev_bf16(b2), torch.from_numpy(t1).cuda(), torch.from_numpy(t2).cuda(), lo, cnt)
+    ref = _oracle(S.bf16_to_f32(b1).astype(np.float64), S.bf16_to_f32(b2).astype(np.float64), t1, t2, lo, cnt)
+    for k in ("g1", "g2", "dsum1", "dsum2"):
+        assert _rel(got[k].cpu().numpy(), ref[k]) < 1e-3, k
+    assert got["clamps"] == pytest.approx(ref["clamps"], rel=0.02, abs=2)
+    if tmin <= 0.005:
+        assert ref["clamps"] > 0
+
+
+def test_g_values_rejects_bad_slices():
+    import torch
+    import paper_2407_01445_b200 as P
+    b1, b2 = S.embeddings(64, 16, 1)
+    t = torch.full((32,), 0.05, dtype=torch.float64, device="cuda")
+    with pytest.raises(P.FastclipError) as e:
+        P.g_values(to_dev_bf16(b1), to_dev_bf16(b2), t, t, 48, 32)   # slice past the batch
+    assert e.value.code == 2
