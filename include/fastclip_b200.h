@@ -174,6 +174,16 @@ int fc_g_values(const void* e1g, const void* e2g, int32_t batch, int32_t dim, co
                 const double* t2_local, int32_t local_begin, int32_t local_count, double* g1, double* g2,
                 double* dsum1, double* dsum2, uint64_t* clamps, void* stream);
 
+/* Per-function entry point: engine::embedding_cotangents (engine.cpp:77-121) for the local
+ * slice [local_begin, local_begin + local_count) of a global batch with the caller's PairWeights
+ * (engine.hpp:29-32) over G: w1, w2, t1, t2 (device) fp64 [batch]. e1g/e2g: (device) bf16
+ * [batch x dim]; de1/de2: (device) fp32 [local_count x dim], overwritten (scale 1/(local_count
+ * (batch-1)), engine.cpp:84-85). Runs the step's pass-1, pass-2 and gradient-GEMM kernels;
+ * asynchronous on `stream`. Errors as fc_g_values. */
+int fc_embedding_cotangents(const void* e1g, const void* e2g, int32_t batch, int32_t dim, const double* w1,
+                            const double* w2, const double* t1, const double* t2, int32_t local_begin,
+                            int32_t local_count, float* de1, float* de2, void* stream);
+
 const char* fc_last_error(void);
 
 #ifdef __cplusplus

@@ -95,6 +95,41 @@ int sm_count(int dev) {
 
 bool is_individual(int v) { return v == FC_ISOGCLR || v == FC_FASTCLIP_V2; }
 
+// Contiguous stream-K ranges over the (tile, k-block) sequence with equal estimated cost
+// per cluster: k-blocks + kDrain per unit (each unit ends in a full-tile epilogue that the
+// single TMEM accumulator cannot overlap). Greedy fill against a binary-searched budget.
+static void balance_stream_k(fc::GemmParams& gp, int n_clusters, int gemm_drain) {
+  const long long KB = gp.kb_total, U = static_cast<long long>(gp.n_tiles) * KB;
+  // cost of one unit boundary in k-blocks (measured best ~8 at K = 5120; FC_GEMM_DRAIN overrides)
+  const long long kDrain = gemm_drain > 0 ? gemm_drain : std::max<long long>(1, KB / 10);
+  auto fill = [&](long long budget, bool write) {
+    long long u = 0;
+    int c = 0;
+    for (; c < n_clusters && u < U; ++c) {
+      if (write) gp.unit_lo[c] = static_cast<int>(u);
+      long long left = budget;
+      while (u < U) {
+        const long long in_tile = KB - u % KB;
+        if (left <= kDrain) break;
+        const long long take = std::min(in_tile, left - kDrain);
+        u += take;
+        left -= take + kDrain;
+        if (take < in_tile) break;
+      }
+    }
+    if (write) for (int k = c; k <= n_clusters; ++k) gp.unit_lo[k] = static_cast<int>(U);
+    return u >= U;
+  };
+  long long lo = 1, hi = U + kDrain * (gp.n_tiles + 1);
+  while (lo < hi) {   // smallest budget that covers every unit with n_clusters clusters
+    const long long mid = (lo + hi) / 2;
+    if (fill(mid, false)) hi = mid; else lo = mid + 1;
+  }
+  fill(lo, true);
+  gp.unit_lo[n_clusters] = static_cast<int>(U);
+}
+
+
 struct LossStep {
   fc_config cfg{};
   int B = 0, Bl = 0, d = 0, K = 1, rank = 0, ldq = 0, n_jt = 0, n_sm = 148;
@@ -469,39 +504,7 @@ struct LossStep {
     map_e2 = e2;
   }
 
-  // Contiguous stream-K ranges over the (tile, k-block) sequence with equal estimated cost
-  // per cluster: k-blocks + kDrain per unit (each unit ends in a full-tile epilogue that the
-  // single TMEM accumulator cannot overlap). Greedy fill against a binary-searched budget.
-  void balance_units(fc::GemmParams& gp, int n_clusters) const {
-    const long long KB = gp.kb_total, U = static_cast<long long>(gp.n_tiles) * KB;
-    // cost of one unit boundary in k-blocks (measured best ~8 at K = 5120; FC_GEMM_DRAIN overrides)
-    const long long kDrain = gemm_drain > 0 ? gemm_drain : std::max<long long>(1, KB / 10);
-    auto fill = [&](long long budget, bool write) {
-      long long u = 0;
-      int c = 0;
-      for (; c < n_clusters && u < U; ++c) {
-        if (write) gp.unit_lo[c] = static_cast<int>(u);
-        long long left = budget;
-        while (u < U) {
-          const long long in_tile = KB - u % KB;
-          if (left <= kDrain) break;
-          const long long take = std::min(in_tile, left - kDrain);
-          u += take;
-          left -= take + kDrain;
-          if (take < in_tile) break;
-        }
-      }
-      if (write) for (int k = c; k <= n_clusters; ++k) gp.unit_lo[k] = static_cast<int>(U);
-      return u >= U;
-    };
-    long long lo = 1, hi = U + kDrain * (gp.n_tiles + 1);
-    while (lo < hi) {   // smallest budget that covers every unit with n_clusters clusters
-      const long long mid = (lo + hi) / 2;
-      if (fill(mid, false)) hi = mid; else lo = mid + 1;
-    }
-    fill(lo, true);
-    gp.unit_lo[n_clusters] = static_cast<int>(U);
-  }
+  void balance_units(fc::GemmParams& gp, int n_clusters) const { balance_stream_k(gp, n_clusters, gemm_drain); }
 
   int pair_grid(long items) const {
     long pairs = std::min<long>(n_sm / 2, items);
@@ -1193,7 +1196,7 @@ int fc_g_values(const void* e1g, const void* e2g, int32_t batch, int32_t dim, co
     FC_CUDA(cudaMemsetAsync(bnd, 0, 4 * sizeof(float) + sizeof(unsigned long long), st));
     fc::fc_rows_kernel<<<(B * 32 + 127) / 128, 128, 0, st>>>(static_cast<const __nv_bfloat16*>(e1g),
                                                             static_cast<const __nv_bfloat16*>(e2g), B, d, lo, cnt,
-                                                            t1_local, t2_local, rsR, rsC, bnd);
+                                                            t1_local, t2_local, rsR, rsC, bnd, nullptr);
     FC_CUDA(cudaGetLastError());
     const uint64_t rb = static_cast<uint64_t>(d) * 2;
     CUtensorMap m1 = make_map(e1g, d, B, rb, 64, 128), m2 = make_map(e2g, d, B, rb, 64, 128);
@@ -1228,6 +1231,146 @@ int fc_g_values(const void* e1g, const void* e2g, int32_t batch, int32_t dim, co
                                                          dsum1, dsum2);
     FC_CUDA(cudaGetLastError());
     if (clamps) FC_CUDA(cudaMemcpyAsync(clamps, ncl, sizeof(uint64_t), cudaMemcpyDeviceToDevice, st));
+    FC_CUDA(cudaFreeAsync(ws, st));
+  });
+}
+
+// engine::embedding_cotangents (engine.cpp:77-121) for the local slice [local_begin,
+// local_begin + local_count) of a global batch with the caller's PairWeights (w, t over G):
+// pass 1 (row sums for r_i), the pass-2 Q' tiles of both segments (two-exponential path, t per
+// anchor) and the weighted-gradient GEMM -- the step's kernels on caller-provided operands.
+// Stateless: workspaces come from the stream-ordered allocator.
+int fc_embedding_cotangents(const void* e1g, const void* e2g, int32_t batch, int32_t dim, const double* w1,
+                            const double* w2, const double* t1, const double* t2, int32_t local_begin,
+                            int32_t local_count, float* de1, float* de2, void* stream) {
+  return guarded([&] {
+    if (batch < 2) throw FcError{FC_ERR_DEGENERATE_BATCH, "embedding_cotangents: global batch must have >= 2 pairs"};
+    if (local_begin < 0 || local_count <= 0 || local_begin + local_count > batch)
+      throw FcError{FC_ERR_SHAPE, "embedding_cotangents: local slice outside the global batch"};
+    if (dim < 8 || dim % 8 != 0) throw FcError{FC_ERR_UNSUPPORTED, "dim must be a positive multiple of 8"};
+    if (!e1g || !e2g || !w1 || !w2 || !t1 || !t2 || !de1 || !de2)
+      throw FcError{FC_ERR_SHAPE, "embedding_cotangents: null pointer"};
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const int B = batch, d = dim, lo = local_begin, cnt = local_count;
+    const int n_jt = (B + fc::kPairN - 1) / fc::kPairN, nparts = n_jt * 4;
+    const int ldq = (B + 63) / 64 * 64;
+    const size_t np = static_cast<size_t>(n_jt) * fc::kPairN;
+    // workspace: partials, row stats, diag, 8 parameter arrays, r, bounds + clamps, Q'
+    const size_t part_b = static_cast<size_t>(cnt) * nparts * sizeof(float2);
+    const size_t q_b = 2 * static_cast<size_t>(cnt) * ldq * 2;
+    const size_t off_rs = 2 * part_b, off_diag = off_rs + 2 * cnt * sizeof(float2);
+    const size_t off_par = (off_diag + B * sizeof(float) + 255) / 256 * 256;
+    const size_t off_r = off_par + 8 * np * sizeof(float);
+    const size_t off_b = (off_r + cnt * sizeof(float) + 255) / 256 * 256;
+    const size_t off_q = off_b + 256;
+    uint8_t* ws = nullptr;
+    FC_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&ws), off_q + q_b, st));
+    float2* pR = reinterpret_cast<float2*>(ws);
+    float2* pC = reinterpret_cast<float2*>(ws + part_b);
+    float2* rsR = reinterpret_cast<float2*>(ws + off_rs);
+    float2* rsC = rsR + cnt;
+    float* diag = reinterpret_cast<float*>(ws + off_diag);
+    float* par = reinterpret_cast<float*>(ws + off_par);
+    float* rco = reinterpret_cast<float*>(ws + off_r);
+    float* bnd = reinterpret_cast<float*>(ws + off_b);
+    unsigned long long* ncl = reinterpret_cast<unsigned long long*>(bnd + 4);
+    __nv_bfloat16* q = reinterpret_cast<__nv_bfloat16*>(ws + off_q);
+    FC_CUDA(cudaMemsetAsync(par, 0, 8 * np * sizeof(float), st));   // zero-padded column tiles
+    FC_CUDA(cudaMemsetAsync(bnd, 0, 256, st));
+    FC_CUDA(cudaMemsetAsync(de1, 0, static_cast<size_t>(cnt) * d * sizeof(float), st));   // reduce-add targets
+    FC_CUDA(cudaMemsetAsync(de2, 0, static_cast<size_t>(cnt) * d * sizeof(float), st));
+    const auto* E1 = static_cast<const __nv_bfloat16*>(e1g);
+    const auto* E2 = static_cast<const __nv_bfloat16*>(e2g);
+    fc::fc_rows_kernel<<<(B * 32 + 127) / 128, 128, 0, st>>>(E1, E2, B, d, lo, cnt, t1 + lo, t2 + lo, rsR, rsC, bnd,
+                                                            diag);
+    float* kap1 = par; float* bet1 = par + np; float* coef1 = par + 2 * np; float* fac1 = par + 3 * np;
+    float* kap2 = par + 4 * np; float* bet2 = par + 5 * np; float* coef2 = par + 6 * np; float* fac2 = par + 7 * np;
+    fc::fc_pair_params_kernel<<<(B + 255) / 256, 256, 0, st>>>(diag, w1, w2, t1, t2, B, kap1, bet1, coef1, fac1, kap2,
+                                                               bet2, coef2, fac2, bnd);
+    FC_CUDA(cudaGetLastError());
+    const uint64_t rb = static_cast<uint64_t>(d) * 2;
+    CUtensorMap m1k = make_map(e1g, d, B, rb, 64, 128), m2k = make_map(e2g, d, B, rb, 64, 128);
+    CUtensorMap m1n = make_map(e1g, d, B, rb, 64, 64), m2n = make_map(e2g, d, B, rb, 64, 64);
+    int dev = 0;
+    FC_CUDA(cudaGetDevice(&dev));
+    static bool smem_set = false;
+    if (!smem_set) {
+      FC_CUDA(fc::sim_set_smem());
+      FC_CUDA(fc::gemm_set_smem());
+      smem_set = true;
+    }
+    const int n_sm = sm_count(dev);
+    // pass 1: row sums of S[L,G] and S^T[L,G] at the local anchors' temperatures -> r_i
+    fc::SimParams sp{};
+    sp.nseg = 2;
+    sp.d = d;
+    sp.ldq = ldq;
+    sp.n_jt = n_jt;
+    for (int s2 = 0; s2 < 2; ++s2) {
+      fc::SimSeg& g = sp.seg[s2];
+      g.rows = cnt;
+      g.a_row0 = lo;
+      g.cols = B;
+      g.row_stat = s2 ? rsC : rsR;
+      g.partial = s2 ? pC : pR;
+      sp.n_rb[s2] = (cnt + fc::kPairM - 1) / fc::kPairM;
+    }
+    sp.n_items = (sp.n_rb[0] + sp.n_rb[1]) * n_jt;
+    sp.clamps = ncl;
+    sp.bounds = bnd;
+    sp.n_bounds = 1;
+    CUtensorMap mA[2] = {m1k, m2k}, mB[2] = {m2k, m1k};
+    const int grid = 2 * std::max(1, std::min(n_sm / 2, sp.n_items));
+    FC_CUDA(fc::launch_sim(fc::kSimStats, sp, mA, mB, nullptr, grid, st, nullptr));
+    fc::fc_rcoef_kernel<<<(cnt + 127) / 128, 128, 0, st>>>(pR, pC, nparts, cnt, lo, w1, w2, t1, t2, rco);
+    FC_CUDA(cudaGetLastError());
+    // pass 2: Q'_R = Q[L,G], Q'_C = Q[G,L]^T (bf16), both from S tiles of segment R / C
+    CUtensorMap mQo[2], mQ[2];
+    for (int s2 = 0; s2 < 2; ++s2) {
+      __nv_bfloat16* qs = q + static_cast<size_t>(s2) * cnt * ldq;
+      mQo[s2] = make_map(qs, ldq, cnt, static_cast<uint64_t>(ldq) * 2, 32, 32, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16,
+                         CU_TENSOR_MAP_SWIZZLE_64B);
+      mQ[s2] = make_map(qs, ldq, cnt, static_cast<uint64_t>(ldq) * 2, 64, 128);
+      fc::SimSeg& g = sp.seg[s2];
+      g.row_stat = nullptr;
+      g.partial = nullptr;
+      g.row_kappa = (s2 ? kap2 : kap1) + lo;
+      g.row_beta = (s2 ? bet2 : bet1) + lo;
+      g.row_coef = (s2 ? coef2 : coef1) + lo;
+      g.row_fac = (s2 ? fac2 : fac1) + lo;
+      g.col_kappa = s2 ? kap1 : kap2;
+      g.col_beta = s2 ? bet1 : bet2;
+      g.col_coef = s2 ? coef1 : coef2;
+      g.col_fac = s2 ? fac1 : fac2;
+      g.q = qs;
+    }
+    sp.q_factor = 0;   // a temperature per anchor: the two-exponential Q path
+    FC_CUDA(fc::launch_sim(fc::kSimQ, sp, mA, mB, mQo, grid, st, nullptr));
+    // dE = c (Q' E - r o E_L), c = 1 / (local_count (B - 1)) (engine.cpp:84-85)
+    fc::GemmParams gp{};
+    gp.nseg = 2;
+    gp.d = d;
+    gp.n_nb = (d + fc::kGemmN - 1) / fc::kGemmN;
+    gp.pairs_per_cluster = 1;
+    gp.kb_total = ldq / fc::kBlockK;
+    gp.scale = static_cast<float>(1.0 / (static_cast<double>(cnt) * static_cast<double>(B - 1)));
+    CUtensorMap mO[2];
+    for (int s2 = 0; s2 < 2; ++s2) {
+      fc::GemmSeg& g = gp.seg[s2];
+      g.a_mn_major = 0;
+      g.rows = cnt;
+      g.x_row0 = lo;
+      g.r = rco;
+      g.x = s2 ? E1 : E2;
+      g.out = s2 ? de2 : de1;
+      gp.n_mb[s2] = (cnt + fc::kPairM - 1) / fc::kPairM;
+      mO[s2] = make_map(g.out, d, cnt, static_cast<uint64_t>(d) * 4, 32, 32, CU_TENSOR_MAP_DATA_TYPE_FLOAT32);
+    }
+    gp.n_tiles = (gp.n_mb[0] + gp.n_mb[1]) * gp.n_nb;
+    const int gemm_ctas = (n_sm / 2) * 2;
+    balance_stream_k(gp, gemm_ctas / 2, 0);
+    CUtensorMap mX[2] = {m2n, m1n};
+    FC_CUDA(fc::launch_gemm(false, gp, mQ, mX, mO, gemm_ctas, st));
     FC_CUDA(cudaFreeAsync(ws, st));
   });
 }

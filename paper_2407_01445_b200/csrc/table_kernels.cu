@@ -356,7 +356,7 @@ namespace fc {
 // caller's temperatures (engine.cpp:151-176 takes t per local anchor).
 __global__ void fc_rows_kernel(const __nv_bfloat16* __restrict__ e1, const __nv_bfloat16* __restrict__ e2, int B,
                                int d, int lo, int cnt, const double* __restrict__ t1, const double* __restrict__ t2,
-                               float2* rowstat_R, float2* rowstat_C, float* bounds) {
+                               float2* rowstat_R, float2* rowstat_C, float* bounds, float* diag) {
   const int w = (blockIdx.x * blockDim.x + threadIdx.x) / 32;
   const int lane = threadIdx.x & 31;
   float acc = 0.f, n1 = 0.f, n2 = 0.f;
@@ -379,6 +379,7 @@ __global__ void fc_rows_kernel(const __nv_bfloat16* __restrict__ e1, const __nv_
   if (lane != 0 || w >= B) return;
   atomicMax(reinterpret_cast<int*>(bounds) + 0, __float_as_int(n1));   // non-negative floats order like ints
   atomicMax(reinterpret_cast<int*>(bounds) + 1, __float_as_int(n2));
+  if (diag) diag[w] = acc;
   const int r = w - lo;
   if (r < 0 || r >= cnt) return;
   const float k1 = static_cast<float>(kLog2eD / t1[r]), k2 = static_cast<float>(kLog2eD / t2[r]);
@@ -408,6 +409,48 @@ __global__ void fc_gsum_kernel(const float2* __restrict__ pR, const float2* __re
     ds1[r] = (-(d1 / (t1[r] * t1[r]))) * inv;
     ds2[r] = (-(d2 / (t2[r] * t2[r]))) * inv;
   }
+}
+
+// engine::embedding_cotangents parameters (fc_embedding_cotangents): the pass-2 exponent /
+// weight parameters of every anchor a of G from the caller's PairWeights (engine.hpp:29-32):
+// kappa = log2(e)/t_a, beta = -S_aa kappa, coef = w_a / t_a, fac = coef 2^beta; the kappa
+// maximum goes to bounds[2]. Arrays are zero-padded to whole 256-column tiles by the caller.
+__global__ void fc_pair_params_kernel(const float* __restrict__ diag, const double* __restrict__ w1,
+                                      const double* __restrict__ w2, const double* __restrict__ t1,
+                                      const double* __restrict__ t2, int B, float* kap1, float* bet1, float* coef1,
+                                      float* fac1, float* kap2, float* bet2, float* coef2, float* fac2,
+                                      float* bounds) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= B) return;
+  AnchorParams p;
+  p.t1 = t1[i];
+  p.t2 = t2[i];
+  p.c1 = w1[i] / p.t1;
+  p.c2 = w2[i] / p.t2;
+  p.k1 = static_cast<float>(kLog2eD / p.t1);
+  p.k2 = static_cast<float>(kLog2eD / p.t2);
+  const float s_ii = diag[i];
+  const float b1 = -s_ii * p.k1, b2 = -s_ii * p.k2;
+  const float c1 = static_cast<float>(p.c1), c2 = static_cast<float>(p.c2);
+  kap1[i] = p.k1; bet1[i] = b1; coef1[i] = c1; fac1[i] = c1 * exp2f(b1);
+  kap2[i] = p.k2; bet2[i] = b2; coef2[i] = c2; fac2[i] = c2 * exp2f(b2);
+  atomicMax(reinterpret_cast<int*>(bounds) + 2, __float_as_int(fmaxf(p.k1, p.k2)));
+}
+
+// r_i = (w1_i/t1_i) S1_i + (w2_i/t2_i) S2_i of the local rows (fixed-order sum of the pass-1
+// partials), the anchor-part coefficient of engine.cpp:93-106.
+__global__ void fc_rcoef_kernel(const float2* __restrict__ pR, const float2* __restrict__ pC, int nparts, int cnt,
+                                int lo, const double* __restrict__ w1, const double* __restrict__ w2,
+                                const double* __restrict__ t1, const double* __restrict__ t2, float* rcoef) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= cnt) return;
+  double s1 = 0.0, s2 = 0.0;
+  for (int q = 0; q < nparts; ++q) {
+    s1 += pR[static_cast<size_t>(r) * nparts + q].x;
+    s2 += pC[static_cast<size_t>(r) * nparts + q].x;
+  }
+  const int i = lo + r;
+  rcoef[r] = static_cast<float>(w1[i] / t1[i] * s1 + w2[i] / t2[i] * s2);
 }
 
 }  // namespace fc

@@ -92,7 +92,15 @@ __global__ void fc_reduce_kernel(StepArgs a);
 __global__ void fc_indiv_update_kernel(StepArgs a);
 __global__ void fc_rows_kernel(const __nv_bfloat16* __restrict__ e1, const __nv_bfloat16* __restrict__ e2, int B,
                                int d, int lo, int cnt, const double* __restrict__ t1, const double* __restrict__ t2,
-                               float2* rowstat_R, float2* rowstat_C, float* bounds);
+                               float2* rowstat_R, float2* rowstat_C, float* bounds, float* diag);
+__global__ void fc_pair_params_kernel(const float* __restrict__ diag, const double* __restrict__ w1,
+                                      const double* __restrict__ w2, const double* __restrict__ t1,
+                                      const double* __restrict__ t2, int B, float* kap1, float* bet1, float* coef1,
+                                      float* fac1, float* kap2, float* bet2, float* coef2, float* fac2,
+                                      float* bounds);
+__global__ void fc_rcoef_kernel(const float2* __restrict__ pR, const float2* __restrict__ pC, int nparts, int cnt,
+                                int lo, const double* __restrict__ w1, const double* __restrict__ w2,
+                                const double* __restrict__ t1, const double* __restrict__ t2, float* rcoef);
 __global__ void fc_gsum_kernel(const float2* __restrict__ pR, const float2* __restrict__ pC, int nparts, int cnt,
                                int B, const float2* __restrict__ rsR, const float2* __restrict__ rsC,
                                const double* __restrict__ t1, const double* __restrict__ t2, double* g1, double* g2,

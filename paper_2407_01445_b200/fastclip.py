@@ -103,6 +103,7 @@ def lib():
         L.fc_phase_times.argtypes = [P, I32, C.POINTER(C.c_float), I32]
         L.fc_debug_similarity.argtypes = [P, P, I32, I32, I32, P, P]
         L.fc_g_values.argtypes = [P, P, I32, I32, P, P, I32, I32, P, P, P, P, P, P]
+        L.fc_embedding_cotangents.argtypes = [P, P, I32, I32, P, P, P, P, I32, I32, P, P, P]
         L.fc_last_error.restype = C.c_char_p
         _lib = L
     return _lib
@@ -113,6 +114,7 @@ EXPORTED = [
     "fc_destroy", "fc_loss_step", "fc_step_scalars_get", "fc_local_views", "fc_table_download",
     "fc_table_upload", "fc_tau_state_get", "fc_tau_state_set", "fc_kernels_per_step",
     "fc_debug_similarity", "fc_last_error", "fc_set_phase_timing", "fc_phase_times", "fc_g_values",
+    "fc_embedding_cotangents",
 ]
 PHASES = ["allgather_e", "prep", "pass1_stats", "tables_tau", "pass2_q", "grad_gemm"]
 
@@ -295,6 +297,26 @@ def g_values(e1g, e2g, t1_local, t2_local, local_begin: int, local_count: int, d
                              _dptr(out["dsum2"]) if dtau_sums else None, _dptr(ncl), C.c_void_p(stream.cuda_stream)))
     out["clamps"] = int(ncl.item())
     return out
+
+
+def embedding_cotangents(e1g, e2g, w1, w2, t1, t2, local_begin: int, local_count: int):
+    """engine::embedding_cotangents (engine.cpp:77-121): dE1, dE2 (CUDA fp32 [local_count, d]) of
+    the local slice from the PairWeights w1, w2, t1, t2 over G (fp64 [B]), e1g / e2g CUDA bf16
+    [B, d], through the step's pass-1 / pass-2 / gradient-GEMM kernels."""
+    import torch
+    B, d = e1g.shape
+    for name, x in (("e1g", e1g), ("e2g", e2g)):
+        if x.dtype != torch.bfloat16 or not x.is_cuda or not x.is_contiguous() or tuple(x.shape) != (B, d):
+            raise FastclipError(2, f"{name} must be a contiguous CUDA bf16 tensor of shape ({B}, {d})")
+    ws = [x.to(device=e1g.device, dtype=torch.float64).contiguous() for x in (w1, w2, t1, t2)]
+    if any(x.numel() != B for x in ws):
+        raise FastclipError(2, f"w1, w2, t1, t2 must have {B} entries")
+    de1 = torch.empty(local_count, d, device=e1g.device, dtype=torch.float32)
+    de2 = torch.empty(local_count, d, device=e1g.device, dtype=torch.float32)
+    stream = torch.cuda.current_stream(e1g.device)
+    _check(lib().fc_embedding_cotangents(_dptr(e1g), _dptr(e2g), B, d, *[_dptr(x) for x in ws], int(local_begin),
+                                         int(local_count), _dptr(de1), _dptr(de2), C.c_void_p(stream.cuda_stream)))
+    return de1, de2
 
 
 def debug_similarity(a, b):

@@ -66,3 +66,35 @@ def test_g_values_rejects_bad_slices():
     with pytest.raises(P.FastclipError) as e:
         P.g_values(to_dev_bf16(b1), to_dev_bf16(b2), t, t, 48, 32)   # slice past the batch
     assert e.value.code == 2
+
+
+def _oracle_cot(E1, E2, w1, w2, t1, t2, lo, cnt):
+    L = O.lib("oracle")
+    DP = C.POINTER(C.c_double)
+    L.oc_embedding_cotangents.argtypes = [C.c_int, C.c_int, DP, DP, DP, DP, DP, DP, C.c_int, C.c_int, DP, DP]
+    B, d = E1.shape
+    p = lambda a: a.ctypes.data_as(DP)
+    d1, d2 = np.zeros((cnt, d)), np.zeros((cnt, d))
+    assert L.oc_embedding_cotangents(B, d, p(E1), p(E2), p(w1), p(w2), p(t1), p(t2), lo, cnt, p(d1), p(d2)) == 0
+    return d1, d2
+
+
+@pytest.mark.parametrize("B,d,lo,cnt,tmin,tmax", [
+    (600, 200, 128, 256, 0.02, 0.1),     # ragged, middle slice, per-anchor temperatures (v2-like)
+    (512, 128, 0, 512, 0.07, 0.07),      # whole batch, one temperature (v3-like)
+    (384, 64, 300, 84, 0.01, 0.03),      # small tail slice
+])
+def test_embedding_cotangents_match_oracle(B, d, lo, cnt, tmin, tmax):
+    import torch
+    import paper_2407_01445_b200 as P
+    b1, b2 = S.embeddings(B, d, 41)
+    rng = np.random.default_rng(9)
+    t1, t2 = rng.uniform(tmin, tmax, B), rng.uniform(tmin, tmax, B)
+    w1, w2 = t1 / (1e-14 + 10 ** rng.uniform(-6, 0, B)), t2 / (1e-14 + 10 ** rng.uniform(-6, 0, B))
+    cuda = lambda a: torch.from_numpy(a).cuda()
+    de1, de2 = P.embedding_cotangents(to_dev_bf16(b1), to_dev_bf16(b2), cuda(w1), cuda(w2), cuda(t1), cuda(t2), lo, cnt)
+    r1, r2 = _oracle_cot(S.bf16_to_f32(b1).astype(np.float64), S.bf16_to_f32(b2).astype(np.float64), w1, w2, t1, t2,
+                         lo, cnt)
+    nr = lambda a, b: float(np.linalg.norm(a - b) / np.linalg.norm(b))
+    assert nr(de1.cpu().numpy().astype(np.float64), r1) < 2e-3
+    assert nr(de2.cpu().numpy().astype(np.float64), r2) < 2e-3
