@@ -184,6 +184,20 @@ int fc_embedding_cotangents(const void* e1g, const void* e2g, int32_t batch, int
                             const double* w2, const double* t1, const double* t2, int32_t local_begin,
                             int32_t local_count, float* de1, float* de2, void* stream);
 
+/* opt::temperature_step (optimizers.cpp:77-83): Adam with weight decay 0 (bias correction with
+ * step + 1, then ++step; optimizers.cpp:65-75) and the projection max(tau, tau0). Host scalar;
+ * FC_ERR_NUMERIC for a non-finite gradient (optimizers.cpp:67). */
+int fc_temperature_step(double* m, double* v, int64_t* step, double tau, double grad, double lr, double beta1,
+                        double beta2, double eps, double tau0, double* tau_out);
+
+/* UTable::update + snapshot (state.cpp:45-71) on caller-owned device tables u1/u2 [n_train]:
+ * u <- (1 - gamma) u + gamma g at ids[0..count) (distinct), post-update values into
+ * u1_out/u2_out [count] (may be NULL). FC_ERR_DOMAIN for gamma outside (0,1] (state.cpp:50);
+ * a device-side ShapeError (id outside [0, n_train), state.cpp:46) or domain_error (g < 0,
+ * state.cpp:51) is written to *status (device int32, may be NULL) and that entry is skipped. */
+int fc_table_update(double* u1, double* u2, int64_t n_train, const int32_t* ids, const double* g1, const double* g2,
+                    int32_t count, double gamma, double* u1_out, double* u2_out, int32_t* status, void* stream);
+
 const char* fc_last_error(void);
 
 #ifdef __cplusplus

@@ -950,6 +950,64 @@ double fc_epsilon_at(double initial, double late, int64_t switch_epoch, int64_t 
   return epoch < switch_epoch ? initial : late;
 }
 
+// opt::temperature_step (optimizers.cpp:77-83): scalar_adamw_step with weight decay 0
+// (optimizers.cpp:65-75: bias correction with step + 1, then ++step) and the projection
+// max(tau, tau0). Host scalar, the same arithmetic as the device finalize_step.
+int fc_temperature_step(double* m, double* v, int64_t* step, double tau, double grad, double lr, double beta1,
+                        double beta2, double eps, double tau0, double* tau_out) {
+  if (!m || !v || !step || !tau_out) return FC_ERR_SHAPE;
+  if (!std::isfinite(grad)) {
+    g_last_error = "temperature_step: non-finite gradient (NumericError, optimizers.cpp:67)";
+    return FC_ERR_NUMERIC;
+  }
+  *m = beta1 * *m + (1.0 - beta1) * grad;
+  *v = beta2 * *v + (1.0 - beta2) * grad * grad;
+  const double c1 = 1.0 - std::pow(beta1, static_cast<double>(*step + 1));
+  const double c2 = 1.0 - std::pow(beta2, static_cast<double>(*step + 1));
+  *step += 1;
+  const double r = (*m / c1) / (std::sqrt(*v / c2) + eps);
+  const double next = tau - lr * (r + 0.0 * tau);
+  *tau_out = next < tau0 ? tau0 : next;
+  return FC_OK;
+}
+
+// UTable::update + snapshot (state.cpp:45-71) on device tables: u <- (1 - gamma) u + gamma g at
+// ids[0..count), then the post-update values in batch order.
+__global__ void fc_table_update_kernel(double* u1, double* u2, int64_t n, const int32_t* ids, const double* g1,
+                                       const double* g2, int count, double gamma, double* o1, double* o2,
+                                       int32_t* status) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= count) return;
+  const int id = ids[r];
+  if (id < 0 || id >= n) {   // ShapeError (state.cpp:46)
+    if (status) atomicExch(status, FC_ERR_SHAPE);
+    return;
+  }
+  const double a = g1[r], b = g2[r];
+  if (a < 0.0 || b < 0.0) {   // domain_error (state.cpp:51)
+    if (status) atomicExch(status, FC_ERR_DOMAIN);
+    return;
+  }
+  const double x1 = (1.0 - gamma) * u1[id] + gamma * a;
+  const double x2 = (1.0 - gamma) * u2[id] + gamma * b;
+  u1[id] = x1;
+  u2[id] = x2;
+  if (o1) o1[r] = x1;
+  if (o2) o2[r] = x2;
+}
+
+int fc_table_update(double* u1, double* u2, int64_t n_train, const int32_t* ids, const double* g1, const double* g2,
+                    int32_t count, double gamma, double* u1_out, double* u2_out, int32_t* status, void* stream) {
+  return guarded([&] {
+    if (!(gamma > 0.0) || gamma > 1.0) throw FcError{FC_ERR_DOMAIN, "gamma must be in (0,1] (state.cpp:50)"};
+    if (!u1 || !u2 || !ids || !g1 || !g2 || count < 0) throw FcError{FC_ERR_SHAPE, "table_update: bad arguments"};
+    if (count == 0) return;
+    fc_table_update_kernel<<<(count + 255) / 256, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+        u1, u2, n_train, ids, g1, g2, count, gamma, u1_out, u2_out, status);
+    FC_CUDA(cudaGetLastError());
+  });
+}
+
 int fc_nccl_unique_id(uint8_t out[128]) {
   return guarded([&] {
     ncclUniqueId id;

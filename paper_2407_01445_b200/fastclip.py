@@ -104,6 +104,8 @@ def lib():
         L.fc_debug_similarity.argtypes = [P, P, I32, I32, I32, P, P]
         L.fc_g_values.argtypes = [P, P, I32, I32, P, P, I32, I32, P, P, P, P, P, P]
         L.fc_embedding_cotangents.argtypes = [P, P, I32, I32, P, P, P, P, I32, I32, P, P, P]
+        L.fc_temperature_step.argtypes = [DP, DP, LP, D, D, D, D, D, D, D, DP]
+        L.fc_table_update.argtypes = [P, P, I64, P, P, P, I32, D, P, P, P, P]
         L.fc_last_error.restype = C.c_char_p
         _lib = L
     return _lib
@@ -114,7 +116,7 @@ EXPORTED = [
     "fc_destroy", "fc_loss_step", "fc_step_scalars_get", "fc_local_views", "fc_table_download",
     "fc_table_upload", "fc_tau_state_get", "fc_tau_state_set", "fc_kernels_per_step",
     "fc_debug_similarity", "fc_last_error", "fc_set_phase_timing", "fc_phase_times", "fc_g_values",
-    "fc_embedding_cotangents",
+    "fc_embedding_cotangents", "fc_temperature_step", "fc_table_update",
 ]
 PHASES = ["allgather_e", "prep", "pass1_stats", "tables_tau", "pass2_q", "grad_gemm"]
 
@@ -317,6 +319,31 @@ def embedding_cotangents(e1g, e2g, w1, w2, t1, t2, local_begin: int, local_count
     _check(lib().fc_embedding_cotangents(_dptr(e1g), _dptr(e2g), B, d, *[_dptr(x) for x in ws], int(local_begin),
                                          int(local_count), _dptr(de1), _dptr(de2), C.c_void_p(stream.cuda_stream)))
     return de1, de2
+
+
+def temperature_step(state: dict, tau: float, grad: float, lr: float, beta1=0.9, beta2=0.999, eps=1e-8,
+                     tau0=0.005) -> float:
+    """opt::temperature_step (optimizers.cpp:77-83) on state {"m", "v", "step"} (updated in place)."""
+    m, v, st, out = C.c_double(state["m"]), C.c_double(state["v"]), C.c_int64(state["step"]), C.c_double(0.0)
+    _check(lib().fc_temperature_step(C.byref(m), C.byref(v), C.byref(st), tau, grad, lr, beta1, beta2, eps, tau0,
+                                     C.byref(out)))
+    state.update(m=m.value, v=v.value, step=st.value)
+    return out.value
+
+
+def table_update(u1, u2, ids, g1, g2, gamma: float):
+    """UTable::update + snapshot (state.cpp:45-71) on CUDA fp64 tables u1/u2 (in place); returns
+    (u1 snapshot, u2 snapshot, status) with status the device-detected error code (0 = ok)."""
+    import torch
+    n = u1.numel()
+    cnt = ids.numel()
+    o1 = torch.empty(cnt, device=u1.device, dtype=torch.float64)
+    o2 = torch.empty(cnt, device=u1.device, dtype=torch.float64)
+    status = torch.zeros(1, device=u1.device, dtype=torch.int32)
+    stream = torch.cuda.current_stream(u1.device)
+    _check(lib().fc_table_update(_dptr(u1), _dptr(u2), n, _dptr(ids), _dptr(g1), _dptr(g2), cnt, gamma, _dptr(o1),
+                                 _dptr(o2), _dptr(status), C.c_void_p(stream.cuda_stream)))
+    return o1, o2, int(status.item())
 
 
 def debug_similarity(a, b):

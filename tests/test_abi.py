@@ -56,3 +56,28 @@ def test_create_rejects_bad_shapes_without_gpu_work():
     with pytest.raises(P.FastclipError) as e:
         P.LossStep(cfg)
     assert e.value.kind in ("Unsupported", "CudaError")
+
+
+def test_temperature_step_matches_oracle():
+    # opt::temperature_step (optimizers.cpp:77-83) through the C ABI (host scalar) against the
+    # C restatement, over a sequence of steps incl. the projection onto tau0 and a NaN gradient
+    import ctypes as C
+    import oracle as O
+    import paper_2407_01445_b200 as P
+    L = O.lib("oracle")
+    L.oc_temperature_step.argtypes = [C.POINTER(C.c_double), C.POINTER(C.c_double), C.POINTER(C.c_int64), C.c_double,
+                                      C.c_double, C.c_double, C.c_double, C.c_double, C.c_double, C.c_double,
+                                      C.POINTER(C.c_double)]
+    st = dict(m=0.0, v=0.0, step=0)
+    m, v, s, out = C.c_double(0.0), C.c_double(0.0), C.c_int64(0), C.c_double(0.0)
+    tau_a = tau_b = 0.03
+    for k, g in enumerate([3.1, -2.0, 0.5, 40.0, 40.0, 40.0, -1e-3]):
+        tau_a = P.temperature_step(st, tau_a, g, 2e-4 if k < 3 else 5e-2)
+        assert L.oc_temperature_step(C.byref(m), C.byref(v), C.byref(s), tau_b, g, 2e-4 if k < 3 else 5e-2, 0.9, 0.999,
+                                     1e-8, 0.005, C.byref(out)) == 0
+        tau_b = out.value
+        assert tau_a == tau_b and st["m"] == m.value and st["v"] == v.value and st["step"] == s.value
+    assert tau_a == 0.005                                  # projected onto tau0
+    with pytest.raises(P.FastclipError) as e:
+        P.temperature_step(st, tau_a, float("nan"), 1e-3)
+    assert e.value.code == 9

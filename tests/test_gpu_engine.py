@@ -98,3 +98,34 @@ def test_embedding_cotangents_match_oracle(B, d, lo, cnt, tmin, tmax):
     nr = lambda a, b: float(np.linalg.norm(a - b) / np.linalg.norm(b))
     assert nr(de1.cpu().numpy().astype(np.float64), r1) < 2e-3
     assert nr(de2.cpu().numpy().astype(np.float64), r2) < 2e-3
+
+
+def test_table_update_matches_state_semantics():
+    # UTable::update + snapshot (state.cpp:45-71): fp64 EMA at the ids, snapshot in batch order,
+    # untouched entries bit-identical; an id outside the table is a ShapeError (skipped)
+    import torch
+    import paper_2407_01445_b200 as P
+    N, n = 5000, 300
+    rng = np.random.default_rng(3)
+    u1, u2 = S.warm_u(N, 1), S.warm_u(N, 2)
+    ids = rng.choice(N, n, replace=False).astype(np.int32)
+    g1, g2 = rng.uniform(0, 2, n), rng.uniform(0, 2, n)
+    d = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()
+    U1, U2 = d(u1), d(u2)
+    o1, o2, status = P.table_update(U1, U2, d(ids), d(g1), d(g2), 0.6)
+    r1, r2 = u1.copy(), u2.copy()
+    r1[ids] = 0.4 * u1[ids] + 0.6 * g1
+    r2[ids] = 0.4 * u2[ids] + 0.6 * g2
+    assert status == 0
+    mask = np.ones(N, bool)
+    mask[ids] = False
+    for got, ref in ((U1.cpu().numpy(), r1), (U2.cpu().numpy(), r2)):
+        np.testing.assert_array_equal(got[mask], ref[mask])            # untouched: bit-identical
+        np.testing.assert_allclose(got[ids], ref[ids], rtol=1e-14)     # fp64 EMA (FMA contraction)
+    np.testing.assert_array_equal(o1.cpu().numpy(), U1.cpu().numpy()[ids])   # the snapshot is the table
+    bad = ids.copy()
+    bad[5] = N
+    _, _, status = P.table_update(U1, U2, d(bad), d(g1), d(g2), 0.6)
+    assert status == 2
+    with pytest.raises(P.FastclipError):
+        P.table_update(U1, U2, d(ids), d(g1), d(g2), 1.5)   # gamma outside (0, 1]
