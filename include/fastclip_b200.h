@@ -198,6 +198,16 @@ int fc_temperature_step(double* m, double* v, int64_t* step, double tau, double 
 int fc_table_update(double* u1, double* u2, int64_t n_train, const int32_t* ids, const double* g1, const double* g2,
                     int32_t count, double gamma, double* u1_out, double* u2_out, int32_t* status, void* stream);
 
+/* engine::grad_tau_* for one worker's local anchors from their dtau sums (fc_g_values) and u
+ * snapshot (for MBCL, u = g): v0 grad_tau_unscaled (engine.cpp:208-224), v3 grad_tau_margin
+ * (:226-238) and MBCL (:261-266) write G_tau,k to gtau[0] (before the mean all-reduce,
+ * trainer.cpp:572); v2 / iSogCLR grad_tau_individual (:240-259) write gt1/gt2 [count] (needs
+ * t1/t2 and n_train). All pointers (device) fp64; fixed-order reduction. FC_ERR_CONFIG for the
+ * constant-tau variants (no tau gradient). */
+int fc_grad_tau(int32_t variant, int32_t count, int64_t batch, const double* u1, const double* u2, const double* dsum1,
+                const double* dsum2, const double* t1, const double* t2, double eps, double rho, double tau,
+                int64_t n_train, double* gtau, double* gt1, double* gt2, void* stream);
+
 const char* fc_last_error(void);
 
 #ifdef __cplusplus

@@ -1008,6 +1008,58 @@ int fc_table_update(double* u1, double* u2, int64_t n_train, const int32_t* ids,
   });
 }
 
+// engine::grad_tau_unscaled (v0, engine.cpp:208-224), grad_tau_margin (v3, :226-238),
+// grad_tau_mbcl (:261-266) -> gtau[0] (this worker's G_tau,k, before the mean all-reduce), and
+// grad_tau_individual (v2 / iSogCLR, :240-259) -> gt1/gt2 per local anchor. One block,
+// fixed-order fp64 reduction (deterministic).
+__global__ void fc_grad_tau_kernel(int variant, int count, long long batch, const double* u1, const double* u2,
+                                   const double* ds1, const double* ds2, const double* t1, const double* t2, double eps,
+                                   double rho, double tau, long long n_train, double* gtau, double* gt1, double* gt2) {
+  __shared__ double sh[2][32];
+  const bool indiv = variant == FC_ISOGCLR || variant == FC_FASTCLIP_V2;
+  const double e = variant == FC_OPENCLIP_MBCL ? 1.0 / static_cast<double>(batch - 1) : eps;
+  double a = 0.0, b = 0.0;
+  for (int r = threadIdx.x; r < count; r += blockDim.x) {
+    if (indiv) {
+      const double inv_n = 1.0 / static_cast<double>(n_train);
+      gt1[r] = inv_n * (log(eps + u1[r]) + rho + t1[r] * ds1[r] / (eps + u1[r]));
+      gt2[r] = inv_n * (log(eps + u2[r]) + rho + t2[r] * ds2[r] / (eps + u2[r]));
+    } else {
+      a += ds1[r] / (e + u1[r]) + ds2[r] / (e + u2[r]);
+      b += log(eps + u1[r]) + log(eps + u2[r]);
+    }
+  }
+  if (indiv) return;
+  for (int o = 16; o > 0; o >>= 1) {
+    a += __shfl_xor_sync(0xffffffffu, a, o);
+    b += __shfl_xor_sync(0xffffffffu, b, o);
+  }
+  if ((threadIdx.x & 31) == 0) { sh[0][threadIdx.x >> 5] = a; sh[1][threadIdx.x >> 5] = b; }
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  a = 0.0; b = 0.0;
+  for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) { a += sh[0][w]; b += sh[1][w]; }
+  const double unscaled = a / static_cast<double>(count);
+  *gtau = variant == FC_FASTCLIP_V3 ? b / static_cast<double>(count) + 2.0 * rho + tau * unscaled : unscaled;
+}
+
+int fc_grad_tau(int32_t variant, int32_t count, int64_t batch, const double* u1, const double* u2, const double* dsum1,
+                const double* dsum2, const double* t1, const double* t2, double eps, double rho, double tau,
+                int64_t n_train, double* gtau, double* gt1, double* gt2, void* stream) {
+  return guarded([&] {
+    if (variant < 0 || variant > 6) throw FcError{FC_ERR_CONFIG, "unknown variant"};
+    if (variant == FC_SOGCLR || variant == FC_FASTCLIP_V1) throw FcError{FC_ERR_CONFIG, "constant-tau variant has no tau gradient"};
+    if (count < 1 || batch < 2) throw FcError{FC_ERR_DEGENERATE_BATCH, "grad_tau: empty slice or batch < 2"};
+    const bool indiv = variant == FC_ISOGCLR || variant == FC_FASTCLIP_V2;
+    if (!u1 || !u2 || !dsum1 || !dsum2 || (indiv && (!t1 || !t2 || !gt1 || !gt2 || n_train < 2)) || (!indiv && !gtau))
+      throw FcError{FC_ERR_SHAPE, "grad_tau: null pointer / n_train"};
+    if (eps < 0.0) throw FcError{FC_ERR_DOMAIN, "epsilon must be non-negative"};
+    fc_grad_tau_kernel<<<1, 1024, 0, static_cast<cudaStream_t>(stream)>>>(variant, count, batch, u1, u2, dsum1, dsum2, t1, t2,
+                                                                          eps, rho, tau, n_train, gtau, gt1, gt2);
+    FC_CUDA(cudaGetLastError());
+  });
+}
+
 int fc_nccl_unique_id(uint8_t out[128]) {
   return guarded([&] {
     ncclUniqueId id;

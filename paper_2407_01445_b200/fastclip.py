@@ -106,6 +106,7 @@ def lib():
         L.fc_embedding_cotangents.argtypes = [P, P, I32, I32, P, P, P, P, I32, I32, P, P, P]
         L.fc_temperature_step.argtypes = [DP, DP, LP, D, D, D, D, D, D, D, DP]
         L.fc_table_update.argtypes = [P, P, I64, P, P, P, I32, D, P, P, P, P]
+        L.fc_grad_tau.argtypes = [I32, I32, I64, P, P, P, P, P, P, D, D, D, I64, P, P, P, P]
         L.fc_last_error.restype = C.c_char_p
         _lib = L
     return _lib
@@ -117,6 +118,7 @@ EXPORTED = [
     "fc_table_upload", "fc_tau_state_get", "fc_tau_state_set", "fc_kernels_per_step",
     "fc_debug_similarity", "fc_last_error", "fc_set_phase_timing", "fc_phase_times", "fc_g_values",
     "fc_embedding_cotangents", "fc_temperature_step", "fc_table_update",
+    "fc_grad_tau",
 ]
 PHASES = ["allgather_e", "prep", "pass1_stats", "tables_tau", "pass2_q", "grad_gemm"]
 
@@ -344,6 +346,24 @@ def table_update(u1, u2, ids, g1, g2, gamma: float):
     _check(lib().fc_table_update(_dptr(u1), _dptr(u2), n, _dptr(ids), _dptr(g1), _dptr(g2), cnt, gamma, _dptr(o1),
                                  _dptr(o2), _dptr(status), C.c_void_p(stream.cuda_stream)))
     return o1, o2, int(status.item())
+
+
+def grad_tau(variant, u1, u2, dsum1, dsum2, batch: int, eps: float, rho: float = 0.0, tau: float = 0.0,
+             t1=None, t2=None, n_train: int = 0):
+    """engine::grad_tau_* (engine.cpp:208-266) from a worker's u snapshot and dtau sums (CUDA fp64):
+    a Python float G_tau,k for v0 / v3 / MBCL, or (gt1, gt2) CUDA tensors for v2 / iSogCLR."""
+    import torch
+    v = VARIANTS[variant] if isinstance(variant, str) else int(variant)
+    n = u1.numel()
+    indiv = v in (VARIANTS["isogclr"], VARIANTS["fastclip_v2"])
+    g = torch.zeros(1, device=u1.device, dtype=torch.float64)
+    gt1 = torch.empty(n, device=u1.device, dtype=torch.float64) if indiv else None
+    gt2 = torch.empty(n, device=u1.device, dtype=torch.float64) if indiv else None
+    stream = torch.cuda.current_stream(u1.device)
+    ptr = lambda x: _dptr(x) if x is not None else None
+    _check(lib().fc_grad_tau(v, n, int(batch), _dptr(u1), _dptr(u2), _dptr(dsum1), _dptr(dsum2), ptr(t1), ptr(t2), eps,
+                             rho, tau, int(n_train), _dptr(g), ptr(gt1), ptr(gt2), C.c_void_p(stream.cuda_stream)))
+    return (gt1, gt2) if indiv else float(g.item())
 
 
 def debug_similarity(a, b):

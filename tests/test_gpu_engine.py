@@ -129,3 +129,31 @@ def test_table_update_matches_state_semantics():
     assert status == 2
     with pytest.raises(P.FastclipError):
         P.table_update(U1, U2, d(ids), d(g1), d(g2), 1.5)   # gamma outside (0, 1]
+
+
+@pytest.mark.parametrize("variant", ["fastclip_v3", "fastclip_v0", "openclip_mbcl", "fastclip_v2"])
+def test_grad_tau_composes_to_the_step_gradient(variant):
+    # fc_g_values (dtau sums at tau^t) + fc_grad_tau on the oracle's u snapshot reproduce the
+    # oracle step's G_tau (v0 / v3 / MBCL) or per-index gtau1 / gtau2 (v2), K = 1
+    import torch
+    import paper_2407_01445_b200 as P
+    B, d, N = 384, 96, 4000
+    cfg = O.default_config(variant, N)
+    st = O.new_state(cfg)
+    st.u1[:] = S.warm_u(N, 0)
+    st.u2[:] = S.warm_u(N, 1)
+    b1, b2 = S.embeddings(B, d, 12)
+    ids = S.ids(B, N, 12)
+    tau = st.tau
+    ref = O.step(cfg, st, 1, S.bf16_to_f32(b1).astype(np.float64), S.bf16_to_f32(b2).astype(np.float64), ids, 0.6, 1e-14)
+    cuda = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()
+    gv = P.g_values(to_dev_bf16(b1), to_dev_bf16(b2), cuda(ref["t1"]), cuda(ref["t2"]), 0, B)
+    out = P.grad_tau(variant, cuda(ref["u1"]), cuda(ref["u2"]), gv["dsum1"], gv["dsum2"], B, 1e-14, cfg["rho"], tau,
+                     cuda(ref["t1"]), cuda(ref["t2"]), N)
+    if variant == "fastclip_v2":
+        # per-index terms log(eps + u) + rho + t dsum / (eps + u) can cancel to ~0 for single
+        # indices, so the error is taken relative to the largest |gtau| (numdiff.hpp:45-56 floor)
+        for got, r in ((out[0], ref["gtau1"]), (out[1], ref["gtau2"])):
+            assert np.max(np.abs(got.cpu().numpy() - r)) <= 1e-3 * np.max(np.abs(r))
+    else:
+        assert abs(out - ref["gtau"]) <= 1e-3 * abs(ref["gtau"])
