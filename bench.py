@@ -117,9 +117,14 @@ def cpu_reference_sample(B, d, N, variant, steps, warmup, log):
     the reference sources) on the box's host cores. The reference parallelises over
     data-parallel workers (one std::thread each, fabric.cpp:237-258); we run W workers,
     the largest divisor of B not above nproc. Each worker computes the three full S
-    products of its step (engine.cpp:159,:83,:185) plus its anchors' loops; a bounded
-    sample restricts every worker to La anchors and the per-anchor cost is extrapolated
-    linearly to the full local slice from two sample sizes."""
+    products of its step (engine.cpp:159,:83,:185) plus its anchors' loops (~0.2-0.3 s per
+    anchor: the cotangent loops walk column-major rows). The per-anchor cost is calibrated
+    once from runs with every worker on 1 and on 65 anchors (the S products' run-to-run noise,
+    ~1 s, spread over 64 anchors); each timed step is a bounded sample (every worker on
+    2 anchors, the three full S products kept) extrapolated to the full slice with that cost.
+    A full B = 5120 step measured directly on 8 host threads took 202 s, ~1.5x the
+    extrapolation (the per-anchor cost grows with the slice: cache misses of the column-major
+    walks), so the reported CPU rate is an upper bound and the speed-up against it conservative."""
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import oracle as O
     from paper_2407_01445_b200 import synthetic as S
@@ -138,9 +143,10 @@ def cpu_reference_sample(B, d, N, variant, steps, warmup, log):
         O.step(cfg, st, W, E1, E2, ids, 0.6, 1e-14, backend="ref_fast", local_limit=La)
         return time.perf_counter() - t
 
+    La = min(Bl, 65)
     t1 = run(1)
-    t3 = run(3)
-    per_anchor = max(0.0, (t3 - t1) / 2.0)
+    t_big = run(La)
+    per_anchor = max(0.0, (t_big - t1) / max(1, La - 1))
     fixed = max(0.0, t1 - per_anchor)
     est = []
     for i in range(warmup + steps):
@@ -149,9 +155,9 @@ def cpu_reference_sample(B, d, N, variant, steps, warmup, log):
             est.append(ts + (Bl - 2) * per_anchor)
     t_step = float(np.mean(est)) if est else fixed + Bl * per_anchor
     sample = (f"reference TUs (oracle/_ref) step at B={B}, d={d} as {W} fabric workers x {Bl} anchors; "
-              f"each sample restricts every worker to La anchors (3 full S products kept); per-anchor "
-              f"cost {per_anchor:.3f}s from La=1,3 samples, extrapolated to {Bl} anchors")
-    log(f"[cpu] W={W} t(La=1)={t1:.2f}s t(La=3)={t3:.2f}s -> est step {t_step:.1f}s")
+              f"per-anchor cost {per_anchor * 1e3:.0f}ms from runs with every worker on 1 and {La} anchors; each "
+              f"timed step restricts every worker to 2 anchors (3 full S products kept), extrapolated to {Bl}")
+    log(f"[cpu] W={W} t(La=1)={t1:.2f}s t(La={La})={t_big:.2f}s -> est step {t_step:.1f}s")
     return {"value": 1.0 / t_step, "unit": UNIT, "cores": W, "kind": "reference", "sample": sample,
             "est_step_s": t_step, "fixed_s": fixed, "per_anchor_s": per_anchor}
 
