@@ -5,8 +5,9 @@
 
 One step = the per-rank FastCLIP-v3 loss step (trainer.cpp:427-589) at global B = 5120,
 d = 512, N = 2.7M-entry u table, synthetic bf16 unit-norm embeddings. N > 1: launched with
-torch.distributed.run, one rank per GPU, global batch fixed (strong scaling), NCCL
-all-gathers of E and of the per-sample scalars plus one scalar all-reduce per step.
+torch.distributed.run, one rank per GPU, global batch fixed (strong scaling); per step the
+ranks all-gather E and the per-sample scalar payload through NVLink peer memory (NCCL only
+for the one-time set-up, or as the fallback when GPUs cannot map each other's memory).
 
 `value` is device-timed (CUDA events around each step, L2 flushed between steps, inputs
 resident in HBM), max over ranks; `e2e` times the same step through the public API with
@@ -202,7 +203,8 @@ def workload_config(args, world):
                         f"N={args.n_train} u table (BASELINE.json metric config)",
             "variant": args.variant, "global_batch": args.batch, "local_batch": args.batch // world,
             "dim": args.dim, "n_train": args.n_train, "world": world,
-            "parallelism": f"dp{world} (anchor slices, NCCL all-gather E + scalars)",
+            "parallelism": f"dp{world} (anchor slices; NVLink peer all-gathers of E and the scalar payload)" if world > 1
+                           else "dp1",
             "l2": "flushed between timed steps (256 MiB memset)", "tables": "warm u (log10 u ~ U[-8,0])"}
 
 
