@@ -5,7 +5,7 @@ tests/test_gpu_step.py: g, u, loss, tau, G_tau max rel 1e-3; dE norm-relative 1e
 indexing bit-exact (untouched entries identical, touched entries at the right ids).
 
 Shapes: the north star (v3, B = 5120, d = 512, N = 2.7M); config 2's global batch on one GPU
-(v2, B = 8192, N = 9.1M); config 3's width (v3, d = 768); config 4 (v0 and v2, B = 4096,
+(v2, B = 8192, N = 9.1M); config 3 (v3, d = 768, N = 2.7M and the full N = 315M); config 4 (v0 and v2, B = 4096,
 d = 1024); config 5's next size up (v3, B = 16384)."""
 import numpy as np
 import pytest
@@ -43,6 +43,7 @@ def _check_full(res, tabs, st, what, ids_of):
     ("fastclip_v3", 5120, 512, 2_700_000, 2),    # north star / BASELINE configs[1]
     ("fastclip_v2", 8192, 512, 9_100_000, 1),    # config 2's global batch at K = 1
     ("fastclip_v3", 5120, 768, 2_700_000, 1),    # config 3's width
+    ("fastclip_v3", 5120, 768, 315_000_000, 1),  # config 3 in full: LAION-scale u tables (2 x 2.5 GB fp64)
     ("fastclip_v0", 4096, 1024, 2_700_000, 1),   # config 4
     ("fastclip_v2", 4096, 1024, 2_700_000, 1),   # config 4
     ("fastclip_v3", 16384, 512, 2_700_000, 1),   # config 5 (B = 16k)
