@@ -318,11 +318,12 @@ def main():
         e1, e2, ids = dev_sets[i % n_sets]
         step.step(e1, e2, ids, gamma, eps, de1, de2, stream)
     torch.cuda.synchronize()
-    phase_sum = {k: 0.0 for k in P.fastclip.PHASES}
+    # per-phase median over the timed steps (robust to a single late event record)
+    phase_runs = {k: [] for k in P.fastclip.PHASES}
     for i in range(args.steps):
         for k, v in step.phase_times(i).items():
-            phase_sum[k] += v
-    phases = {k: v / args.steps for k, v in phase_sum.items()}
+            phase_runs[k].append(v)
+    phases = {k: (statistics.median(v) if v else 0.0) for k, v in phase_runs.items()}
     step.disable_phase_timing()
     note("phase timing done")
 
