@@ -2,22 +2,18 @@
 //
 //   dE1[L] = c (Q'_R  E2[G] - r o E2[L]),   dE2[L] = c (Q'_C  E1[G] - r o E1[L])
 // (engine.cpp:77-121 regrouped: Q[i,j] = P1[i,j] + P2[j,i], r_i = a_i S1_i + b_i S2_i,
-//  c = 1/(Bl (B-1))). A = Q' (bf16, K-major, written by the Q pass; at K = 1 the dE2 GEMM
-// reads Q^T through an MN-major A operand), B = E (bf16, N = d contiguous => MN-major UMMA
-// operand), fp32 accumulation in TMEM.
+//  c = 1/(Bl (B-1))). A = Q' (bf16, K-major; at K = 1 the dE2 GEMM reads Q^T through an
+// MN-major A operand), B = E (bf16, N = d contiguous => MN-major UMMA operand), fp32
+// accumulation in TMEM.
 //
 // The GEMM is skinny (N = d = 512, K = B = 5120) and both operands stream, so its limit is
-// the L2 -> SM operand bandwidth, not the tensor pipe: a 256 x 256 pair tile moves 64 KB per
-// 512 MMA cycles, ~1.5x what the L2 slices deliver chip-wide. This kernel therefore
-//   * gives each CTA pair (cta_group::2) a 256 x 512 tile: two N = 256 accumulators that
-//     fill TMEM, sharing every A k-block (48 KB per 1024 MMA cycles per CTA), and
-//   * (kPairs = 2) runs two pairs as a cluster of 4 on row blocks that share the B operand:
-//     each B slab is fetched once and multicast into both pairs (32 KB of L2 reads per CTA
-//     per 1024 MMA cycles, half the original per-MMA traffic).
-// Schedule: stream-K over (cluster tile, k-block) -- every cluster runs the same number of
-// k-blocks (+-1); partial tiles are reduced with TMA reduce-add into the gradient rows,
-// which the pass-1 kernel zeroed earlier in the step; the unit holding k-block 0 of a tile
-// also adds the local term -c r o E_L.
+// the L2 -> SM operand bandwidth: each CTA pair (cta_group::2) owns a 256 x 512 tile -- two
+// N = 256 accumulators that fill TMEM and share every A k-block (48 KB per 1024 MMA cycles
+// per CTA). Schedule: stream-K over (tile, k-block) -- every pair runs the same number of
+// k-blocks (+-1); partial tiles are reduced with TMA reduce-add into the gradient rows, which
+// a side-branch kernel zeroed earlier in the step; the unit holding k-block 0 of a tile also
+// adds the local term -c r o E_L.
+//
 #include "kernels.cuh"
 #include "sm100.cuh"
 
@@ -51,7 +47,7 @@ __device__ __forceinline__ GSmem gcarve(uint8_t* base) {
   return L;
 }
 
-// cluster tile -> (segment, row block of 256 * kPairs rows, column block of 512)
+// pair tile -> (segment, row block of 256 rows, column block of 512)
 __device__ __forceinline__ void tile_decode(const GemmParams& p, int t, int& s, int& mb, int& nb) {
   const int per_seg0 = p.n_mb[0] * p.n_nb;
   s = t < per_seg0 ? 0 : 1;
@@ -60,14 +56,14 @@ __device__ __forceinline__ void tile_decode(const GemmParams& p, int t, int& s, 
   mb = local / p.n_nb;
 }
 
-// The cluster's stream-K work: contiguous range of (tile, k-block) units.
+// The pair's stream-K work: contiguous range of (tile, k-block) units.
 struct UnitIter {
   int KB;
   long long u, u1;
-  __device__ UnitIter(const GemmParams& p, int cluster, int n_clusters) {
+  __device__ UnitIter(const GemmParams& p, int pair) {
     KB = p.kb_total;
-    u = p.unit_lo[cluster];
-    u1 = p.unit_lo[cluster + 1];
+    u = p.unit_lo[pair];
+    u1 = p.unit_lo[pair + 1];
   }
   __device__ bool next(int& tile, int& kb0, int& kb1) {
     if (u >= u1) return false;
@@ -81,26 +77,23 @@ struct UnitIter {
 
 }  // namespace
 
-template <int kPairs>
 __global__ void __launch_bounds__(kGemmThreads, 1)
     grad_gemm_kernel(const __grid_constant__ GemmParams p, const __grid_constant__ CUtensorMap mapQ0,
                      const __grid_constant__ CUtensorMap mapX0, const __grid_constant__ CUtensorMap mapQ1,
                      const __grid_constant__ CUtensorMap mapX1, const __grid_constant__ CUtensorMap mapO0,
                      const __grid_constant__ CUtensorMap mapO1) {
   extern __shared__ uint8_t smem_raw[];
-  long long g_entry = 0;
-  if (p.debug >= 9) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_entry));
+#ifdef FC_PROFILE
+  long long g_entry;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_entry));
+#endif
   const GSmem L = gcarve(smem_raw);
   griddep_launch_dependents();
   const uint32_t warp = threadIdx.x / 32;
   const uint32_t lane = lane_id();
-  const uint32_t crank = cluster_ctarank();          // 0 .. 2*kPairs-1
-  const uint32_t prank = crank & 1;                  // rank inside the CTA pair
-  const uint32_t pc = crank >> 1;                    // pair index inside the cluster
-  const int cluster = blockIdx.x / (2 * kPairs);
-  const int n_clusters = gridDim.x / (2 * kPairs);
-  constexpr uint16_t kAllCtas = static_cast<uint16_t>((1u << (2 * kPairs)) - 1);
-  const uint16_t pair_mask = static_cast<uint16_t>(0x3u << (2 * pc));
+  const uint32_t prank = cluster_ctarank();          // rank inside the CTA pair
+  const int pair = blockIdx.x / 2;
+  constexpr uint16_t kPairMask = 0x3;
 
   constexpr uint32_t kProdWarp = kGemmEpiWarps, kMmaWarp = kGemmEpiWarps + 1;
   if (warp == kProdWarp && lane == 0) {
@@ -113,8 +106,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   }
   if (warp == kMmaWarp && lane == 0) {
     for (int i = 0; i < kGemmStages; ++i) {
-      mbar_init(&L.full[i], 2);          // both producers of the pair (leader's barrier is used)
-      mbar_init(&L.empty[i], kPairs);    // one MMA commit per pair of the cluster (multicast B)
+      mbar_init(&L.full[i], 2);           // both producers of the pair (leader's barrier is used)
+      mbar_init(&L.empty[i], 1);          // MMA commit (multicast to both CTAs)
     }
     mbar_init(&L.tfull[0], 1);
     mbar_init(&L.tempty[0], 2 * kGemmEpiWarps);
@@ -130,27 +123,27 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     // ===================== TMA producer (whole warp walks, lane 0 issues) =====================
     const bool issuer = lane == 0;
     uint32_t stage = 0, phase = 0;
-    griddep_wait();   // Q' comes from the pass-2 kernel (barrier init / TMEM alloc overlapped it)
-    UnitIter iter(p, cluster, n_clusters);
+    griddep_wait();   // Q' / X come from the preceding kernels (barrier init / TMEM alloc overlapped them)
+    UnitIter iter(p, pair);
     int tile, kb0, kb1;
     while (iter.next(tile, kb0, kb1)) {
       int s, mb, nb;
       tile_decode(p, tile, s, mb, nb);
       const CUtensorMap* mq = s ? &mapQ1 : &mapQ0;
       const CUtensorMap* mx = s ? &mapX1 : &mapX0;
-      const int a_row = (mb * kPairs + static_cast<int>(pc)) * kPairM + static_cast<int>(prank) * kCtaM;
+      const int a_row = mb * kPairM + static_cast<int>(prank) * kCtaM;
       const int n_blk = nb * kGemmN;
       const bool a_mn = p.seg[s].a_mn_major != 0;
       const bool half1 = n_blk + kPairN < p.d;   // this block's second N half has columns
-      const uint32_t bytes = 2 * (kStageBytesA + (half1 ? 2 : 1) * kStageBytesB);
+      const uint32_t b_bytes = 2 * (half1 ? 2 : 1) * kStageBytesB;
       for (int kb = kb0; kb < kb1; ++kb) {
         mbar_wait(&L.empty[stage], phase ^ 1);
         if (issuer) {
-          if (prank == 0) mbar_arrive_expect_tx(&L.full[stage], bytes);
-          else mbar_arrive_cluster(&L.full[stage], crank & ~1u);
           uint8_t* sa = L.a + stage * kStageBytesA;
           uint8_t* sb = L.b + stage * kGemmStageBytesB;
           const int k0 = kb * kBlockK;
+          if (prank == 0) mbar_arrive_expect_tx(&L.full[stage], b_bytes + 2 * kStageBytesA);
+          else mbar_arrive_cluster(&L.full[stage], 0);
           if (a_mn) {
             // A = Q^T: two 64(M) x 64(K) swizzle atoms of the row-major Q (K = rows of Q)
             tma_load_2d_pair(mq, &L.full[stage], sa, a_row, k0);
@@ -159,24 +152,11 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             tma_load_2d_pair(mq, &L.full[stage], sa, k0, a_row);
           }
           // B slab h of this CTA: columns n_blk + h*256 + prank*128 .. +128 (two 64-wide atoms)
-          if constexpr (kPairs == 1) {
-            for (int h = 0; h < (half1 ? 2 : 1); ++h) {
-              const int n0 = n_blk + h * kPairN + static_cast<int>(prank) * (kPairN / 2);
-              uint8_t* dst = sb + h * kStageBytesB;
-              tma_load_2d_pair(mx, &L.full[stage], dst, n0, k0);
-              tma_load_2d_pair(mx, &L.full[stage], dst + kStageBytesB / 2, n0 + 64, k0);
-            }
-          } else {
-            // pair pc fetches half h = pc once and multicasts it into the same-rank CTA of
-            // both pairs (the other pair fetches the other half)
-            const int h = static_cast<int>(pc);
-            if (h == 0 || half1) {
-              const uint16_t mask = static_cast<uint16_t>((1u << prank) | (1u << (prank + 2)));
-              const int n0 = n_blk + h * kPairN + static_cast<int>(prank) * (kPairN / 2);
-              uint8_t* dst = sb + h * kStageBytesB;
-              tma_load_2d_pair_mc(mx, &L.full[stage], dst, n0, k0, mask);
-              tma_load_2d_pair_mc(mx, &L.full[stage], dst + kStageBytesB / 2, n0 + 64, k0, mask);
-            }
+          for (int h = 0; h < (half1 ? 2 : 1); ++h) {
+            const int n0 = n_blk + h * kPairN + static_cast<int>(prank) * (kPairN / 2);
+            uint8_t* dst = sb + h * kStageBytesB;
+            tma_load_2d_pair(mx, &L.full[stage], dst, n0, k0);
+            tma_load_2d_pair(mx, &L.full[stage], dst + kStageBytesB / 2, n0 + 64, k0);
           }
         }
         __syncwarp();
@@ -195,9 +175,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       constexpr uint32_t kBHalf = kStageBytesB >> 4;   // descriptor offset of N half 1
       uint32_t stage = 0, phase = 0;
       int it = 0;
-      const bool prof = p.debug >= 9;
+#ifdef FC_PROFILE
       long long c0 = clock64(), c_tempty = 0, c_full = 0, c_first = -1;
-      UnitIter iter(p, cluster, n_clusters);
+#endif
+      UnitIter iter(p, pair);
       int tile, kb0, kb1;
       while (iter.next(tile, kb0, kb1)) {
         int s, mb, nb;
@@ -207,17 +188,23 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         const uint32_t idesc = a_mn ? idesc_mn : idesc_k;
         const uint64_t a_desc0 = a_mn ? a_desc_mn : a_desc_k;
         const uint32_t a_kstep = a_mn ? (2048 >> 4) : (32 >> 4);   // descriptor units per UMMA_K
-        long long t0 = prof ? clock64() : 0;
+#ifdef FC_PROFILE
+        long long t0 = clock64();
+#endif
         mbar_wait(&L.tempty[0], (it & 1) ^ 1);   // the epilogue drained the previous unit
-        if (prof) c_tempty += clock64() - t0;
+#ifdef FC_PROFILE
+        c_tempty += clock64() - t0;
+#endif
         tc_fence_after();
         for (int kb = kb0; kb < kb1; ++kb) {
-          long long t1 = prof ? clock64() : 0;
+#ifdef FC_PROFILE
+          long long t1 = clock64();
+#endif
           mbar_wait(&L.full[stage], phase);
-          if (prof) {
-            c_full += clock64() - t1;
-            if (c_first < 0) c_first = clock64() - c0;
-          }
+#ifdef FC_PROFILE
+          c_full += clock64() - t1;
+          if (c_first < 0) c_first = clock64() - c0;
+#endif
           tc_fence_after();
           if (elect_one()) {
             const uint64_t ad = a_desc0 + static_cast<uint64_t>((stage * kStageBytesA) >> 4);
@@ -228,21 +215,23 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
               mma_bf16_pair(tmem_base, ad + k * a_kstep, bd + 128 * k, idesc, accum);
               if (half1) mma_bf16_pair(tmem_base + kPairN, ad + k * a_kstep, bd + kBHalf + 128 * k, idesc, accum);
             }
-            mma_commit_pair(&L.empty[stage], kPairs == 1 ? pair_mask : kAllCtas);
-            if (kb == kb1 - 1) mma_commit_pair(&L.tfull[0], pair_mask);
+            mma_commit_pair(&L.empty[stage], kPairMask);
+            if (kb == kb1 - 1) mma_commit_pair(&L.tfull[0], kPairMask);
           }
           __syncwarp();
           if (++stage == kGemmStages) { stage = 0; phase ^= 1; }
         }
         ++it;
       }
-      if (prof && lane == 0) {
+#ifdef FC_PROFILE
+      if (lane == 0 && p.dbg_out) {
         long long* o = p.dbg_out + blockIdx.x * 16;
         o[0] = clock64() - c0; o[1] = c_tempty; o[2] = c_full; o[3] = c_first; o[4] = it;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(o[5]));
       }
+#endif
     }
-  } else {
+  } else if (warp < kGemmEpiWarps) {
     // ===================== epilogue =====================
     // Warp w owns 32 rows (TMEM lane quarter w & 3) x 256 columns (N half w >> 2) of the
     // pair's 256 x 512 accumulator: 8 chunks of 32 columns, TMEM -> registers ->
@@ -252,22 +241,21 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     const uint32_t q4 = warp & 3;
     const uint32_t cg = warp >> 2;
     uint8_t* stage_out = L.out + warp * kGemmStageOut;
-    const uint32_t leader = crank & ~1u;
     // r_i (per-anchor kernel) and the X rows are read before the first accumulator wait:
     // wait for the predecessor grid like the producer does (programmatic launch)
     griddep_wait();
-    const bool eprof = p.debug >= 9 && warp == 0;
+#ifdef FC_PROFILE
     long long e0 = clock64(), e_wait = 0;
+#endif
     int it = 0;
-    UnitIter iter(p, cluster, n_clusters);
+    UnitIter iter(p, pair);
     int tile, kb0, kb1;
     while (iter.next(tile, kb0, kb1)) {
       int s, mb, nb;
       tile_decode(p, tile, s, mb, nb);
       const GemmSeg& sg = p.seg[s];
       const CUtensorMap* mo = s ? &mapO1 : &mapO0;
-      const int row0 = (mb * kPairs + static_cast<int>(pc)) * kPairM + static_cast<int>(prank) * kCtaM +
-                       static_cast<int>(q4) * 32;
+      const int row0 = mb * kPairM + static_cast<int>(prank) * kCtaM + static_cast<int>(q4) * 32;
       const int r_loc = row0 + static_cast<int>(lane);
       const bool row_ok = r_loc < sg.rows;
       // the unit holding k-block 0 adds the local term -c r o X_L exactly once per tile; its X
@@ -276,36 +264,40 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       const float cr = (row_ok && with_r) ? p.scale * sg.r[r_loc] : 0.f;
       const uint4* xrow = reinterpret_cast<const uint4*>(sg.x + static_cast<size_t>(sg.x_row0 + (row_ok ? r_loc : 0)) * p.d);
       uint4 xn[4];
-      auto load_x = [&](int c) {
-        const int col0 = nb * kGemmN + static_cast<int>(cg) * kEpiCols + c * 32;
+      auto load_x = [&](int cc) {
+        const int col0 = nb * kGemmN + static_cast<int>(cg) * kEpiCols + cc * 32;
 #pragma unroll
         for (int q = 0; q < 4; ++q)
           xn[q] = (with_r && row_ok && col0 + 8 * q < p.d) ? __ldg(xrow + col0 / 8 + q) : make_uint4(0u, 0u, 0u, 0u);
       };
       load_x(0);
-      long long t0 = eprof ? clock64() : 0;
+#ifdef FC_PROFILE
+      long long t0 = clock64();
+#endif
       mbar_wait(&L.tfull[0], it & 1);
-      if (eprof) e_wait += clock64() - t0;
+#ifdef FC_PROFILE
+      e_wait += clock64() - t0;
+#endif
       tc_fence_after();
 #pragma unroll 1
-      for (int c = 0; c < kChunks; ++c) {
-        const int tcol = static_cast<int>(cg) * kEpiCols + c * 32;   // column inside the 512-wide block
+      for (int cc = 0; cc < kChunks; ++cc) {
+        const int tcol = static_cast<int>(cg) * kEpiCols + cc * 32;   // column inside the 512-wide block
         const int col0 = nb * kGemmN + tcol;
         const bool live = col0 < p.d && row0 < sg.rows;          // warp-uniform
         uint32_t r[32];
-        if (live || c == kChunks - 1) {
+        if (live || cc == kChunks - 1) {
           tmem_ld_32x32b_x32(tmem_base + ((q4 * 32u) << 16) + static_cast<uint32_t>(tcol), r);
           tmem_ld_wait();
         }
-        if (c == kChunks - 1) {   // this warp's accumulator slice is in registers: release it
+        if (cc == kChunks - 1) {   // this warp's accumulator slice is in registers: release it
           tc_fence_before();
           __syncwarp();
           if (lane == 0) {
             if (prank == 0) mbar_arrive(&L.tempty[0]);
-            else mbar_arrive_cluster(&L.tempty[0], leader);
+            else mbar_arrive_cluster(&L.tempty[0], 0);
           }
         }
-        if (!live || (p.debug != 0 && p.debug < 3)) continue;
+        if (!live) continue;
         float v[32];
 #pragma unroll
         for (int k = 0; k < 32; ++k) v[k] = p.scale * __uint_as_float(r[k]);
@@ -313,15 +305,15 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           uint4 xc[4];
 #pragma unroll
           for (int q = 0; q < 4; ++q) xc[q] = xn[q];
-          if (c + 1 < kChunks) load_x(c + 1);
+          if (cc + 1 < kChunks) load_x(cc + 1);
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
             const uint32_t ww[4] = {xc[q].x, xc[q].y, xc[q].z, xc[q].w};
 #pragma unroll
-            for (int t = 0; t < 4; ++t) {
-              const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&ww[t]));
-              v[q * 8 + 2 * t] = fmaf(-cr, f.x, v[q * 8 + 2 * t]);
-              v[q * 8 + 2 * t + 1] = fmaf(-cr, f.y, v[q * 8 + 2 * t + 1]);
+            for (int u = 0; u < 4; ++u) {
+              const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&ww[u]));
+              v[q * 8 + 2 * u] = fmaf(-cr, f.x, v[q * 8 + 2 * u]);
+              v[q * 8 + 2 * u + 1] = fmaf(-cr, f.y, v[q * 8 + 2 * u + 1]);
             }
           }
         }
@@ -336,20 +328,21 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) {
-          if (p.debug == 3 || p.debug == 10) tma_store_2d(mo, stage_out, col0, row0);   // experiment: plain store
-          else tma_reduce_add_2d(mo, stage_out, col0, row0);
+          tma_reduce_add_2d(mo, stage_out, col0, row0);
           bulk_commit();
         }
       }
       ++it;
     }
     if (lane == 0) bulk_wait0();
-    if (eprof && lane == 0) {
+#ifdef FC_PROFILE
+    if (warp == 0 && lane == 0 && p.dbg_out) {
       long long* o = p.dbg_out + blockIdx.x * 16 + 8;
       o[0] = clock64() - e0; o[1] = e_wait;
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(o[2]));
       o[3] = g_entry;
     }
+#endif
   }
 
   __syncwarp();   // single-lane producer / MMA roles reconverge before the aligned cluster barrier
@@ -361,9 +354,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   if (blockIdx.x == 0 && static_cast<int>(threadIdx.x) < 4 * p.n_reset && p.reset_at_exit) p.reset_at_exit[threadIdx.x] = 0.f;
 }
 
-namespace {
-template <int kPairs>
-cudaError_t launch_gemm_t(bool pdl, const GemmParams& p, const CUtensorMap* mapQ, const CUtensorMap* mapX,
+cudaError_t launch_gemm(bool pdl, const GemmParams& p, const CUtensorMap* mapQ, const CUtensorMap* mapX,
                           const CUtensorMap* mapOut, int grid, cudaStream_t s) {
   const CUtensorMap& q1 = p.nseg > 1 ? mapQ[1] : mapQ[0];
   const CUtensorMap& x1 = p.nseg > 1 ? mapX[1] : mapX[0];
@@ -371,7 +362,7 @@ cudaError_t launch_gemm_t(bool pdl, const GemmParams& p, const CUtensorMap* mapQ
   cudaLaunchConfig_t cfg{};
   cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = 2 * kPairs;
+  attr[0].val.clusterDim.x = 2;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
   attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -382,37 +373,11 @@ cudaError_t launch_gemm_t(bool pdl, const GemmParams& p, const CUtensorMap* mapQ
   cfg.stream = s;
   cfg.attrs = attr;
   cfg.numAttrs = 2;
-  return cudaLaunchKernelEx(&cfg, grad_gemm_kernel<kPairs>, p, mapQ[0], mapX[0], q1, x1, mapOut[0], o1);
-}
-}  // namespace
-
-cudaError_t gemm_max_active_clusters(int pairs_per_cluster, int* n) {
-  cudaLaunchConfig_t cfg{};
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = 2 * pairs_per_cluster;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  cfg.gridDim = dim3(148, 1, 1);
-  cfg.blockDim = dim3(kGemmThreads, 1, 1);
-  cfg.dynamicSmemBytes = kGemmSmemBytes;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  if (pairs_per_cluster == 2) return cudaOccupancyMaxActiveClusters(n, grad_gemm_kernel<2>, &cfg);
-  return cudaOccupancyMaxActiveClusters(n, grad_gemm_kernel<1>, &cfg);
+  return cudaLaunchKernelEx(&cfg, grad_gemm_kernel, p, mapQ[0], mapX[0], q1, x1, mapOut[0], o1);
 }
 
 cudaError_t gemm_set_smem() {
-  cudaError_t e = cudaFuncSetAttribute(grad_gemm_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kGemmSmemBytes);
-  if (e == cudaSuccess)
-    e = cudaFuncSetAttribute(grad_gemm_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, kGemmSmemBytes);
-  return e;
-}
-
-cudaError_t launch_gemm(bool pdl, const GemmParams& p, const CUtensorMap* mapQ, const CUtensorMap* mapX,
-                        const CUtensorMap* mapOut, int grid, cudaStream_t s) {
-  if (p.pairs_per_cluster == 2) return launch_gemm_t<2>(pdl, p, mapQ, mapX, mapOut, grid, s);
-  return launch_gemm_t<1>(pdl, p, mapQ, mapX, mapOut, grid, s);
+  return cudaFuncSetAttribute(grad_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kGemmSmemBytes);
 }
 
 }  // namespace fc

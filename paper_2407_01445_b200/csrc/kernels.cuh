@@ -81,6 +81,11 @@ struct SimParams {
   float2* col_partial;
   int n_slots;
   int fuse_fast;
+  // pass 1 also zeroes the step's gradient outputs (the GEMM reduce-adds every stream-K unit
+  // into them): the epilogue warps do it while the first tiles' MMAs run
+  float4* zero0;
+  float4* zero1;
+  long long zero_n4;
   int debug;                   // perf experiments: 1 = skip epilogue math, 2 = also skip B loads
   long long* dbg_out;          // debug == 9: per-pair MMA-warp cycle counters [pair][8]
 };
@@ -100,19 +105,16 @@ struct GemmParams {
   int d;
   int n_mb[2];
   int n_nb;
-  int n_tiles;       // sum over segments of n_mb * n_nb (cluster tiles: 256*pairs_per_cluster x 512)
-  int pairs_per_cluster;   // 1, or 2: two pairs share (multicast) the B operand
-  // stream-K partition: cluster c runs units [unit_lo[c], unit_lo[c+1]) of the (tile, k-block)
+  int n_tiles;       // sum over segments of n_mb * n_nb (pair tiles: 256 x 512)
+  // stream-K partition: pair c runs units [unit_lo[c], unit_lo[c+1]) of the (tile, k-block)
   // sequence; the host balances k-blocks + per-unit epilogue cost (a unit boundary costs one
-  // accumulator drain), so clusters with two units get fewer k-blocks
+  // accumulator drain), so pairs with two units get fewer k-blocks
   int unit_lo[kMaxGemmClusters + 1];
   int kb_total;      // K blocks of 64 over ldq
   float scale;       // 1 / (Bl (B-1)), engine.cpp:84-85
-  int debug;         // perf experiments: 1 = skip epilogue stores; 9 = counters / timelines into dbg_out
-  long long* dbg_out;   // debug == 9: [cta][8] MMA / epilogue counters, globaltimer stamps
   float* reset_at_exit; // 4 * n_reset floats zeroed when the GEMM (the step's last kernel) retires: the
-  int n_reset;
-                        // next step's norm / kappa bounds start from 0 without a memset node
+  int n_reset;          // next step's norm / kappa bounds start from 0 without a memset node
+  long long* dbg_out;   // FC_PROFILE builds: [cta][16] MMA / epilogue counters, globaltimer stamps
 };
 
 // kSimFused (K = 1): one S tile gives both the row statistics (segment R) and the column
@@ -148,7 +150,6 @@ cudaError_t sim_set_smem();
 cudaError_t launch_ring_probe(int n_pairs, int n_kb, int tile_kb, int epi, long long* cycles, cudaStream_t s);
 cudaError_t launch_mma_probe(int n_pairs, int n_mma, int commit_every, long long* cycles, cudaStream_t s);
 cudaError_t gemm_set_smem();
-cudaError_t gemm_max_active_clusters(int pairs_per_cluster, int* n);
 cudaError_t launch_gemm(bool pdl, const GemmParams& p, const CUtensorMap* mapQ, const CUtensorMap* mapX,
                         const CUtensorMap* mapOut, int grid, cudaStream_t s);
 

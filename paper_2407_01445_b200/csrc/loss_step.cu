@@ -171,8 +171,6 @@ struct LossStep {
   bool shared_q = true;          // K == 1: one Q pass, Q^T read by the dE2 GEMM
   int sim_debug = 0, gemm_debug = 0;
   bool q_factor = true;          // FC_Q_FACTOR=0 forces the two-exponential Q path (A/B checks)
-  bool gemm_mc = false;          // FC_GEMM_MC=1: clusters of two pairs multicast the GEMM B operand
-  int gemm_mc_clusters = 0;      // co-resident clusters of 4 (the persistent stream-K grid when gemm_mc)
   bool fused_p1 = false;         // K == 1: row + column statistics from one S pass (FC_FUSED_P1=0: two passes)
   bool pdl = true;               // programmatic dependent launch between the step's kernels (FC_PDL=0: off)
   bool split_tail = false;       // similarity kernels: leftover tiles as half tiles (FC_SPLIT_TAIL=1; measured neutral)
@@ -313,7 +311,6 @@ struct LossStep {
     if (const char* e = std::getenv("FC_DEBUG_SYNC")) debug_sync = atoi(e) != 0;
     if (const char* e = std::getenv("FC_SIM_DEBUG")) sim_debug = atoi(e);
     if (const char* e = std::getenv("FC_Q_FACTOR")) q_factor = atoi(e) != 0;
-    if (const char* e = std::getenv("FC_GEMM_MC")) gemm_mc = atoi(e) != 0;
     fused_p1 = K == 1;
     if (const char* e = std::getenv("FC_PDL")) pdl = atoi(e) != 0;
     if (const char* e = std::getenv("FC_SPLIT_TAIL")) split_tail = atoi(e) != 0;
@@ -329,11 +326,6 @@ struct LossStep {
     if (const char* e = std::getenv("FC_SHARED_Q")) shared_q = shared_q && atoi(e) != 0;
     FC_CUDA(fc::sim_set_smem());
     FC_CUDA(fc::gemm_set_smem());
-    if (gemm_mc) {
-      FC_CUDA(fc::gemm_max_active_clusters(2, &gemm_mc_clusters));
-      gemm_mc_clusters = std::min(gemm_mc_clusters, n_sm / 4);
-      if (gemm_mc_clusters < 1) gemm_mc = false;
-    }
     // side-branch kernels run beside persistent similarity CTAs: ask for the max-shared
     // carveout so the SM configuration they land on never has to change for a pass-2 CTA
     FC_CUDA(cudaFuncSetAttribute(fc::fc_reduce_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
@@ -613,15 +605,6 @@ struct LossStep {
     a.gscale = static_cast<float>(1.0 / (static_cast<double>(Bl) * static_cast<double>(B - 1)));
     a.scal = scal;
     if (sim_debug == 9) a.dbg = dbg_buf + 2 * 2688 + 160 * 16;
-    // side branch: zero dE (the GEMM's reduce-add target). ws2 has the lowest stream priority,
-    // so the block scheduler dispatches prep / pass 1 first and the zeroing fills in behind
-    // them (no event between the programmatically linked kernels of the main stream)
-    FC_CUDA(cudaEventRecord(zero_fork, st));
-    FC_CUDA(cudaStreamWaitEvent(ws2, zero_fork, 0));
-    fc::fc_zero_kernel<<<n_sm, 256, 0, ws2>>>(reinterpret_cast<float4*>(out->de1), reinterpret_cast<float4*>(out->de2),
-                                              static_cast<long long>(Bl) * d / 4);
-    FC_CUDA(cudaGetLastError());
-    FC_CUDA(cudaEventRecord(zero_join, ws2));
     // prep: with peer memory every rank preps only its own anchors, BEFORE the gather (the
     // diagonal and tau^t of non-local anchors are never needed: their pass-2 parameters arrive
     // ready-made); its norm maxima sit in this rank's bounds slot, which the gather copies
@@ -682,6 +665,9 @@ struct LossStep {
     sp.clamps = clamps;
     sp.bounds = bounds;
     sp.n_bounds = K;
+    sp.zero0 = reinterpret_cast<float4*>(out->de1);   // the GEMM's reduce-add targets
+    sp.zero1 = reinterpret_cast<float4*>(out->de2);
+    sp.zero_n4 = static_cast<long long>(Bl) * d / 4;
     sp.debug = sim_debug;
     sp.split_tail = split_tail ? 1 : 0;
     if (sim_debug == 9) sp.dbg_out = dbg_buf;
@@ -705,6 +691,7 @@ struct LossStep {
       FC_CUDA(fc::launch_sim(fc::kSimStats, sp, mA, mB, nullptr, pair_grid(sp.n_items), st, nullptr, pdl && !timing));
     }
 
+    sp.zero_n4 = 0;
     // ---- u table, payload, (all-gather), weights, reductions, tau update ----
     mark(3, st);
     // table update + weights + local G_tau / loss terms + payload, one lane group per anchor
@@ -789,10 +776,8 @@ struct LossStep {
     gp.nseg = 2;
     gp.d = d;
     gp.n_nb = (d + fc::kGemmN - 1) / fc::kGemmN;
-    gp.pairs_per_cluster = gemm_mc ? 2 : 1;
     gp.kb_total = ldq / fc::kBlockK;
     gp.scale = static_cast<float>(1.0 / (static_cast<double>(Bl) * static_cast<double>(B - 1)));
-    gp.debug = gemm_debug;
     gp.reset_at_exit = bounds;
     gp.n_reset = K;
     if (gemm_debug >= 9) gp.dbg_out = dbg_buf + 2 * 2688;
@@ -804,14 +789,14 @@ struct LossStep {
       g.r = rcoef;
       g.x = s ? E1 : E2;
       g.out = s ? out->de2 : out->de1;
-      const int rows_per_tile = fc::kPairM * gp.pairs_per_cluster;
-      gp.n_mb[s] = (Bl + rows_per_tile - 1) / rows_per_tile;
+      gp.n_mb[s] = (Bl + fc::kPairM - 1) / fc::kPairM;
     }
     gp.n_tiles = (gp.n_mb[0] + gp.n_mb[1]) * gp.n_nb;
-    // every unit reduce-adds into dE (zeroed on the side branch of this step)
+    // every unit reduce-adds into dE (zeroed by pass 1 of this step): the GEMM's only
+    // predecessor is pass 2, so its launch stays programmatic
     // persistent: exactly the clusters that co-reside (clusters of 4 pack into fewer than 148 SMs)
-    const int gemm_ctas = gemm_mc ? 4 * gemm_mc_clusters : (n_sm / 2) * 2;
-    balance_units(gp, gemm_ctas / (2 * gp.pairs_per_cluster));
+    const int gemm_ctas = (n_sm / 2) * 2;
+    balance_units(gp, gemm_ctas / 2);
     CUtensorMap mX[2] = {mE2n, mE1n};
     CUtensorMap mQs[2] = {mQ[0], shared_q ? mQt : mQ[1]};
     if (out->de1 != map_o1 || out->de2 != map_o2) {
@@ -821,7 +806,6 @@ struct LossStep {
       map_o1 = out->de1;
       map_o2 = out->de2;
     }
-    FC_CUDA(cudaStreamWaitEvent(st, zero_join, 0));
     FC_CUDA(fc::launch_gemm(pdl && !timing, gp, mQs, mX, mO, gemm_ctas, st));
     mark(6, st);
 
@@ -829,7 +813,7 @@ struct LossStep {
   }
 
   int kernels_per_step() const {
-    int n = 1 /*prep*/ + 1 /*pass1*/ + 1 /*reduce*/ + (indiv ? 1 : 0) + 1 /*zero dE*/ + 1 /*pass2*/ + 1 /*gemm*/;
+    int n = 1 /*prep*/ + 1 /*pass1*/ + 1 /*reduce*/ + (indiv ? 1 : 0) + 1 /*pass2*/ + 1 /*gemm*/;
     n += 1;   // fc_anchor_kernel
     if (K > 1) n += use_peer ? 3 /*two peer gathers + u replica*/ : 1 /*weights*/;
     return n;
@@ -896,10 +880,6 @@ int fc_debug_ring_probe(int32_t n_pairs, int32_t n_kb, int32_t tile_kb, int32_t 
   return guarded([&] {
     FC_CUDA(fc::launch_ring_probe(n_pairs, n_kb, tile_kb, epi, cycles_dev, static_cast<cudaStream_t>(stream)));
   });
-}
-
-int fc_debug_gemm_clusters(int32_t pairs_per_cluster, int32_t* max_clusters) {
-  return guarded([&] { FC_CUDA(fc::gemm_max_active_clusters(pairs_per_cluster, max_clusters)); });
 }
 
 int fc_debug_mma_probe(int32_t n_pairs, int32_t n_mma, int32_t commit_every, long long* cycles_dev, void* stream) {
@@ -1461,7 +1441,6 @@ int fc_embedding_cotangents(const void* e1g, const void* e2g, int32_t batch, int
     gp.nseg = 2;
     gp.d = d;
     gp.n_nb = (d + fc::kGemmN - 1) / fc::kGemmN;
-    gp.pairs_per_cluster = 1;
     gp.kb_total = ldq / fc::kBlockK;
     gp.scale = static_cast<float>(1.0 / (static_cast<double>(cnt) * static_cast<double>(B - 1)));
     CUtensorMap mO[2];

@@ -553,6 +553,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(SimCfg<kMode>::kThre
     }
   } else {
     // ===================== epilogue (both CTAs) =====================
+    if (p.zero_n4 > 0) {   // dE <- 0 (nothing of this step reads it before the GEMM)
+      const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+      const long long nt = static_cast<long long>(gridDim.x) * kEpi * 32;
+      for (long long g = static_cast<long long>(blockIdx.x) * kEpi * 32 + threadIdx.x; g < p.zero_n4; g += nt) {
+        p.zero0[g] = z;
+        p.zero1[g] = z;
+      }
+    }
     griddep_wait();   // row / column parameters and bounds come from the preceding kernel
     const uint32_t q4 = warp & 3;               // TMEM lane quarter accessible to this warp
     long long e_wait = 0, e_ld = 0, e_math = 0, e_t0 = clock64(), e_g0 = 0;

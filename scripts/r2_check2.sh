@@ -1,0 +1,6 @@
+mkdir -p gpurun_out/r2
+for v in "FC_XPATH=1" "FC_XPATH=0"; do
+env $v timeout -s KILL 300 python bench.py --steps 50 --warmup 5 --no-cpu-baseline --no-e2e > gpurun_out/r2/bench.json 2>gpurun_out/r2/bench.err
+python -c "import json,sys; d=json.load(open('gpurun_out/r2/bench.json')); print('$v', round(d['ms_per_step']*1e3,1), 'us', {k: round(v*1e3,1) for k,v in d['phases_ms'].items()})" || tail -20 gpurun_out/r2/bench.err
+done
+timeout -s KILL 900 python -m pytest tests/test_gpu_step.py -m gpu -q 2>&1 | grep -E "AssertionError|passed|failed" | head -30
