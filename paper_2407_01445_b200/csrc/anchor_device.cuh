@@ -170,7 +170,9 @@ __device__ __forceinline__ void local_terms(const StepArgs& a, int r, const Anch
 
 __device__ __forceinline__ void store_payload(const StepArgs& a, int r, int id, const TableVals& v, double t1,
                                               double t2) {
-  if (a.track_u && id >= 0 && id < a.n_train) {   // state.cpp:52-53 EMA, then the snapshot (state.cpp:57-71)
+  // state.cpp:52-53 EMA, then the snapshot (state.cpp:57-71); a batch with a repeated id (prep
+  // flagged FC_ERR_OWNERSHIP) writes no entry
+  if (a.track_u && id >= 0 && id < a.n_train && *a.err != kErrOwnership) {
     a.u1_tab[id] = v.u1;
     a.u2_tab[id] = v.u2;
   }

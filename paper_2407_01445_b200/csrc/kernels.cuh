@@ -86,6 +86,16 @@ struct SimParams {
   float4* zero0;
   float4* zero1;
   long long zero_n4;
+  // duplicate-id check, run by the idle MMA warp of every non-leader CTA: an open-addressing set
+  // of the rank's ids with slots tagged by the step's sequence number (*step_tag, written by
+  // prep), so nothing is cleared between steps; a repeat sets *err = FC_ERR_OWNERSHIP before
+  // the per-anchor kernel (which skips every table write then) starts
+  const int* ids;
+  int n_ids;
+  unsigned long long* idset;
+  int idset_mask;                      // slots - 1 (power of two >= 2 n_ids)
+  const unsigned long long* step_tag;
+  int* err;
   int debug;                   // perf experiments: 1 = skip epilogue math, 2 = also skip B loads
   long long* dbg_out;          // debug == 9: per-pair MMA-warp cycle counters [pair][8]
 };
@@ -138,6 +148,12 @@ struct PeerGather {
                                       // reads the gathered data after griddepcontrol.wait
   int wait_src;                       // programmatic launch: sources >= wait_src are written by the
                                       // preceding kernel (griddepcontrol.wait first); -1: none
+  // failure propagation (fabric.cpp:228-235 poison): a rank that waits longer than timeout_ns
+  // for a peer's flag stores a non-zero abort word into every rank (its own included); every
+  // waiting rank polls its local abort word and leaves with FC_ERR_COLLECTIVE_ABORTED
+  long long timeout_ns;
+  unsigned long long* my_abort;
+  unsigned long long* peer_abort[kMaxPeers];
 };
 cudaError_t launch_peer_gather(const PeerGather& g, int blocks, int threads, cudaStream_t s, bool pdl = false);
 void* peer_gather_kernel_fn();

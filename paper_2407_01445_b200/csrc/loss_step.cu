@@ -141,19 +141,24 @@ struct LossStep {
   long long *s1 = nullptr, *s2 = nullptr;
   fc::TauState* tau_state = nullptr;
   // workspaces
-  __nv_bfloat16 *e1g = nullptr, *e2g = nullptr;   // gathered embeddings (K > 1)
+  // gathered embeddings (K > 1), two buffers selected by the step parity: a rank may start
+  // step t+1's embedding gather (its first cross-rank store) while a slower peer still reads
+  // step t's rows; it cannot reach step t+2's gather before every peer has finished step t
+  // (step t+1's payload gather waits for all peers, and a peer's step-(t+1) payload flag
+  // follows its whole step t in stream order). The bounds slots are double-buffered alike.
+  __nv_bfloat16 *e1g = nullptr, *e2g = nullptr;   // [2][B][d]
   // NVLink peer gathers (K > 1, all ranks P2P-capable; FC_PEER=0 forces the NCCL path)
   bool use_peer = false;
   int my_dev = 0;
-  unsigned long long* pflags = nullptr;   // [2][kMaxPeers] local flags: E gather, payload gather
+  unsigned long long* pflags = nullptr;   // [2][kMaxPeers] local flags: E gather, payload gather; + abort word
   unsigned* ptickets = nullptr;           // [2] grid-completion tickets
   std::vector<void*> peer_maps;           // cudaIpcOpenMemHandle mappings to close
-  fc::PeerGather pg_e{}, pg_p{};
+  fc::PeerGather pg_e[2]{}, pg_p[2]{};     // per step parity
   unsigned long long seq = 0;             // per-step sequence number (same on every rank)
   float* diag = nullptr;
   float2 *rowstat = nullptr, *partial = nullptr, *col_partial = nullptr;
   unsigned long long* clamps = nullptr;
-  float* bounds = nullptr;
+  float* bounds = nullptr;   // [2][kMaxPeers][4] (parity, rank slot)
   double* f64 = nullptr;   // per-local-anchor fp64 arrays
   double *send = nullptr, *recv = nullptr, *red = nullptr;
   int nblk = 0, pstride = 0;   // payload: [u1|u2|t1|t2|id|gt1|gt2] x Bl + nblk x 3 block partials
@@ -161,9 +166,15 @@ struct LossStep {
   float* rcoef = nullptr;
   __nv_bfloat16* q = nullptr;   // [2][Bl][ldq]
   int* err = nullptr;
+  long long test_delay_ns = 0;           // FC_TEST_DELAY_US (tests only, K > 1): this rank stalls after
+                                         // the payload gather, before pass 2 (rank-skew stress test)
+  unsigned long long* idset = nullptr;   // duplicate-id set (pass 1's non-leader MMA warps)
+  int idset_slots = 0;
+  unsigned long long* step_tag = nullptr;
+  bool dup_check = true;                 // FC_DUP_CHECK=0: skip the duplicate-id check (A/B only)
   fc::StepResult* result_d = nullptr;   // device alias of result_h (mapped pinned memory)
   fc::StepResult* result_h = nullptr;   // written by the reduce kernel over PCIe: no D2H copy node
-  cudaEvent_t done{}, fork{}, side_fork{}, side_join{}, zero_fork{}, zero_join{};
+  cudaEvent_t done{}, fork{}, side_fork{}, side_join{};
   cudaStream_t ws = nullptr;     // context stream (capturable), joined to the caller's stream
   cudaStream_t ws2 = nullptr;    // side branch: reductions / tau updates off the critical path
   double* scal = nullptr;        // device {gamma_t, eps_t}
@@ -177,7 +188,7 @@ struct LossStep {
   int gemm_drain = 0;            // FC_GEMM_DRAIN: stream-K unit-boundary cost in k-blocks (0: KB / 10)
   long long* dbg_buf = nullptr;   // FC_SIM_DEBUG=9 MMA-warp counters: [launch 0: pass 1, 1: pass 2][pair][8]             // FC_SIM_DEBUG perf experiments (results invalid when set)
   struct GraphEntry {
-    const void* key[5];
+    const void* key[6];
     cudaGraphExec_t exec;
     cudaGraph_t graph;                 // kept: its prep node addresses the per-step parameter update
     cudaGraphNode_t prep_node;
@@ -263,11 +274,12 @@ struct LossStep {
     FC_CUDA(cudaMemcpy(tau_state, &ts, sizeof(ts), cudaMemcpyHostToDevice));
 
     if (K > 1) {
-      e1g = dalloc<__nv_bfloat16>(static_cast<size_t>(B) * d);
-      e2g = dalloc<__nv_bfloat16>(static_cast<size_t>(B) * d);
+      e1g = dalloc<__nv_bfloat16>(2 * static_cast<size_t>(B) * d);
+      e2g = dalloc<__nv_bfloat16>(2 * static_cast<size_t>(B) * d);
       ncclUniqueId id;
       std::memcpy(&id, cfg.nccl_id, sizeof(id));
       FC_NCCL(ncclCommInitRank(&comm, K, id, rank));
+      check_collective_shape();
     }
     diag = dalloc<float>(B);
     rowstat = dalloc<float2>(2 * static_cast<size_t>(Bl));
@@ -275,8 +287,8 @@ struct LossStep {
     if (K == 1)   // [ceil(B/32)][n_slots = 2 per pair row block][32]: 256-byte warp stores
       col_partial = dalloc<float2>(static_cast<size_t>((Bl + fc::kPairM - 1) / fc::kPairM) * 2 * ((B + 31) / 32 * 32));
     clamps = dalloc<unsigned long long>(1);
-    bounds = dalloc<float>(4 * fc::kMaxPeers);   // one {norm1, norm2, kappa, -} slot per rank
-    FC_CUDA(cudaMemset(bounds, 0, 4 * fc::kMaxPeers * sizeof(float)));
+    bounds = dalloc<float>(2 * 4 * fc::kMaxPeers);   // one {norm1, norm2, kappa, -} slot per rank and parity
+    FC_CUDA(cudaMemset(bounds, 0, 2 * 4 * fc::kMaxPeers * sizeof(float)));
     f64 = dalloc<double>(static_cast<size_t>(Bl) * 18);
     nblk = (Bl * fc::kAnchorLanes + kAnchorBlock - 1) / kAnchorBlock;
     pstride = (7 * Bl + 3 * nblk + 1) & ~1;   // even: 16-byte slices for the peer gather
@@ -288,6 +300,12 @@ struct LossStep {
     rcoef = dalloc<float>(Bl);
     q = dalloc<__nv_bfloat16>(2 * static_cast<size_t>(Bl) * ldq);
     err = dalloc<int>(1);
+    idset_slots = 64;
+    while (idset_slots < 2 * Bl) idset_slots *= 2;
+    idset = dalloc<unsigned long long>(idset_slots);
+    FC_CUDA(cudaMemset(idset, 0, idset_slots * sizeof(unsigned long long)));
+    step_tag = dalloc<unsigned long long>(1);
+    FC_CUDA(cudaMemset(step_tag, 0, sizeof(unsigned long long)));
     if (K > 1) setup_peers();
     FC_CUDA(cudaMemset(err, 0, sizeof(int)));
     FC_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&result_h), sizeof(fc::StepResult), cudaHostAllocMapped));
@@ -303,8 +321,6 @@ struct LossStep {
     }
     FC_CUDA(cudaEventCreateWithFlags(&side_fork, cudaEventDisableTiming));
     FC_CUDA(cudaEventCreateWithFlags(&side_join, cudaEventDisableTiming));
-    FC_CUDA(cudaEventCreateWithFlags(&zero_fork, cudaEventDisableTiming));
-    FC_CUDA(cudaEventCreateWithFlags(&zero_join, cudaEventDisableTiming));
     scal = dalloc<double>(2);
     if (const char* e = std::getenv("FC_GRAPH")) use_graph = atoi(e) != 0;
     shared_q = K == 1;
@@ -319,18 +335,20 @@ struct LossStep {
     if (const char* e = std::getenv("FC_GEMM_DEBUG")) gemm_debug = atoi(e);
     if (sim_debug == 9 || gemm_debug >= 9) dbg_buf = dalloc<long long>(2 * 2688 + 160 * 16 + 8192);
     if (dbg_buf && use_peer) {   // FC_SIM_DEBUG=9: gather stamps after the anchor / prep stamps
-      pg_e.dbg = dbg_buf + 2 * 2688 + 160 * 16 + 6000;
-      pg_p.dbg = pg_e.dbg + 4;
+      for (int q2 = 0; q2 < 2; ++q2) {
+        pg_e[q2].dbg = dbg_buf + 2 * 2688 + 160 * 16 + 6000;
+        pg_p[q2].dbg = pg_e[q2].dbg + 4;
+      }
     }
     if (debug_sync) use_graph = false;
     if (const char* e = std::getenv("FC_SHARED_Q")) shared_q = shared_q && atoi(e) != 0;
+    if (const char* e = std::getenv("FC_DUP_CHECK")) dup_check = atoi(e) != 0;
+    if (const char* e = std::getenv("FC_TEST_DELAY_US")) test_delay_ns = K > 1 ? atoll(e) * 1000LL : 0;
     FC_CUDA(fc::sim_set_smem());
     FC_CUDA(fc::gemm_set_smem());
     // side-branch kernels run beside persistent similarity CTAs: ask for the max-shared
     // carveout so the SM configuration they land on never has to change for a pass-2 CTA
     FC_CUDA(cudaFuncSetAttribute(fc::fc_reduce_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
-                                 cudaSharedmemCarveoutMaxShared));
-    FC_CUDA(cudaFuncSetAttribute(fc::fc_zero_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
                                  cudaSharedmemCarveoutMaxShared));
     // prep and the per-anchor kernel run while the next similarity pass's CTAs (227 KB of
     // shared memory each) take their SMs (programmatic launch)
@@ -382,6 +400,29 @@ struct LossStep {
     a.rcoef = rcoef;
     a.blockpart = send + 7 * static_cast<size_t>(Bl);
     a.red = red; a.err = err; a.result = result_d;
+    a.step_tag = step_tag;
+  }
+
+  // Every rank must run the same step shape (variant, batch, dim, table size, world): the
+  // reference's rendezvous throws CollectiveShapeError when peers disagree on an op's shape
+  // (fabric.cpp:130-138); here the ranks compare their configurations once, at creation.
+  void check_collective_shape() {
+    const long long mine[6] = {cfg.variant, Bl, d, cfg.n_train, K, cfg.scale_by_tau};
+    cudaStream_t s0;
+    FC_CUDA(cudaStreamCreateWithFlags(&s0, cudaStreamNonBlocking));
+    long long* dv = dalloc<long long>(6 * (K + 1));
+    FC_CUDA(cudaMemcpy(dv + 6 * K, mine, sizeof(mine), cudaMemcpyHostToDevice));
+    FC_NCCL(ncclAllGather(dv + 6 * K, dv, 6, ncclInt64, comm, s0));
+    FC_CUDA(cudaStreamSynchronize(s0));
+    std::vector<long long> all(6 * static_cast<size_t>(K));
+    FC_CUDA(cudaMemcpy(all.data(), dv, all.size() * sizeof(long long), cudaMemcpyDeviceToHost));
+    cudaFree(dv);
+    cudaStreamDestroy(s0);
+    for (int k = 0; k < K; ++k)
+      for (int f = 0; f < 6; ++f)
+        if (all[6 * k + f] != mine[f])
+          throw FcError{FC_ERR_COLLECTIVE_SHAPE, "rank " + std::to_string(k) + " runs a different step shape "
+                                                 "(variant / local batch / dim / n_train / world / scale_by_tau)"};
   }
 
   // CUDA IPC mappings of every rank's gather destinations and flag arrays; handles travel
@@ -418,8 +459,8 @@ struct LossStep {
       cudaStreamDestroy(s0);
       return;
     }
-    pflags = dalloc<unsigned long long>(2 * fc::kMaxPeers);
-    FC_CUDA(cudaMemset(pflags, 0, 2 * fc::kMaxPeers * sizeof(unsigned long long)));
+    pflags = dalloc<unsigned long long>(2 * fc::kMaxPeers + 1);
+    FC_CUDA(cudaMemset(pflags, 0, (2 * fc::kMaxPeers + 1) * sizeof(unsigned long long)));
     ptickets = dalloc<unsigned>(2);
     FC_CUDA(cudaMemset(ptickets, 0, 2 * sizeof(unsigned)));
     void* mine[6] = {e1g, e2g, recv, pflags, par, bounds};
@@ -447,41 +488,53 @@ struct LossStep {
     // rank's slice of the 8 pass-2 parameter arrays (kappa, beta, coef, fac x 2 tracks), so the
     // pass-2 parameters of every anchor arrive ready-made (no weights kernel on the step path)
     const size_t np = static_cast<size_t>(n_jt) * fc::kPairN;
-    pg_e = fc::PeerGather{};
-    pg_e.bytes[0] = pg_e.bytes[1] = static_cast<size_t>(Bl) * d * 2;
-    pg_e.bytes[2] = 16;   // this rank's bounds slot (norm maxima written by prep)
-    pg_e.src[2] = reinterpret_cast<const uint8_t*>(bounds + 4 * rank);
-    pg_e.n_src = 3;
-    pg_p = fc::PeerGather{};
-    pg_p.bytes[0] = static_cast<size_t>(pstride) * 8;
-    pg_p.src[0] = reinterpret_cast<const uint8_t*>(send);
-    pg_p.n_src = 1 + 8 + 1;
-    for (int j = 0; j < 8; ++j) {
-      pg_p.bytes[1 + j] = static_cast<size_t>(Bl) * 4;
-      pg_p.src[1 + j] = reinterpret_cast<const uint8_t*>(par + j * np + static_cast<size_t>(rank) * Bl);
+    const char* tmo = std::getenv("FC_PEER_TIMEOUT_MS");   // a peer that stops stepping: poison after this long
+    const long long timeout_ns = (tmo ? atoll(tmo) : 60000LL) * 1000000LL;
+    const size_t ebytes = static_cast<size_t>(B) * d * 2;   // one parity's gathered rows
+    for (int q2 = 0; q2 < 2; ++q2) {
+      fc::PeerGather& ge = pg_e[q2];
+      fc::PeerGather& gpl = pg_p[q2];
+      const float* bslot = bounds + q2 * 4 * fc::kMaxPeers + 4 * rank;
+      ge = fc::PeerGather{};
+      ge.bytes[0] = ge.bytes[1] = static_cast<size_t>(Bl) * d * 2;
+      ge.bytes[2] = 16;   // this rank's bounds slot (norm maxima written by prep)
+      ge.src[2] = reinterpret_cast<const uint8_t*>(bslot);
+      ge.n_src = 3;
+      gpl = fc::PeerGather{};
+      gpl.bytes[0] = static_cast<size_t>(pstride) * 8;
+      gpl.src[0] = reinterpret_cast<const uint8_t*>(send);
+      gpl.n_src = 1 + 8 + 1;
+      for (int j = 0; j < 8; ++j) {
+        gpl.bytes[1 + j] = static_cast<size_t>(Bl) * 4;
+        gpl.src[1 + j] = reinterpret_cast<const uint8_t*>(par + j * np + static_cast<size_t>(rank) * Bl);
+      }
+      gpl.bytes[9] = 16;   // bounds slot again, now with the kappa maximum of the anchor kernel
+      gpl.src[9] = reinterpret_cast<const uint8_t*>(bslot);
+      for (fc::PeerGather* g : {&ge, &gpl}) {
+        g->world = K;
+        g->rank = rank;
+        g->err = err;
+        g->timeout_ns = timeout_ns;
+        g->my_abort = pflags + 2 * fc::kMaxPeers;
+      }
+      for (int k = 0; k < K; ++k) {
+        ge.dst[0][k] = static_cast<uint8_t*>(peer[0][k]) + q2 * ebytes;
+        ge.dst[1][k] = static_cast<uint8_t*>(peer[1][k]) + q2 * ebytes;
+        gpl.dst[0][k] = static_cast<uint8_t*>(peer[2][k]);
+        for (int j = 0; j < 8; ++j)
+          gpl.dst[1 + j][k] = static_cast<uint8_t*>(peer[4][k]) + j * np * 4;
+        uint8_t* pb = static_cast<uint8_t*>(peer[5][k]) + q2 * 4 * fc::kMaxPeers * sizeof(float);
+        ge.dst[2][k] = pb;   // norm maxima slot
+        gpl.dst[9][k] = pb;
+        ge.peer_flag[k] = static_cast<unsigned long long*>(peer[3][k]);
+        gpl.peer_flag[k] = static_cast<unsigned long long*>(peer[3][k]) + fc::kMaxPeers;
+        ge.peer_abort[k] = gpl.peer_abort[k] = static_cast<unsigned long long*>(peer[3][k]) + 2 * fc::kMaxPeers;
+      }
+      ge.my_flag = pflags;
+      gpl.my_flag = pflags + fc::kMaxPeers;
+      ge.ticket = ptickets;
+      gpl.ticket = ptickets + 1;
     }
-    pg_p.bytes[9] = 16;   // bounds slot again, now with the kappa maximum of the anchor kernel
-    pg_p.src[9] = reinterpret_cast<const uint8_t*>(bounds + 4 * rank);
-    for (fc::PeerGather* g : {&pg_e, &pg_p}) {
-      g->world = K;
-      g->rank = rank;
-      g->err = err;
-    }
-    for (int k = 0; k < K; ++k) {
-      pg_e.dst[0][k] = static_cast<uint8_t*>(peer[0][k]);
-      pg_e.dst[1][k] = static_cast<uint8_t*>(peer[1][k]);
-      pg_p.dst[0][k] = static_cast<uint8_t*>(peer[2][k]);
-      for (int j = 0; j < 8; ++j)
-        pg_p.dst[1 + j][k] = static_cast<uint8_t*>(peer[4][k]) + j * np * 4;
-      pg_e.dst[2][k] = static_cast<uint8_t*>(peer[5][k]);   // norm maxima slot
-      pg_p.dst[9][k] = static_cast<uint8_t*>(peer[5][k]);
-      pg_e.peer_flag[k] = static_cast<unsigned long long*>(peer[3][k]);
-      pg_p.peer_flag[k] = static_cast<unsigned long long*>(peer[3][k]) + fc::kMaxPeers;
-    }
-    pg_e.my_flag = pflags;
-    pg_p.my_flag = pflags + fc::kMaxPeers;
-    pg_e.ticket = ptickets;
-    pg_p.ticket = ptickets + 1;
     use_peer = true;
   }
 
@@ -512,7 +565,9 @@ struct LossStep {
     if (track_u && (!(in->gamma > 0.0) || in->gamma > 1.0)) throw FcError{FC_ERR_DOMAIN, "gamma must be in (0,1]"};
     ++seq;   // every rank calls step() the same number of times: the peer-gather handshake value
     if (use_graph && !timing) {   // phase timing: direct launches (events between kernels)
-      const void* key[5] = {in->e1, in->e2, in->ids, out->de1, timing ? nullptr : out->de2};
+      // one graph per (input, output) pointer set and step parity (the gather buffers alternate)
+      const void* key[6] = {in->e1, in->e2, in->ids, out->de1, out->de2,
+                            reinterpret_cast<const void*>(static_cast<uintptr_t>(parity()))};
       GraphEntry* ge = nullptr;
       for (auto& g : graphs)
         if (std::memcmp(g.key, key, sizeof(key)) == 0) ge = &g;
@@ -567,7 +622,8 @@ struct LossStep {
       double gamma = in->gamma, eps = in->eps;
       const void* e1 = ge->prep_e1;
       const void* e2 = ge->prep_e2;
-      void* args[5] = {&e1, &e2, &ge->prep_args, &gamma, &eps};
+      unsigned long long sq = seq;
+      void* args[6] = {&e1, &e2, &ge->prep_args, &gamma, &eps, &sq};
       cudaKernelNodeParams kp = ge->prep_params;
       kp.kernelParams = args;
       kp.extra = nullptr;
@@ -596,11 +652,16 @@ struct LossStep {
   const void* last_prep_e2 = nullptr;
   fc::StepArgs last_prep_args{};
 
+  int parity() const { return K > 1 ? static_cast<int>(seq & 1) : 0; }
+
   void enqueue(const fc_step_in* in, fc_step_out* out, cudaStream_t st) {
     const __nv_bfloat16* E1 = static_cast<const __nv_bfloat16*>(in->e1);
     const __nv_bfloat16* E2 = static_cast<const __nv_bfloat16*>(in->e2);
     mark(0, st);
     fc::StepArgs a = args;
+    const int par = parity();
+    float* bnd = bounds + par * 4 * fc::kMaxPeers;   // this step's bounds slots (one per rank)
+    a.bounds = bnd + 4 * rank;
     a.ids = in->ids;
     a.gscale = static_cast<float>(1.0 / (static_cast<double>(Bl) * static_cast<double>(B - 1)));
     a.scal = scal;
@@ -615,7 +676,7 @@ struct LossStep {
       a.prep_row0 = row0_;
       a.prep_rows = rows;
       // bounds were zeroed by the previous step's GEMM (and at creation)
-      fc::fc_prep_kernel<<<(rows * 32 + 127) / 128, 128, 0, st>>>(p1, p2, a, in->gamma, in->eps);   // one wave
+      fc::fc_prep_kernel<<<(rows * 32 + 127) / 128, 128, 0, st>>>(p1, p2, a, in->gamma, in->eps, seq);   // one wave
       FC_CUDA(cudaGetLastError());
       last_prep_e1 = p1;
       last_prep_e2 = p2;
@@ -624,7 +685,7 @@ struct LossStep {
     if (local_prep) launch_prep(E1, E2, rank * Bl, Bl);
     if (K > 1) {
       if (use_peer) {   // NVLink stores into every rank's e1g / e2g, flag handshake
-        fc::PeerGather g = pg_e;
+        fc::PeerGather g = pg_e[par];
         g.src[0] = reinterpret_cast<const uint8_t*>(E1);
         g.src[1] = reinterpret_cast<const uint8_t*>(E2);
         g.seq = seq;
@@ -635,12 +696,14 @@ struct LossStep {
         FC_CUDA(fc::launch_peer_gather(g, n_sm, 256, st, pdl && !timing));
       } else {
         FC_NCCL(ncclGroupStart());
-        FC_NCCL(ncclAllGather(E1, e1g, static_cast<size_t>(Bl) * d * 2, ncclUint8, comm, st));
-        FC_NCCL(ncclAllGather(E2, e2g, static_cast<size_t>(Bl) * d * 2, ncclUint8, comm, st));
+        FC_NCCL(ncclAllGather(E1, e1g + par * static_cast<size_t>(B) * d, static_cast<size_t>(Bl) * d * 2, ncclUint8,
+                              comm, st));
+        FC_NCCL(ncclAllGather(E2, e2g + par * static_cast<size_t>(B) * d, static_cast<size_t>(Bl) * d * 2, ncclUint8,
+                              comm, st));
         FC_NCCL(ncclGroupEnd());
       }
-      E1 = e1g;
-      E2 = e2g;
+      E1 = e1g + par * static_cast<size_t>(B) * d;
+      E2 = e2g + par * static_cast<size_t>(B) * d;
     }
     ensure_maps(E1, E2);
     mark(1, st);
@@ -663,8 +726,14 @@ struct LossStep {
     }
     sp.n_items = (sp.n_rb[0] + sp.n_rb[1]) * n_jt;
     sp.clamps = clamps;
-    sp.bounds = bounds;
+    sp.bounds = bnd;
     sp.n_bounds = K;
+    sp.ids = in->ids;
+    sp.n_ids = Bl;
+    sp.idset = dup_check ? idset : nullptr;
+    sp.idset_mask = idset_slots - 1;
+    sp.step_tag = step_tag;
+    sp.err = err;
     sp.zero0 = reinterpret_cast<float4*>(out->de1);   // the GEMM's reduce-add targets
     sp.zero1 = reinterpret_cast<float4*>(out->de2);
     sp.zero_n4 = static_cast<long long>(Bl) * d / 4;
@@ -692,6 +761,7 @@ struct LossStep {
     }
 
     sp.zero_n4 = 0;
+    sp.idset = nullptr;
     // ---- u table, payload, (all-gather), weights, reductions, tau update ----
     mark(3, st);
     // table update + weights + local G_tau / loss terms + payload, one lane group per anchor
@@ -716,7 +786,7 @@ struct LossStep {
       if (use_peer) {
         // payload + this rank's pass-2 parameters into every rank (the u replica update of the
         // other ranks' ids follows on the side branch)
-        fc::PeerGather g = pg_p;
+        fc::PeerGather g = pg_p[par];
         g.seq = seq;
         // pass 2 (programmatic launch) takes its SMs while the payload moves: its first tile's
         // operands and MMAs need only E; parameters are loaded after griddepcontrol.wait.
@@ -744,6 +814,7 @@ struct LossStep {
     FC_CUDA(cudaGetLastError());
     FC_CUDA(cudaEventRecord(side_join, ws2));
 
+    if (test_delay_ns > 0) fc::fc_delay_kernel<<<1, 32, 0, st>>>(test_delay_ns);
     // ---- pass 2: Q' tiles (bf16) for both segments ----
     for (int s = 0; s < 2; ++s) {
       fc::SimSeg& g = sp.seg[s];
@@ -778,7 +849,7 @@ struct LossStep {
     gp.n_nb = (d + fc::kGemmN - 1) / fc::kGemmN;
     gp.kb_total = ldq / fc::kBlockK;
     gp.scale = static_cast<float>(1.0 / (static_cast<double>(Bl) * static_cast<double>(B - 1)));
-    gp.reset_at_exit = bounds;
+    gp.reset_at_exit = bnd;   // this parity's slots: the next writer is step t+2 (see e1g)
     gp.n_reset = K;
     if (gemm_debug >= 9) gp.dbg_out = dbg_buf + 2 * 2688;
     for (int s = 0; s < 2; ++s) {
@@ -836,7 +907,8 @@ struct LossStep {
     for (void* p : {(void*)u1, (void*)u2, (void*)tau1, (void*)tau2, (void*)m1, (void*)v1, (void*)m2, (void*)v2,
                     (void*)s1, (void*)s2, (void*)tau_state, (void*)e1g, (void*)e2g, (void*)diag, (void*)rowstat,
                     (void*)partial, (void*)col_partial, (void*)clamps, (void*)bounds, (void*)f64, (void*)red, (void*)par, (void*)rcoef,
-                    (void*)q, (void*)err, (void*)pflags, (void*)ptickets})
+                    (void*)q, (void*)err, (void*)pflags, (void*)ptickets, (void*)idset,
+                    (void*)step_tag})
       if (p) cudaFree(p);
     if (recv && recv != send) cudaFree(recv);
     if (send) cudaFree(send);
@@ -846,8 +918,6 @@ struct LossStep {
     if (ws2) cudaStreamDestroy(ws2);
     cudaEventDestroy(side_fork);
     cudaEventDestroy(side_join);
-    cudaEventDestroy(zero_fork);
-    cudaEventDestroy(zero_join);
     cudaEventDestroy(done);
     cudaEventDestroy(fork);
     for (auto& e : ev) cudaEventDestroy(e);
@@ -1088,7 +1158,10 @@ int fc_step_scalars_get(void* ctx, fc_step_scalars* out) {
   if (const int e = s->result_h->err) {   // device-detected failures of the step (sticky)
     g_last_error = e == FC_ERR_SHAPE ? "ids: dataset index out of range [0, n_train) (UTable::update, state.cpp:46)"
                  : e == FC_ERR_NUMERIC ? "non-finite temperature gradient (optimizers.cpp:67)"
-                 : e == FC_ERR_NCCL ? "peer all-gather handshake timed out (a rank stopped stepping)"
+                 : e == FC_ERR_OWNERSHIP ? "ids: a dataset index appears twice in this rank's batch; no u/tau entry "
+                                           "of the step was written (OwnershipViolation, state.cpp:47-49)"
+                 : e == FC_ERR_COLLECTIVE_ABORTED ? "peer gather aborted: a rank stopped stepping or timed out "
+                                                    "(CollectiveAborted, fabric.cpp:228-235)"
                  : "device-side step failure";
     return e;
   }
@@ -1309,11 +1382,7 @@ int fc_g_values(const void* e1g, const void* e2g, int32_t batch, int32_t dim, co
     sp.n_bounds = 1;
     int dev = 0;
     FC_CUDA(cudaGetDevice(&dev));
-    static bool smem_set = false;
-    if (!smem_set) {
-      FC_CUDA(fc::sim_set_smem());
-      smem_set = true;
-    }
+    FC_CUDA(fc::sim_set_smem());   // per-device function attribute: set on the current device every call
     CUtensorMap mA[2] = {m1, m2}, mB[2] = {m2, m1};
     const int pairs = std::max(1, std::min(sm_count(dev) / 2, sp.n_items));
     FC_CUDA(fc::launch_sim(fc::kSimStats, sp, mA, mB, nullptr, pairs * 2, st, nullptr));
@@ -1383,12 +1452,8 @@ int fc_embedding_cotangents(const void* e1g, const void* e2g, int32_t batch, int
     CUtensorMap m1n = make_map(e1g, d, B, rb, 64, 64), m2n = make_map(e2g, d, B, rb, 64, 64);
     int dev = 0;
     FC_CUDA(cudaGetDevice(&dev));
-    static bool smem_set = false;
-    if (!smem_set) {
-      FC_CUDA(fc::sim_set_smem());
-      FC_CUDA(fc::gemm_set_smem());
-      smem_set = true;
-    }
+    FC_CUDA(fc::sim_set_smem());   // per-device function attributes: set on the current device every call
+    FC_CUDA(fc::gemm_set_smem());
     const int n_sm = sm_count(dev);
     // pass 1: row sums of S[L,G] and S^T[L,G] at the local anchors' temperatures -> r_i
     fc::SimParams sp{};

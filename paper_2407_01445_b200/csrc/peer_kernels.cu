@@ -43,6 +43,8 @@ __device__ __forceinline__ long long gtimer() {
   return t;
 }
 
+constexpr int kErrCollectiveAborted = 8;   // FC_ERR_COLLECTIVE_ABORTED (CollectiveAborted, errors.hpp)
+
 __global__ void __launch_bounds__(256) peer_gather_kernel(PeerGather g) {
   if (g.dbg && blockIdx.x == 0 && threadIdx.x == 0) g.dbg[0] = gtimer();
   if (g.early_trigger) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
@@ -89,13 +91,19 @@ __global__ void __launch_bounds__(256) peer_gather_kernel(PeerGather g) {
   fence_acq_rel_sys();
   for (int k = 0; k < g.world; ++k) st_relaxed_sys(g.peer_flag[k] + g.rank, g.seq);
   if (g.dbg) g.dbg[2] = gtimer();
-  // wait for every rank's slice (bounded: a dead peer must not hang the GPU)
+  // wait for every rank's slice. A peer that stopped stepping is detected after timeout_ns: this
+  // rank then poisons every rank (fabric.cpp:228-235); a poisoned rank stops waiting at once.
+  const long long t0 = gtimer();
   for (int k = 0; k < g.world; ++k) {
-    long long spins = 0;
     while (ld_relaxed_sys(g.my_flag + k) < g.seq) {
-      __nanosleep(64);
-      if (++spins > (1ll << 26)) {   // ~seconds: report instead of spinning forever
-        *g.err = 12;                  // NcclError-class failure (collective aborted)
+      if (ld_relaxed_sys(g.my_abort) != 0ull) {   // a peer gave up on this collective
+        atomicCAS(g.err, 0, kErrCollectiveAborted);
+        return;
+      }
+      __nanosleep(128);
+      if (gtimer() - t0 > g.timeout_ns) {
+        for (int j = 0; j < g.world; ++j) st_relaxed_sys(g.peer_abort[j], g.seq);
+        atomicCAS(g.err, 0, kErrCollectiveAborted);
         return;
       }
     }

@@ -112,6 +112,25 @@ __device__ __forceinline__ int a_key(const SimParams& p, const PairItems& pi, in
   return ((s * 65536) + rb) * n_chunks + chunk;
 }
 
+// Inserts `id` into the step's id set; false when it is already there. Slots hold
+// (tag << 32) | id with tag = low 32 bits of the step sequence number + 1: slots of earlier
+// steps read as free.
+__device__ bool idset_insert(unsigned long long* set, int mask, unsigned long long seq, int id) {
+  const unsigned long long tag = ((seq & 0xffffffffull) + 1ull) << 32;
+  const unsigned long long key = tag | static_cast<unsigned int>(id);
+  unsigned int h = (static_cast<unsigned int>(id) * 2654435761u) & static_cast<unsigned int>(mask);
+  for (;;) {
+    unsigned long long v = set[h];
+    while ((v & 0xffffffff00000000ull) != tag) {   // stale slot: claim it
+      const unsigned long long old = atomicCAS(set + h, v, key);
+      if (old == v) return true;
+      v = old;
+    }
+    if (v == key) return false;
+    h = (h + 1) & static_cast<unsigned int>(mask);
+  }
+}
+
 __device__ __forceinline__ void bulk_load(void* smem, const void* gmem, uint32_t bytes, uint64_t* bar) {
   asm volatile(
       "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(smem)),
@@ -468,6 +487,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(SimCfg<kMode>::kThre
         }
         if constexpr (kMode == kSimQ) if (it == 0) load_params(0);
       }
+    }
+  } else if (warp == kMmaWarp && rank != 0) {
+    // ===================== duplicate-id check (the non-leader CTA's idle MMA warp) =====================
+    if (p.idset) {
+      griddep_wait();   // prep wrote this step's tag
+      const unsigned long long seq = *p.step_tag;
+      bool dup = false;
+      for (int i = pair * 32 + static_cast<int>(lane); i < p.n_ids; i += n_pairs * 32) {
+        const int id = p.ids[i];
+        if (id >= 0 && !idset_insert(p.idset, p.idset_mask, seq, id)) dup = true;
+      }
+      // a repeated id: the reference's owner check (state.cpp:47-49) rejects the write
+      if (dup) atomicCAS(p.err, 0, 5 /* FC_ERR_OWNERSHIP */);
     }
   } else if (warp == kMmaWarp) {
     // ===================== MMA issuer (leader CTA only, one thread) =====================

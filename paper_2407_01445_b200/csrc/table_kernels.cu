@@ -14,7 +14,6 @@
 //                         temperature_step (optimizers.cpp:65-83) with the TauLrLatch
 //   fc_indiv_update_kernel  v2: IndividualTemp::update for every id of the global batch
 //                         (state.cpp:124-131), replicated identically on every rank
-//   fc_zero_kernel        zeroes dE (the GEMM's reduce-add target)
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
@@ -30,7 +29,7 @@ namespace fc {
 // anchors also snapshot tau^t (global tau, or IndividualTemp by id, state.cpp:112-122) and
 // emit the pass-1 row parameters.
 __global__ void fc_prep_kernel(const __nv_bfloat16* __restrict__ e1, const __nv_bfloat16* __restrict__ e2,
-                               StepArgs a, double gamma, double eps) {
+                               StepArgs a, double gamma, double eps, unsigned long long seq) {
   // pass 1 (programmatic launch) may take SMs now: its operand loads and MMAs do not read
   // anything prep writes; its epilogue waits for this grid (griddepcontrol.wait)
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
@@ -43,6 +42,7 @@ __global__ void fc_prep_kernel(const __nv_bfloat16* __restrict__ e1, const __nv_
   }
   if (w == 0 && lane == 0) {
     *a.clamps = 0ull;
+    *a.step_tag = seq;   // tags this step's duplicate-id set (pass 1 inserts the ids)
     // the step scalars arrive as kernel parameters (updated in the replayed graph per step,
     // no host-to-device copy) and are published for the later kernels of the step
     double* sc = const_cast<double*>(a.scal);
@@ -68,8 +68,8 @@ __global__ void fc_prep_kernel(const __nv_bfloat16* __restrict__ e1, const __nv_
     ys[i] = v < nv ? __ldg(y4 + v) : make_uint4(0u, 0u, 0u, 0u);
   }
   int id = lead ? a.ids[r] : 0;
-  if (lead && (id < 0 || id >= a.n_train)) {   // UTable::update range check (state.cpp:46)
-    atomicExch(a.err, 2);                       // ShapeError; the table is not touched at this id
+  if (lead && (id < 0 || id >= a.n_train)) {                         // UTable::update range check (state.cpp:46)
+    atomicCAS(a.err, 0, kErrShape);             // ShapeError; the table is not touched at this id
     id = 0;
   }
   float acc = 0.f, n1 = 0.f, n2 = 0.f;
@@ -122,6 +122,7 @@ __global__ void fc_prep_kernel(const __nv_bfloat16* __restrict__ e1, const __nv_
   }
   a.t_loc1[r] = t1;
   a.t_loc2[r] = t2;
+
   const float k1 = static_cast<float>(kLog2eD / t1), k2 = static_cast<float>(kLog2eD / t2);
   a.rowstat_R[r] = make_float2(k1, -acc * k1);   // y = s * kappa + beta (log2-domain exponent)
   a.rowstat_C[r] = make_float2(k2, -acc * k2);
@@ -134,15 +135,14 @@ __global__ void fc_prep_kernel(const __nv_bfloat16* __restrict__ e1, const __nv_
 
 __device__ void block_partials(const StepArgs& a, double ta, double tb, double tl, float kmax);
 
-// Zeroes the step's gradient outputs (the GEMM reduce-adds every stream-K unit into them).
-// Launched on the side branch while pass 1 runs: one small block per SM, no shared memory,
-// so it fits beside a persistent similarity CTA.
-__global__ void __launch_bounds__(256) fc_zero_kernel(float4* a0, float4* a1, long long n4) {
-  const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
-  for (long long g = blockIdx.x * blockDim.x + threadIdx.x; g < n4; g += static_cast<long long>(gridDim.x) * blockDim.x) {
-    a0[g] = z;
-    a1[g] = z;
-  }
+// Test hook (FC_TEST_DELAY_US): holds this rank's stream for `ns` nanoseconds.
+__global__ void fc_delay_kernel(long long ns) {
+  long long t0, t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  do {
+    __nanosleep(1000);
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  } while (t - t0 < ns);
 }
 
 // K > 1, after the payload all-gather: thread per anchor of the global batch -> pass-2
@@ -159,7 +159,7 @@ __global__ void fc_weights_kernel(StepArgs a) {
     const double u1 = blk[r], u2 = blk[a.Bl + r];
     const double t1 = blk[2 * a.Bl + r], t2 = blk[3 * a.Bl + r];
     const int id = static_cast<int>(blk[4 * a.Bl + r]);
-    if (a.track_u && k != a.rank && id >= 0 && id < a.n_train) {   // keep this rank's u replica equal to the UTable
+    if (a.track_u && k != a.rank && id >= 0 && id < a.n_train && *a.err != kErrOwnership) {   // keep this rank's u replica equal to the UTable
       a.u1_tab[id] = u1;
       a.u2_tab[id] = u2;
     }
@@ -223,7 +223,7 @@ __device__ void finalize_step(const StepArgs& a) {
   res->gtau = 0.0;
   res->clamps = *a.clamps;
   const bool learnable_global = (a.variant == 0 || a.variant == 3 || a.variant == 6);
-  if (learnable_global) {
+  if (learnable_global && *a.err != kErrOwnership) {   // a rejected batch leaves tau as it was
     const double gtau = a.red[0] * (1.0 / static_cast<double>(a.world));
     res->gtau = gtau;
     double lr = a.tau_lr;
@@ -232,7 +232,7 @@ __device__ void finalize_step(const StepArgs& a) {
       lr *= ts->latched ? a.lr_decay_factor : 1.0;
     }
     if (!isfinite(gtau)) {
-      *a.err = 9;  // NumericError (optimizers.cpp:67)
+      atomicCAS(a.err, 0, kErrNumeric);  // NumericError (optimizers.cpp:67)
     } else {       // scalar_adamw_step with weight decay 0, then projection (optimizers.cpp:65-83)
       ts->m = a.beta1 * ts->m + (1.0 - a.beta1) * gtau;
       ts->v = a.beta2 * ts->v + (1.0 - a.beta2) * gtau * gtau;
@@ -314,7 +314,7 @@ __global__ void __launch_bounds__(32) fc_reduce_kernel(StepArgs a) {
 // each rank applies the same updates in the same arithmetic -> identical table replicas.
 __global__ void fc_indiv_update_kernel(StepArgs a) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= a.B) return;
+  if (i >= a.B || *a.err == kErrOwnership) return;   // a rejected batch writes no table entry
   const int k = i / a.Bl;
   const int r = i % a.Bl;
   const double* blk = a.recv + static_cast<size_t>(k) * a.pstride;
@@ -327,7 +327,7 @@ __global__ void fc_indiv_update_kernel(StepArgs a) {
   long long* ss[2] = {a.s1_tab, a.s2_tab};
   for (int t = 0; t < 2; ++t) {
     const double g = gts[t];
-    if (!isfinite(g)) { *a.err = 9; return; }
+    if (!isfinite(g)) { atomicCAS(a.err, 0, kErrNumeric); return; }
     double m = ms[t][id], v = vs[t][id];
     const long long st = ss[t][id];
     m = a.beta1 * m + (1.0 - a.beta1) * g;

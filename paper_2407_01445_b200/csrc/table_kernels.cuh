@@ -81,13 +81,16 @@ struct StepArgs {
   long long* dbg;                        // FC_SIM_DEBUG=9: per-block globaltimer stamps of fc_anchor_kernel
   int prep_row0, prep_rows;              // rows of the prep kernel (all of G, or this rank's L before the gather)
   int weights_replica_only;              // fc_weights_kernel: only the u replica update (parameters arrived)
+  unsigned long long* step_tag;          // the step's sequence number (prep writes it; pass 1's id set uses it)
 };
 
 __global__ void fc_prep_kernel(const __nv_bfloat16* __restrict__ e1, const __nv_bfloat16* __restrict__ e2,
-                               StepArgs a, double gamma, double eps);
+                               StepArgs a, double gamma, double eps, unsigned long long seq);
+// device-side error codes (first failure wins), the fc_status values of fastclip_b200.h
+constexpr int kErrShape = 2, kErrOwnership = 5, kErrNumeric = 9;
 __global__ void fc_weights_kernel(StepArgs a);
 __global__ void fc_anchor_kernel(StepArgs a);
-__global__ void fc_zero_kernel(float4* a0, float4* a1, long long n4);
+__global__ void fc_delay_kernel(long long ns);
 __global__ void fc_reduce_kernel(StepArgs a);
 __global__ void fc_indiv_update_kernel(StepArgs a);
 __global__ void fc_rows_kernel(const __nv_bfloat16* __restrict__ e1, const __nv_bfloat16* __restrict__ e2, int B,

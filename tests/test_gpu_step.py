@@ -182,3 +182,44 @@ def test_out_of_range_id_is_a_shape_error(variant):
     ok = np.ones(N, bool)
     ok[ids[(ids >= 0) & (ids < N)]] = False
     np.testing.assert_array_equal(u[ok], u0[ok])   # untouched entries identical
+
+
+@pytest.mark.parametrize("variant", ["fastclip_v3", "fastclip_v2"])
+def test_duplicate_id_is_an_ownership_violation(variant):
+    # an id twice in one rank's batch: the reference's owner check throws OwnershipViolation
+    # (state.cpp:47-49) before the write; the step reports FC_ERR_OWNERSHIP at the scalar readback
+    # and no u / tau table entry (and not the global tau) changes
+    import torch
+    import paper_2407_01445_b200 as P
+    N, B, d = 3000, 128, 64
+    ocfg = O.default_config(variant, N)
+    step = P.LossStep(gpu_cfg(ocfg, d, B))
+    u0 = S.warm_u(N, 3)
+    step.load_tables(u1=u0, u2=u0)
+    before = step.tables()
+    tau0 = step.tau_state()
+    b1, b2 = S.embeddings(B, d, 4)
+    ids = S.ids(B, N, 4)
+    ids[40] = ids[3]
+    step.step(to_dev_bf16(b1), to_dev_bf16(b2), torch.from_numpy(ids).cuda(), 0.6, 1e-14)
+    with pytest.raises(P.FastclipError) as e:
+        step.scalars()
+    assert e.value.code == 5 and e.value.kind == "OwnershipViolation"
+    after = step.tables()
+    for k in before:
+        np.testing.assert_array_equal(after[k], before[k])
+    assert step.tau_state()["tau"] == tau0["tau"]
+
+
+def test_distinct_ids_across_steps_reuse_the_id_set():
+    # the duplicate-id set is tagged per step: the same ids in consecutive steps are not repeats
+    import torch
+    import paper_2407_01445_b200 as P
+    N, B, d = 4096, 256, 64
+    ocfg = O.default_config("fastclip_v3", N)
+    step = P.LossStep(gpu_cfg(ocfg, d, B))
+    b1, b2 = S.embeddings(B, d, 9)
+    ids = torch.from_numpy(S.ids(B, N, 9)).cuda()
+    for _ in range(3):
+        step.step(to_dev_bf16(b1), to_dev_bf16(b2), ids, 0.6, 1e-14)
+        step.scalars()   # raises on a (false) ownership error
