@@ -208,6 +208,93 @@ int fc_grad_tau(int32_t variant, int32_t count, int64_t batch, const double* u1,
                 const double* dsum2, const double* t1, const double* t2, double eps, double rho, double tau,
                 int64_t n_train, double* gtau, double* gt1, double* gt2, void* stream);
 
+/* ---- on-disk state in the reference's binary formats ---- */
+
+/* UTable::write (state.cpp:73-76: int64 n + n doubles per track, u1 then u2) followed, for the
+ * individual-temperature variants, by IndividualTemp::write (state.cpp:133-144: tau1, tau2, tau0,
+ * then the {m, v, step} ScalarAdam records of both tracks): the context's device tables to `path`.
+ * Synchronises the device. FC_ERR_IO when the file cannot be written. */
+int fc_table_write(void* ctx, const char* path);
+/* UTable::read / IndividualTemp::read (state.cpp:87-95, :146-162) into the device tables.
+ * FC_ERR_IO on a truncated stream or differing track lengths (IoError), FC_ERR_SHAPE when the
+ * table size differs from n_train (UTable::load, state.cpp:78-81). */
+int fc_table_read(void* ctx, const char* path);
+
+/* The model part of an FCK1 checkpoint (io::Checkpoint, checkpoint.hpp:16-40): the loss step
+ * owns the temperature, its Adam state and latch, and the tables; the caller owns the rest. */
+typedef struct {
+  uint64_t seed;
+  int64_t next_epoch;
+  int64_t global_step;
+  int32_t image_shape[4];     /* TowerShape: kind (0 linear, 1 mlp), d_in, d_hidden, d_out */
+  int32_t text_shape[4];
+  int64_t n_params;           /* length of params / opt_m / opt_v */
+  double* params;             /* host [n_params] (read: filled when non-NULL and n_params matches) */
+  double* opt_m;
+  double* opt_v;
+  int64_t opt_step;
+} fc_model_state;
+
+/* write_checkpoint (checkpoint.cpp:57-82): magic "FCK1", the model part (NULL: empty model), then
+ * this context's tau, tau-Adam {m, v, step}, latch, u1, u2 and the IndividualTemp record. */
+int fc_checkpoint_write(void* ctx, const char* path, const fc_model_state* model);
+/* read_checkpoint (checkpoint.cpp:84-114) for a resume: restores tau / tau-Adam / latch / tables into
+ * the context and returns the model part in *model (may be NULL). FC_ERR_IO on a bad magic or a
+ * truncated file, FC_ERR_CONFIG when the IndividualTemp record does not match the variant. */
+int fc_checkpoint_read(void* ctx, const char* path, fc_model_state* model);
+
+/* ---- the model-side step after the loss step (§8(f) row 1), fp64 device arrays ---- */
+
+/* TwoTowerModel::forward (encoder.cpp:98-134) of one tower: kind 0 linear (theta = [W (d_out x
+ * d_in) | b]), kind 1 tanh-MLP (theta = [W1 | b1 | W2 | b2]); x [rows x d_in]; h [rows x d_hidden]
+ * (mlp, else NULL), z / e [rows x d_out], znorm [rows]; e_bf16 (may be NULL): e rounded to bf16, the
+ * loss step's input. *status (device int32) gets FC_ERR_NUMERIC for a row with |z| < 1e-12. */
+int fc_tower_forward(int32_t kind, int32_t rows, int32_t d_in, int32_t d_hidden, int32_t d_out, const double* theta,
+                     const double* x, double* h, double* z, double* e, double* znorm, uint16_t* e_bf16,
+                     int32_t* status, void* stream);
+/* TwoTowerModel::vjp (encoder.cpp:136-177): the loss step's dE (fp32 [rows x d_out]) through the
+ * normalisation Jacobian, cot_z = (cot - e (e . cot)) / |z|, into the tower's parameter gradient
+ * (accumulated into grad, the tower's slice of the flat gradient; assemble_packet, engine.cpp:268-276). */
+int fc_tower_vjp(int32_t kind, int32_t rows, int32_t d_in, int32_t d_hidden, int32_t d_out, const double* theta,
+                 const double* x, const double* h, const double* e, const double* znorm, const float* cot,
+                 double* grad, void* stream);
+/* all_reduce_mean "grad-reduce" (trainer.cpp:540-546, fabric.cpp:204-208) of a flat gradient over
+ * the context's ranks (in place; a no-op at world 1). */
+int fc_grad_allreduce_mean(void* ctx, double* grad, int64_t n, void* stream);
+/* opt::adamw_step (optimizers.cpp:33-41) on a flat parameter vector; *step is the host step counter
+ * (bias corrections 1 - beta^(step+1), then ++step). A non-finite gradient sets *status (device
+ * int32) to FC_ERR_NUMERIC and leaves theta / m / v unchanged (check_shapes, optimizers.cpp:13). */
+int fc_adamw_step(int64_t n, double* theta, double* m, double* v, int64_t* step, const double* grad, double lr,
+                  double beta1, double beta2, double eps, double weight_decay, int32_t* status, void* stream);
+/* opt::lamb_step (optimizers.cpp:43-63): per-layer trust ratios over the segments
+ * [seg_off[k], seg_off[k] + seg_len[k]) (host arrays), ratio 1 for a zero denominator or with
+ * force_alpha_one. Synchronises `stream` before returning. */
+int fc_lamb_step(int64_t n, double* theta, double* m, double* v, int64_t* step, const double* grad, double lr,
+                 double beta1, double beta2, double eps, double weight_decay, int32_t n_seg, const int64_t* seg_off,
+                 const int64_t* seg_len, int32_t force_alpha_one, int32_t* status, void* stream);
+const char* fc_model_last_error(void);
+
+/* ---- the step before the hot path: index stream and synthetic inputs (§8(f) row 4) ---- */
+
+/* BatchPlan (trainer.cpp:206-241) over the reference's RNG streams (rng.hpp:14-65: splitmix64
+ * stream ids, std::mt19937_64, rejection `below`, descending Fisher-Yates): epoch permutations and
+ * per-worker contiguous slices identical to the reference's. FC_ERR_CONFIG when the global batch
+ * does not divide n_train (trainer.cpp:208-213) or the world does not divide the batch. */
+int fc_batch_plan_create(int64_t n_train, int32_t global_batch, uint64_t seed, void** plan);
+int fc_batch_plan_destroy(void* plan);
+int64_t fc_batch_plan_iters_per_epoch(void* plan);
+int fc_batch_plan_permutation(void* plan, int64_t epoch, int32_t* out /* [n_train] */);
+int fc_batch_plan_local(void* plan, int64_t epoch, int64_t iter, int32_t worker, int32_t world,
+                        int32_t* out /* [global_batch / world] */);
+const char* fc_plan_last_error(void);
+/* SURVEY.md §8(d) synthetic inputs from the seed's rng.hpp streams: unit-norm E1 rows and
+ * E2 = normalize(E1 + sigma N(0, I)), rounded to bf16 (host arrays [rows x dim] of bf16 bits); and
+ * `count` distinct ids in [0, n) by a partial Fisher-Yates. */
+int fc_synthetic_embeddings(uint64_t seed, int32_t rows, int32_t dim, double sigma, uint16_t* e1, uint16_t* e2);
+int fc_synthetic_ids(uint64_t seed, int32_t count, int64_t n, int32_t* ids);
+/* a warm u table: log10 u ~ U[-8, 0] (the paper's u percentiles), host [n] */
+int fc_synthetic_warm_u(uint64_t seed, int64_t n, double* out);
+
 const char* fc_last_error(void);
 
 #ifdef __cplusplus

@@ -175,6 +175,29 @@ def lib(kind: str = "oracle"):
             L.ref_gamma_cosine.argtypes = [C.c_longlong, C.c_longlong, C.c_longlong, D]
             L.ref_safe_exp.argtypes = [D]
             L.ref_exp_clamp_count.restype = C.c_ulonglong
+            # ref_next.cpp: the §8(f) rows next to the loss step (state / checkpoint formats, index
+            # plan, model optimizers, reduce-scatter pieces, wire model)
+            LL, ULL, CP = C.c_longlong, C.c_ulonglong, C.c_char_p
+            LP = C.POINTER(C.c_longlong)
+            L.ref_tables_write.argtypes = [CP, LL, _DP, _DP, _DP, _DP, D, _DP, _DP, LP, _DP, _DP, LP]
+            L.ref_tables_read.argtypes = [CP, LL, I, _DP, _DP, _DP, _DP, _DP, _DP, _DP, LP, _DP, _DP, LP]
+            L.ref_checkpoint_rewrite.argtypes = [CP, CP]
+            L.ref_checkpoint_fields.argtypes = [CP, C.POINTER(ULL), LP, LP, LP, _DP, _DP, _DP, LP,
+                                                C.POINTER(I), C.POINTER(I)]
+            L.ref_checkpoint_make.argtypes = [CP, ULL, LL, LL, I, I, LL, _DP, _DP, _DP, LL, D, D, D, LL, I, LL,
+                                              _DP, _DP]
+            L.ref_batch_plan_local.argtypes = [LL, I, ULL, LL, LL, I, I, C.POINTER(C.c_int)]
+            L.ref_stream_seed2.restype = ULL
+            L.ref_stream_seed2.argtypes = [ULL, ULL, ULL, I]
+            L.ref_rng_normals.argtypes = [ULL, LL, _DP]
+            L.ref_rng_below.argtypes = [ULL, LL, ULL, C.POINTER(ULL)]
+            L.ref_adamw_step.argtypes = [LL, _DP, _DP, _DP, LP, _DP, D, D, D, D, D]
+            L.ref_lamb_step.argtypes = [LL, _DP, _DP, _DP, LP, _DP, D, D, D, D, D, I, LP, LP, I]
+            L.ref_rs_partials.argtypes = [I, I, _DP, _DP, _DP, _DP, _DP, _DP, I, I, _DP, _DP]
+            L.ref_rs_shard_scale.restype = D
+            L.ref_rs_shard_scale.argtypes = [I, I, LL]
+            L.ref_wire.restype = ULL
+            L.ref_wire.argtypes = [I, I, ULL]
     return _libs[kind]
 
 

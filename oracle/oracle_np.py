@@ -231,3 +231,44 @@ def _selftest():   # pragma: no cover -- manual timing
 
 if __name__ == "__main__":
     _selftest()
+
+
+# ---- the model-side step -- restatement of encoder.cpp:98-177 ----
+
+def tower_forward(kind: int, theta: np.ndarray, x: np.ndarray, d_hidden: int, d_out: int) -> dict:
+    """TwoTowerModel::forward (encoder.cpp:98-134): linear z = x W^T + b (:110-113) or tanh-MLP
+    (:115-123), then e = z / |z| row-wise (:125-132)."""
+    d_in = x.shape[1]
+    h = None
+    if kind == 0:
+        w = theta[:d_out * d_in].reshape(d_out, d_in)
+        b = theta[d_out * d_in:d_out * d_in + d_out]
+        z = x @ w.T + b
+    else:
+        H = d_hidden
+        w1 = theta[:H * d_in].reshape(H, d_in)
+        b1 = theta[H * d_in:H * d_in + H]
+        o = H * d_in + H
+        w2 = theta[o:o + d_out * H].reshape(d_out, H)
+        b2 = theta[o + d_out * H:o + d_out * H + d_out]
+        h = np.tanh(x @ w1.T + b1)
+        z = h @ w2.T + b2
+    zn = np.sqrt(np.sum(z * z, axis=1))
+    return dict(x=x, h=h, z=z, e=z / zn[:, None], znorm=zn)
+
+
+def tower_vjp(kind: int, theta: np.ndarray, tape: dict, cot: np.ndarray) -> np.ndarray:
+    """TwoTowerModel::vjp (encoder.cpp:136-177) -> the tower's parameter gradient."""
+    e, zn, x, h = tape["e"], tape["znorm"], tape["x"], tape["h"]
+    radial = np.sum(e * cot, axis=1, keepdims=True)               # encoder.cpp:153
+    cz = (cot - radial * e) / zn[:, None]                          # :154
+    d_out, d_in = e.shape[1], x.shape[1]
+    if kind == 0:                                                  # :158-163
+        return np.concatenate([(cz.T @ x).ravel(), cz.sum(axis=0)])
+    H = h.shape[1]
+    o = H * d_in + H
+    w2 = theta[o:o + d_out * H].reshape(d_out, H)
+    gw2 = cz.T @ h                                                 # :172
+    gb2 = cz.sum(axis=0)
+    ca = (cz @ w2) * (1.0 - h * h)                                 # :174-175
+    return np.concatenate([(ca.T @ x).ravel(), ca.sum(axis=0), gw2.ravel(), gb2])

@@ -23,6 +23,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <fstream>
 #include <string>
 #include <vector>
 
@@ -939,6 +940,118 @@ int guarded(Fn&& fn) {
   }
 }
 
+// ---- the reference's binary formats (state.cpp:11-33, :73-95, :133-162; checkpoint.cpp:9-114) ----
+// Vectors are int64 length + doubles; ScalarAdam is {double m, double v, long long step}; FCK1 is the
+// field sequence of write_checkpoint. Tables are staged through host memory.
+struct BinOut {
+  std::ofstream os;
+  explicit BinOut(const char* path) : os(path, std::ios::binary | std::ios::trunc) {
+    if (!os) throw FcError{FC_ERR_IO, std::string("cannot open '") + path + "' for writing"};
+  }
+  void raw(const void* p, size_t n) { os.write(static_cast<const char*>(p), static_cast<std::streamsize>(n)); }
+  template <class T> void pod(const T& v) { raw(&v, sizeof(T)); }
+  void vec(const double* p, int64_t n) {
+    pod(n);
+    raw(p, sizeof(double) * static_cast<size_t>(n));
+  }
+  void check() {
+    if (!os) throw FcError{FC_ERR_IO, "write failed"};
+  }
+};
+struct BinIn {
+  std::ifstream is;
+  explicit BinIn(const char* path) : is(path, std::ios::binary) {
+    if (!is) throw FcError{FC_ERR_IO, std::string("cannot open '") + path + "'"};
+  }
+  void raw(void* p, size_t n) {
+    is.read(static_cast<char*>(p), static_cast<std::streamsize>(n));
+    if (!is) throw FcError{FC_ERR_IO, "truncated stream"};
+  }
+  template <class T> T pod() {
+    T v;
+    raw(&v, sizeof(T));
+    return v;
+  }
+  std::vector<double> vec() {
+    const int64_t n = pod<int64_t>();
+    if (n < 0) throw FcError{FC_ERR_IO, "negative vector length"};
+    std::vector<double> v(static_cast<size_t>(n));
+    raw(v.data(), sizeof(double) * v.size());
+    return v;
+  }
+};
+
+// UTable::write (state.cpp:73-76) + IndividualTemp::write (state.cpp:133-144) of a context.
+void write_tables(LossStep* s, BinOut& o) {
+  FC_CUDA(cudaDeviceSynchronize());
+  const size_t n = static_cast<size_t>(s->cfg.n_train);
+  std::vector<double> h(n);
+  for (double* t : {s->u1, s->u2}) {
+    FC_CUDA(cudaMemcpy(h.data(), t, n * 8, cudaMemcpyDeviceToHost));
+    o.vec(h.data(), static_cast<int64_t>(n));
+  }
+}
+void write_individual(LossStep* s, BinOut& o) {
+  const size_t n = static_cast<size_t>(s->cfg.n_train);
+  std::vector<double> h(n);
+  for (double* t : {s->tau1, s->tau2}) {
+    FC_CUDA(cudaMemcpy(h.data(), t, n * 8, cudaMemcpyDeviceToHost));
+    o.vec(h.data(), static_cast<int64_t>(n));
+  }
+  o.pod(s->cfg.tau0);
+  std::vector<double> m(n), v(n);
+  std::vector<long long> st(n);
+  std::vector<uint8_t> aos(n * 24);   // ScalarAdam records, AoS (state.cpp:137-143)
+  for (int t = 0; t < 2; ++t) {
+    FC_CUDA(cudaMemcpy(m.data(), t ? s->m2 : s->m1, n * 8, cudaMemcpyDeviceToHost));
+    FC_CUDA(cudaMemcpy(v.data(), t ? s->v2 : s->v1, n * 8, cudaMemcpyDeviceToHost));
+    FC_CUDA(cudaMemcpy(st.data(), t ? s->s2 : s->s1, n * 8, cudaMemcpyDeviceToHost));
+    for (size_t i = 0; i < n; ++i) {
+      std::memcpy(&aos[24 * i], &m[i], 8);
+      std::memcpy(&aos[24 * i + 8], &v[i], 8);
+      std::memcpy(&aos[24 * i + 16], &st[i], 8);
+    }
+    o.raw(aos.data(), aos.size());
+  }
+}
+// UTable::read (state.cpp:87-95) + IndividualTemp::read (state.cpp:146-162) into a context.
+void read_tables(LossStep* s, BinIn& in) {
+  const size_t n = static_cast<size_t>(s->cfg.n_train);
+  const std::vector<double> a = in.vec(), b = in.vec();
+  if (a.size() != b.size()) throw FcError{FC_ERR_IO, "UTable: track lengths differ"};
+  if (a.size() != n) throw FcError{FC_ERR_SHAPE, "UTable::load: size mismatch with n_train"};
+  FC_CUDA(cudaDeviceSynchronize());
+  FC_CUDA(cudaMemcpy(s->u1, a.data(), n * 8, cudaMemcpyHostToDevice));
+  FC_CUDA(cudaMemcpy(s->u2, b.data(), n * 8, cudaMemcpyHostToDevice));
+}
+void read_individual(LossStep* s, BinIn& in) {
+  const size_t n = static_cast<size_t>(s->cfg.n_train);
+  const std::vector<double> t1 = in.vec(), t2 = in.vec();
+  if (t1.size() != t2.size()) throw FcError{FC_ERR_IO, "IndividualTemp: track lengths differ"};
+  if (t1.size() != n) throw FcError{FC_ERR_SHAPE, "IndividualTemp: size mismatch with n_train"};
+  const double tau0 = in.pod<double>();
+  if (tau0 != s->cfg.tau0) throw FcError{FC_ERR_CONFIG, "IndividualTemp: tau0 differs from temperature.tau0"};
+  std::vector<uint8_t> aos(n * 24);
+  std::vector<double> m(n), v(n);
+  std::vector<long long> st(n);
+  FC_CUDA(cudaDeviceSynchronize());
+  FC_CUDA(cudaMemcpy(s->tau1, t1.data(), n * 8, cudaMemcpyHostToDevice));
+  FC_CUDA(cudaMemcpy(s->tau2, t2.data(), n * 8, cudaMemcpyHostToDevice));
+  for (int t = 0; t < 2; ++t) {
+    in.raw(aos.data(), aos.size());
+    for (size_t i = 0; i < n; ++i) {
+      std::memcpy(&m[i], &aos[24 * i], 8);
+      std::memcpy(&v[i], &aos[24 * i + 8], 8);
+      std::memcpy(&st[i], &aos[24 * i + 16], 8);
+    }
+    FC_CUDA(cudaMemcpy(t ? s->m2 : s->m1, m.data(), n * 8, cudaMemcpyHostToDevice));
+    FC_CUDA(cudaMemcpy(t ? s->v2 : s->v1, v.data(), n * 8, cudaMemcpyHostToDevice));
+    FC_CUDA(cudaMemcpy(t ? s->s2 : s->s1, st.data(), n * 8, cudaMemcpyHostToDevice));
+  }
+}
+
+constexpr uint32_t kFck1Magic = 0x46434b31;   // "FCK1" (checkpoint.cpp:9)
+
 }  // namespace
 
 extern "C" {
@@ -1526,6 +1639,124 @@ int fc_embedding_cotangents(const void* e1g, const void* e2g, int32_t batch, int
     CUtensorMap mX[2] = {m2n, m1n};
     FC_CUDA(fc::launch_gemm(false, gp, mQ, mX, mO, gemm_ctas, st));
     FC_CUDA(cudaFreeAsync(ws, st));
+  });
+}
+
+__global__ void fc_scale_kernel(double* x, long long n, double s) {
+  for (long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<long long>(gridDim.x) * blockDim.x)
+    x[i] *= s;
+}
+
+// all_reduce_mean "grad-reduce" (trainer.cpp:540-546): sum over the ranks, then / K
+// (reduce_mean, fabric.cpp:73-83; NCCL's summation order is not the fabric's ascending order).
+int fc_grad_allreduce_mean(void* ctx, double* grad, int64_t n, void* stream) {
+  if (!ctx || (!grad && n > 0) || n < 0) return FC_ERR_SHAPE;
+  auto* s = static_cast<LossStep*>(ctx);
+  return guarded([&] {
+    if (s->K == 1 || n == 0) return;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    FC_NCCL(ncclAllReduce(grad, grad, static_cast<size_t>(n), ncclFloat64, ncclSum, s->comm, st));
+    const long long g = std::min<long long>(4096, (n + 255) / 256);
+    fc_scale_kernel<<<static_cast<int>(g), 256, 0, st>>>(grad, n, 1.0 / static_cast<double>(s->K));
+    FC_CUDA(cudaGetLastError());
+  });
+}
+
+int fc_table_write(void* ctx, const char* path) {
+  if (!ctx || !path) return FC_ERR_SHAPE;
+  auto* s = static_cast<LossStep*>(ctx);
+  return guarded([&] {
+    BinOut o(path);
+    write_tables(s, o);
+    if (s->indiv) write_individual(s, o);
+    o.check();
+  });
+}
+
+int fc_table_read(void* ctx, const char* path) {
+  if (!ctx || !path) return FC_ERR_SHAPE;
+  auto* s = static_cast<LossStep*>(ctx);
+  return guarded([&] {
+    BinIn in(path);
+    read_tables(s, in);
+    if (s->indiv) read_individual(s, in);
+  });
+}
+
+int fc_checkpoint_write(void* ctx, const char* path, const fc_model_state* model) {
+  if (!ctx || !path) return FC_ERR_SHAPE;
+  auto* s = static_cast<LossStep*>(ctx);
+  return guarded([&] {
+    fc_model_state empty{};
+    const fc_model_state& m = model ? *model : empty;
+    if (m.n_params < 0 || (m.n_params > 0 && (!m.params || !m.opt_m || !m.opt_v)))
+      throw FcError{FC_ERR_SHAPE, "checkpoint: model arrays missing"};
+    fc::TauState ts;
+    FC_CUDA(cudaDeviceSynchronize());
+    FC_CUDA(cudaMemcpy(&ts, s->tau_state, sizeof(ts), cudaMemcpyDeviceToHost));
+    BinOut o(path);
+    o.pod(kFck1Magic);
+    o.pod(m.seed);
+    o.pod(m.next_epoch);
+    o.pod(m.global_step);
+    o.raw(m.image_shape, 16);
+    o.raw(m.text_shape, 16);
+    std::vector<double> zero;
+    o.vec(m.n_params ? m.params : zero.data(), m.n_params);
+    o.vec(m.n_params ? m.opt_m : zero.data(), m.n_params);
+    o.vec(m.n_params ? m.opt_v : zero.data(), m.n_params);
+    o.pod(m.opt_step);
+    o.pod(ts.tau);
+    o.pod(ts.m);
+    o.pod(ts.v);
+    o.pod(ts.step);
+    o.pod(static_cast<uint8_t>(ts.latched ? 1 : 0));
+    write_tables(s, o);
+    o.pod(static_cast<uint8_t>(s->indiv ? 1 : 0));
+    if (s->indiv) write_individual(s, o);
+    o.check();
+  });
+}
+
+int fc_checkpoint_read(void* ctx, const char* path, fc_model_state* model) {
+  if (!ctx || !path) return FC_ERR_SHAPE;
+  auto* s = static_cast<LossStep*>(ctx);
+  return guarded([&] {
+    BinIn in(path);
+    if (in.pod<uint32_t>() != kFck1Magic) throw FcError{FC_ERR_IO, std::string("bad magic in '") + path + "'"};
+    fc_model_state m{};
+    m.seed = in.pod<uint64_t>();
+    m.next_epoch = in.pod<int64_t>();
+    m.global_step = in.pod<int64_t>();
+    in.raw(m.image_shape, 16);
+    in.raw(m.text_shape, 16);
+    const std::vector<double> params = in.vec(), om = in.vec(), ov = in.vec();
+    m.n_params = static_cast<int64_t>(params.size());
+    m.opt_step = in.pod<int64_t>();
+    fc::TauState ts{};
+    ts.tau = in.pod<double>();
+    ts.m = in.pod<double>();
+    ts.v = in.pod<double>();
+    ts.step = in.pod<long long>();
+    ts.latched = in.pod<uint8_t>() != 0;
+    read_tables(s, in);
+    const bool has_ind = in.pod<uint8_t>() != 0;
+    if (has_ind != s->indiv)
+      throw FcError{FC_ERR_CONFIG, "checkpoint: IndividualTemp presence does not match the variant"};
+    if (has_ind) read_individual(s, in);
+    FC_CUDA(cudaMemcpy(s->tau_state, &ts, sizeof(ts), cudaMemcpyHostToDevice));
+    if (model) {
+      if (model->params && model->n_params == m.n_params) {
+        std::memcpy(model->params, params.data(), params.size() * 8);
+        if (model->opt_m) std::memcpy(model->opt_m, om.data(), om.size() * 8);
+        if (model->opt_v) std::memcpy(model->opt_v, ov.data(), ov.size() * 8);
+      }
+      m.params = model->params;
+      m.opt_m = model->opt_m;
+      m.opt_v = model->opt_v;
+      *model = m;
+    }
   });
 }
 

@@ -68,6 +68,13 @@ class FcStepScalars(C.Structure):
                 ("exp_clamps", C.c_uint64), ("latched", C.c_int32)]
 
 
+class FcModelState(C.Structure):
+    _fields_ = [("seed", C.c_uint64), ("next_epoch", C.c_int64), ("global_step", C.c_int64),
+                ("image_shape", C.c_int32 * 4), ("text_shape", C.c_int32 * 4), ("n_params", C.c_int64),
+                ("params", C.POINTER(C.c_double)), ("opt_m", C.POINTER(C.c_double)),
+                ("opt_v", C.POINTER(C.c_double)), ("opt_step", C.c_int64)]
+
+
 _lib = None
 
 
@@ -108,6 +115,23 @@ def lib():
         L.fc_table_update.argtypes = [P, P, I64, P, P, P, I32, D, P, P, P, P]
         L.fc_grad_tau.argtypes = [I32, I32, I64, P, P, P, P, P, P, D, D, D, I64, P, P, P, P]
         L.fc_last_error.restype = C.c_char_p
+        L.fc_table_write.argtypes = [P, C.c_char_p]
+        L.fc_table_read.argtypes = [P, C.c_char_p]
+        L.fc_checkpoint_write.argtypes = [P, C.c_char_p, C.POINTER(FcModelState)]
+        L.fc_checkpoint_read.argtypes = [P, C.c_char_p, C.POINTER(FcModelState)]
+        L.fc_batch_plan_create.argtypes = [I64, I32, C.c_uint64, C.POINTER(P)]
+        L.fc_batch_plan_destroy.argtypes = [P]
+        L.fc_batch_plan_iters_per_epoch.argtypes = [P]
+        L.fc_batch_plan_iters_per_epoch.restype = I64
+        L.fc_batch_plan_permutation.argtypes = [P, I64, C.POINTER(C.c_int32)]
+        L.fc_batch_plan_local.argtypes = [P, I64, I64, I32, I32, C.POINTER(C.c_int32)]
+        L.fc_plan_last_error.restype = C.c_char_p
+        L.fc_tower_forward.argtypes = [I32, I32, I32, I32, I32, P, P, P, P, P, P, P, P, P]
+        L.fc_tower_vjp.argtypes = [I32, I32, I32, I32, I32, P, P, P, P, P, P, P, P]
+        L.fc_grad_allreduce_mean.argtypes = [P, P, I64, P]
+        L.fc_adamw_step.argtypes = [I64, P, P, P, LP, P, D, D, D, D, D, P, P]
+        L.fc_lamb_step.argtypes = [I64, P, P, P, LP, P, D, D, D, D, D, I32, LP, LP, I32, P, P]
+        L.fc_model_last_error.restype = C.c_char_p
         _lib = L
     return _lib
 
@@ -118,7 +142,11 @@ EXPORTED = [
     "fc_table_upload", "fc_tau_state_get", "fc_tau_state_set", "fc_kernels_per_step",
     "fc_debug_similarity", "fc_last_error", "fc_set_phase_timing", "fc_phase_times", "fc_g_values",
     "fc_embedding_cotangents", "fc_temperature_step", "fc_table_update",
-    "fc_grad_tau",
+    "fc_grad_tau", "fc_table_write", "fc_table_read", "fc_checkpoint_write", "fc_checkpoint_read",
+    "fc_batch_plan_create", "fc_batch_plan_destroy", "fc_batch_plan_iters_per_epoch", "fc_batch_plan_permutation",
+    "fc_batch_plan_local", "fc_plan_last_error", "fc_synthetic_embeddings", "fc_synthetic_ids", "fc_synthetic_warm_u",
+    "fc_tower_forward", "fc_tower_vjp", "fc_grad_allreduce_mean", "fc_adamw_step", "fc_lamb_step",
+    "fc_model_last_error",
 ]
 PHASES = ["allgather_e", "prep", "pass1_stats", "tables_tau", "pass2_q", "grad_gemm"]
 
@@ -268,6 +296,42 @@ class LossStep:
             out.append(a.ctypes.data_as(C.POINTER(typ)) if a is not None else None)
         return out
 
+    def write_tables(self, path: str):
+        """UTable::write (+ IndividualTemp::write) of the device tables (state.cpp:73-76, :133-144)."""
+        _check(lib().fc_table_write(self._h, os.fsencode(path)))
+
+    def read_tables(self, path: str):
+        """UTable::read (+ IndividualTemp::read) into the device tables (state.cpp:87-95, :146-162)."""
+        _check(lib().fc_table_read(self._h, os.fsencode(path)))
+
+    def write_checkpoint(self, path: str, model: dict | None = None):
+        """write_checkpoint (checkpoint.cpp:57-82): FCK1 with the caller's model part (dict with
+        seed, next_epoch, global_step, image_shape, text_shape, params, opt_m, opt_v, opt_step)."""
+        ms, keep = _model_state(model)
+        _check(lib().fc_checkpoint_write(self._h, os.fsencode(path), C.byref(ms)))
+        del keep
+
+    def read_checkpoint(self, path: str) -> dict:
+        """read_checkpoint (checkpoint.cpp:84-114): restores tau, its Adam state, the latch and the
+        tables into this context; returns the model part."""
+        probe = FcModelState()
+        _check(lib().fc_checkpoint_read(self._h, os.fsencode(path), C.byref(probe)))
+        n = probe.n_params
+        arrs = {k: np.zeros(n) for k in ("params", "opt_m", "opt_v")}
+        ms = FcModelState()
+        ms.n_params = n
+        for k, a in arrs.items():
+            setattr(ms, k, a.ctypes.data_as(C.POINTER(C.c_double)))
+        _check(lib().fc_checkpoint_read(self._h, os.fsencode(path), C.byref(ms)))
+        return dict(seed=ms.seed, next_epoch=ms.next_epoch, global_step=ms.global_step,
+                    image_shape=list(ms.image_shape), text_shape=list(ms.text_shape), opt_step=ms.opt_step, **arrs)
+
+    def grad_allreduce_mean(self, grad, stream=None):
+        """all_reduce_mean "grad-reduce" (trainer.cpp:540-546) of a CUDA fp64 gradient, in place."""
+        import torch
+        stream = stream or torch.cuda.current_stream(grad.device)
+        _check(lib().fc_grad_allreduce_mean(self._h, _dptr(grad), grad.numel(), C.c_void_p(stream.cuda_stream)))
+
     def tau_state(self) -> dict:
         tau, m, v = C.c_double(), C.c_double(), C.c_double()
         st, lat = C.c_int64(), C.c_int32()
@@ -276,6 +340,63 @@ class LossStep:
 
     def set_tau_state(self, tau: float, m: float = 0.0, v: float = 0.0, step: int = 0, latched: int = 0):
         _check(lib().fc_tau_state_set(self._h, tau, m, v, step, latched))
+
+
+def _model_state(model: dict | None):
+    ms = FcModelState()
+    keep = []
+    if model:
+        ms.seed = int(model.get("seed", 0))
+        ms.next_epoch = int(model.get("next_epoch", 0))
+        ms.global_step = int(model.get("global_step", 0))
+        for k in ("image_shape", "text_shape"):
+            getattr(ms, k)[:] = [int(x) for x in model.get(k, (0, 0, 0, 0))]
+        n = len(model.get("params", ()))
+        ms.n_params = n
+        for k in ("params", "opt_m", "opt_v"):
+            a = np.ascontiguousarray(model.get(k, np.zeros(n)), dtype=np.float64)
+            if a.shape != (n,):
+                raise FastclipError(2, f"model {k} must have {n} entries")
+            keep.append(a)
+            setattr(ms, k, a.ctypes.data_as(C.POINTER(C.c_double)))
+        ms.opt_step = int(model.get("opt_step", 0))
+    return ms, keep
+
+
+class BatchPlan:
+    """The reference's index stream (BatchPlan, trainer.cpp:206-241) over its RNG streams
+    (rng.hpp:14-65), host side: per-epoch permutations and contiguous per-worker slices."""
+
+    def __init__(self, n_train: int, global_batch: int, seed: int):
+        self._h = C.c_void_p()
+        rc = lib().fc_batch_plan_create(int(n_train), int(global_batch), int(seed), C.byref(self._h))
+        if rc:
+            raise FastclipError(rc, lib().fc_plan_last_error().decode())
+        self.n_train, self.global_batch = int(n_train), int(global_batch)
+
+    def __del__(self):
+        try:
+            if self._h:
+                lib().fc_batch_plan_destroy(self._h)
+        except Exception:
+            pass
+
+    @property
+    def iters_per_epoch(self) -> int:
+        return int(lib().fc_batch_plan_iters_per_epoch(self._h))
+
+    def permutation(self, epoch: int) -> np.ndarray:
+        out = np.empty(self.n_train, np.int32)
+        _check(lib().fc_batch_plan_permutation(self._h, int(epoch), out.ctypes.data_as(C.POINTER(C.c_int32))))
+        return out
+
+    def local_batch(self, epoch: int, it: int, worker: int = 0, world: int = 1) -> np.ndarray:
+        out = np.empty(self.global_batch // max(world, 1), np.int32)
+        rc = lib().fc_batch_plan_local(self._h, int(epoch), int(it), int(worker), int(world),
+                                       out.ctypes.data_as(C.POINTER(C.c_int32)))
+        if rc:
+            raise FastclipError(rc, lib().fc_plan_last_error().decode())
+        return out
 
 
 def g_values(e1g, e2g, t1_local, t2_local, local_begin: int, local_count: int, dtau_sums: bool = True):
@@ -375,3 +496,80 @@ def debug_similarity(a, b):
     stream = torch.cuda.current_stream(a.device)
     _check(lib().fc_debug_similarity(_dptr(a), _dptr(b), rows, cols, d, _dptr(out), C.c_void_p(stream.cuda_stream)))
     return out
+
+
+# ---- the model-side step after the loss step ----
+
+def _model_check(rc: int):
+    if rc != 0:
+        raise FastclipError(rc, lib().fc_model_last_error().decode(errors="replace"))
+
+
+def tower_param_count(kind: int, d_in: int, d_hidden: int, d_out: int) -> int:
+    """TowerShape::param_count (encoder.cpp:20-23)."""
+    return d_out * d_in + d_out if kind == 0 else d_hidden * d_in + d_hidden + d_out * d_hidden + d_out
+
+
+def tower_forward(kind: int, theta, x, d_hidden: int, d_out: int):
+    """TwoTowerModel::forward (encoder.cpp:98-134) of one tower on CUDA fp64 tensors: returns the
+    tape {x, h, z, e, znorm, e_bf16} (e_bf16: the loss step's input)."""
+    import torch
+    rows, d_in = x.shape
+    dev = x.device
+    tape = dict(x=x, h=torch.empty(rows, d_hidden, device=dev, dtype=torch.float64) if kind == 1 else None,
+                z=torch.empty(rows, d_out, device=dev, dtype=torch.float64),
+                e=torch.empty(rows, d_out, device=dev, dtype=torch.float64),
+                znorm=torch.empty(rows, device=dev, dtype=torch.float64),
+                e_bf16=torch.empty(rows, d_out, device=dev, dtype=torch.bfloat16))
+    status = torch.zeros(1, device=dev, dtype=torch.int32)
+    st = torch.cuda.current_stream(dev)
+    ptr = lambda t: _dptr(t) if t is not None else None
+    _model_check(lib().fc_tower_forward(kind, rows, d_in, d_hidden, d_out, _dptr(theta), _dptr(x), ptr(tape["h"]),
+                                        _dptr(tape["z"]), _dptr(tape["e"]), _dptr(tape["znorm"]), _dptr(tape["e_bf16"]),
+                                        _dptr(status), C.c_void_p(st.cuda_stream)))
+    if int(status.item()):
+        raise FastclipError(int(status.item()), "forward: pre-normalization embedding is numerically zero")
+    return tape
+
+
+def tower_vjp(kind: int, theta, tape: dict, cot, grad):
+    """TwoTowerModel::vjp (encoder.cpp:136-177): accumulates the tower gradient of the fp32
+    cotangent `cot` (the loss step's dE) into `grad` (CUDA fp64, the tower's slice)."""
+    import torch
+    rows, d_out = tape["e"].shape
+    d_in = tape["x"].shape[1]
+    d_hidden = tape["h"].shape[1] if tape["h"] is not None else 0
+    st = torch.cuda.current_stream(cot.device)
+    ptr = lambda t: _dptr(t) if t is not None else None
+    _model_check(lib().fc_tower_vjp(kind, rows, d_in, d_hidden, d_out, _dptr(theta), _dptr(tape["x"]), ptr(tape["h"]),
+                                    _dptr(tape["e"]), _dptr(tape["znorm"]), _dptr(cot.contiguous()), _dptr(grad),
+                                    C.c_void_p(st.cuda_stream)))
+
+
+def adamw_step(theta, m, v, state: dict, grad, lr: float, beta1=0.9, beta2=0.999, eps=1e-8, weight_decay=0.0) -> int:
+    """opt::adamw_step (optimizers.cpp:33-41) on CUDA fp64 tensors; state {"step"} updated.
+    Returns the device status (0, or FC_ERR_NUMERIC for a non-finite gradient)."""
+    import torch
+    status = torch.zeros(1, device=theta.device, dtype=torch.int32)
+    stp = C.c_int64(state["step"])
+    st = torch.cuda.current_stream(theta.device)
+    _model_check(lib().fc_adamw_step(theta.numel(), _dptr(theta), _dptr(m), _dptr(v), C.byref(stp), _dptr(grad), lr,
+                                     beta1, beta2, eps, weight_decay, _dptr(status), C.c_void_p(st.cuda_stream)))
+    state["step"] = stp.value
+    return int(status.item())
+
+
+def lamb_step(theta, m, v, state: dict, grad, lr: float, segments, beta1=0.9, beta2=0.999, eps=1e-8,
+              weight_decay=0.0, force_alpha_one=False) -> int:
+    """opt::lamb_step (optimizers.cpp:43-63) with layer `segments` [(offset, size), ...]."""
+    import torch
+    status = torch.zeros(1, device=theta.device, dtype=torch.int32)
+    off = (C.c_int64 * len(segments))(*[int(o) for o, _ in segments])
+    ln = (C.c_int64 * len(segments))(*[int(n) for _, n in segments])
+    stp = C.c_int64(state["step"])
+    st = torch.cuda.current_stream(theta.device)
+    _model_check(lib().fc_lamb_step(theta.numel(), _dptr(theta), _dptr(m), _dptr(v), C.byref(stp), _dptr(grad), lr,
+                                    beta1, beta2, eps, weight_decay, len(segments), off, ln, int(force_alpha_one),
+                                    _dptr(status), C.c_void_p(st.cuda_stream)))
+    state["step"] = stp.value
+    return int(status.item())

@@ -300,3 +300,46 @@ def test_stalled_peer_aborts_the_collective():
         p.join(timeout=60)
     assert res[1] == [0, 0]
     assert res[0][:2] == [0, 0] and res[0][2] == 8, res[0]
+
+
+def _allreduce_worker(rank, K, nccl_id, q):
+    import torch
+    import paper_2407_01445_b200 as P
+    from gpu_helpers import gpu_cfg
+    try:
+        torch.cuda.set_device(rank)
+        ocfg = O.default_config("fastclip_v3", 4096)
+        cfg = gpu_cfg(ocfg, 64, 64, world=K, rank=rank, device=rank)
+        for i, b in enumerate(nccl_id):
+            cfg.nccl_id[i] = b
+        step = P.LossStep(cfg)
+        g = torch.full((1000,), float(rank + 1), dtype=torch.float64, device=f"cuda:{rank}")
+        g[7] = 10.0 * rank
+        step.grad_allreduce_mean(g)
+        q.put((rank, g.cpu().numpy(), None))
+        step.close()
+    except Exception as e:  # noqa: BLE001
+        q.put((rank, None, repr(e)))
+
+
+def test_grad_allreduce_mean():
+    # all_reduce_mean "grad-reduce" (trainer.cpp:540-546): every rank gets the mean over ranks
+    import torch
+    import torch.multiprocessing as mp
+    import paper_2407_01445_b200 as P
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs 2 GPUs")
+    nccl_id = P.nccl_unique_id()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_allreduce_worker, args=(r, 2, nccl_id, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    for _ in range(2):
+        rank, g, err = q.get(timeout=300)
+        assert err is None, err
+        exp = np.full(1000, 1.5)
+        exp[7] = 5.0
+        np.testing.assert_array_equal(g, exp)
+    for p in procs:
+        p.join(timeout=60)
