@@ -71,6 +71,9 @@ typedef struct {
   int32_t scale_by_tau;       /* loss.scale_by_tau resolved (trainer.cpp:184-194) */
   int32_t device;             /* CUDA device ordinal */
   uint8_t nccl_id[128];       /* ncclUniqueId from rank 0 (fc_nccl_unique_id), world > 1 */
+  int32_t reduction;          /* fabric.reduction (trainer.cpp:85-95): 0 fastclip (all-gather u, each rank
+                                 computes both loss terms), 1 openclip_rs (local weights only, the contrast
+                                 cotangents of the other ranks' anchors reduce-scattered; world > 1) */
 } fc_config;
 
 /* Inputs of one step (trainer.cpp:419-425 outputs + step scalars). */
@@ -294,6 +297,23 @@ int fc_synthetic_embeddings(uint64_t seed, int32_t rows, int32_t dim, double sig
 int fc_synthetic_ids(uint64_t seed, int32_t count, int64_t n, int32_t* ids);
 /* a warm u table: log10 u ~ U[-8, 0] (the paper's u percentiles), host [n] */
 int fc_synthetic_warm_u(uint64_t seed, int64_t n, double* out);
+
+/* CommLedger (fabric.hpp:34-58) of the context's steps: one entry per collective phase of the
+ * reference's fabric ("feature-gather", "u-gather", "tau-gather", "tau-reduce", "rs-grad") with its
+ * primitive (0 all_gather, 1 all_reduce, 2 reduce_scatter), the reference's wire elements
+ * (fabric.cpp:18-28 ring costs, accumulated over steps) and the bytes this rank actually stored to
+ * its peers for that phase (NVLink peer stores or NCCL payloads; the packed payload gather is
+ * split by its fields, and "replica-sync" carries what only the per-GPU table replicas need).
+ * Returns the number of entries written (<= max). */
+typedef struct {
+  char phase[24];
+  int32_t primitive;
+  int32_t world;
+  uint64_t elements;
+  uint64_t bytes;
+} fc_ledger_entry;
+int fc_comm_ledger(void* ctx, fc_ledger_entry* out, int32_t max);
+int fc_comm_ledger_reset(void* ctx);
 
 const char* fc_last_error(void);
 

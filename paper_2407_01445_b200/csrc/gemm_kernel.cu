@@ -155,8 +155,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           for (int h = 0; h < (half1 ? 2 : 1); ++h) {
             const int n0 = n_blk + h * kPairN + static_cast<int>(prank) * (kPairN / 2);
             uint8_t* dst = sb + h * kStageBytesB;
-            tma_load_2d_pair(mx, &L.full[stage], dst, n0, k0);
-            tma_load_2d_pair(mx, &L.full[stage], dst + kStageBytesB / 2, n0 + 64, k0);
+            tma_load_2d_pair(mx, &L.full[stage], dst, n0, k0 + p.seg[s].x_krow0);
+            tma_load_2d_pair(mx, &L.full[stage], dst + kStageBytesB / 2, n0 + 64, k0 + p.seg[s].x_krow0);
           }
         }
         __syncwarp();
@@ -260,7 +260,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       const bool row_ok = r_loc < sg.rows;
       // the unit holding k-block 0 adds the local term -c r o X_L exactly once per tile; its X
       // loads are software-pipelined one chunk ahead (the first before the accumulator wait)
-      const bool with_r = kb0 == 0;
+      const bool with_r = kb0 == 0 && sg.r != nullptr;
       const float cr = (row_ok && with_r) ? p.scale * sg.r[r_loc] : 0.f;
       const uint4* xrow = reinterpret_cast<const uint4*>(sg.x + static_cast<size_t>(sg.x_row0 + (row_ok ? r_loc : 0)) * p.d);
       uint4 xn[4];

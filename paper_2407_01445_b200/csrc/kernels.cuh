@@ -105,7 +105,8 @@ struct GemmSeg {
   int a_mn_major;            // 1: A = Q'^T read through an MN-major operand (K = 1 shares Q)
   int rows;                  // local anchors
   int x_row0;                // global index of local row 0 (for the r o X_local term)
-  const float* r;            // [rows]
+  int x_krow0;               // first row of X the K index maps to (0; rank * Bl for the reduce-scatter partials)
+  const float* r;            // [rows], or NULL: no local term
   const __nv_bfloat16* x;    // [B][d] row-major (the B operand, read for the r term)
   float* out;                // [rows][d], zeroed before the GEMM (reduce-add target)
 };

@@ -167,6 +167,27 @@ struct LossStep {
   float* rcoef = nullptr;
   __nv_bfloat16* q = nullptr;   // [2][Bl][ldq]
   int* err = nullptr;
+  // openclip_rs (fabric.reduction = openclip_rs, K > 1): the other ranks' anchors get zero
+  // pass-2 weights here; their contrast cotangents arrive reduce-scattered (trainer.cpp:492-537)
+  bool rs = false;
+  float* rs_part = nullptr;    // [2][B][d] fp32: for_e1, for_e2 (engine.cpp:123-144) of this rank's anchors
+  float* rs_shard = nullptr;   // [2][Bl][d] fp32: the reduce-scattered sums for this rank's rows
+  CUtensorMap mQtRS[2], mPart[2];
+  struct LedgerRow {
+    std::string phase;
+    int primitive;
+    unsigned long long elements, bytes;
+  };
+  std::vector<LedgerRow> ledger;
+  void book(const char* phase, int prim, unsigned long long elements, unsigned long long bytes) {
+    for (auto& r : ledger)
+      if (r.phase == phase) {
+        r.elements += elements;
+        r.bytes += bytes;
+        return;
+      }
+    ledger.push_back({phase, prim, elements, bytes});
+  }
   long long test_delay_ns = 0;           // FC_TEST_DELAY_US (tests only, K > 1): this rank stalls after
                                          // the payload gather, before pass 2 (rank-skew stress test)
   unsigned long long* idset = nullptr;   // duplicate-id set (pass 1's non-leader MMA warps)
@@ -307,6 +328,19 @@ struct LossStep {
     FC_CUDA(cudaMemset(idset, 0, idset_slots * sizeof(unsigned long long)));
     step_tag = dalloc<unsigned long long>(1);
     FC_CUDA(cudaMemset(step_tag, 0, sizeof(unsigned long long)));
+    rs = K > 1 && cfg.reduction == 1;
+    if (cfg.reduction < 0 || cfg.reduction > 1) throw FcError{FC_ERR_CONFIG, "fabric.reduction: expected 0 (fastclip) or 1 (openclip_rs)"};
+    if (rs) {
+      if (Bl % 64 != 0) throw FcError{FC_ERR_UNSUPPORTED, "openclip_rs needs a local batch that is a multiple of 64"};
+      rs_part = dalloc<float>(2 * static_cast<size_t>(B) * d);
+      rs_shard = dalloc<float>(2 * static_cast<size_t>(Bl) * d);
+      for (int s2 = 0; s2 < 2; ++s2) {
+        // Q'_C^T / Q'_R^T as MN-major A operands (64 x 64 atoms of the row-major [Bl][ldq] Q')
+        mQtRS[s2] = make_map(q + static_cast<size_t>(1 - s2) * Bl * ldq, ldq, Bl, static_cast<uint64_t>(ldq) * 2, 64, 64);
+        mPart[s2] = make_map(rs_part + static_cast<size_t>(s2) * B * d, d, B, static_cast<uint64_t>(d) * 4, 32, 32,
+                             CU_TENSOR_MAP_DATA_TYPE_FLOAT32);
+      }
+    }
     if (K > 1) setup_peers();
     FC_CUDA(cudaMemset(err, 0, sizeof(int)));
     FC_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&result_h), sizeof(fc::StepResult), cudaHostAllocMapped));
@@ -647,6 +681,7 @@ struct LossStep {
       FC_CUDA(cudaStreamWaitEvent(caller, done, 0));
     }
     if (timing) ev_last = ev_cur, ev_cur = (ev_cur + 1) % ev_slots;
+    book_step();
   }
   int ev_last = 0;
   const void* last_prep_e1 = nullptr;   // arguments of the last enqueued prep kernel (graph capture)
@@ -815,6 +850,10 @@ struct LossStep {
     FC_CUDA(cudaGetLastError());
     FC_CUDA(cudaEventRecord(side_join, ws2));
 
+    if (rs) {   // trainer.cpp:504-518: no weights for anchors of other ranks
+      fc::fc_rs_mask_kernel<<<(B + 255) / 256, 256, 0, st>>>(a);
+      FC_CUDA(cudaGetLastError());
+    }
     if (test_delay_ns > 0) fc::fc_delay_kernel<<<1, 32, 0, st>>>(test_delay_ns);
     // ---- pass 2: Q' tiles (bf16) for both segments ----
     for (int s = 0; s < 2; ++s) {
@@ -879,15 +918,81 @@ struct LossStep {
       map_o2 = out->de2;
     }
     FC_CUDA(fc::launch_gemm(pdl && !timing, gp, mQs, mX, mO, gemm_ctas, st));
+    if (rs) enqueue_rs(out, E1, E2, st);
     mark(6, st);
 
     FC_CUDA(cudaStreamWaitEvent(st, side_join, 0));
+  }
+
+  // openclip_rs: this rank's anchors' contrast cotangents for every row of G (for_e1 = Q'_C^T E2[L],
+  // for_e2 = Q'_R^T E1[L]: with the other anchors' weights zeroed, Q' column j of a non-local j holds
+  // exactly engine.cpp:131-141's terms), minus its own rows (already in dE), reduce-scattered in
+  // fp32 over NCCL, scaled by rs_shard_scale / K (engine.cpp:146-149 on the mean = sum / K).
+  void enqueue_rs(fc_step_out* out, const __nv_bfloat16* E1, const __nv_bfloat16* E2, cudaStream_t st) {
+    const size_t bd = static_cast<size_t>(B) * d, ld = static_cast<size_t>(Bl) * d;
+    FC_CUDA(cudaMemsetAsync(rs_part, 0, 2 * bd * sizeof(float), st));
+    fc::GemmParams gp{};
+    gp.nseg = 2;
+    gp.d = d;
+    gp.n_nb = (d + fc::kGemmN - 1) / fc::kGemmN;
+    gp.kb_total = Bl / fc::kBlockK;
+    gp.scale = 1.0f;
+    for (int s2 = 0; s2 < 2; ++s2) {
+      fc::GemmSeg& g = gp.seg[s2];
+      g.a_mn_major = 1;
+      g.rows = B;
+      g.x_row0 = 0;
+      g.x_krow0 = rank * Bl;
+      g.r = nullptr;
+      g.x = s2 ? E1 : E2;
+      g.out = rs_part + s2 * bd;
+      gp.n_mb[s2] = (B + fc::kPairM - 1) / fc::kPairM;
+    }
+    gp.n_tiles = (gp.n_mb[0] + gp.n_mb[1]) * gp.n_nb;
+    const int ctas = (n_sm / 2) * 2;
+    balance_units(gp, ctas / 2);
+    CUtensorMap mX[2] = {mE2n, mE1n};
+    FC_CUDA(fc::launch_gemm(false, gp, mQtRS, mX, mPart, ctas, st));
+    for (int s2 = 0; s2 < 2; ++s2)   // this rank's own rows: already in dE (local contrast terms)
+      FC_CUDA(cudaMemsetAsync(rs_part + s2 * bd + static_cast<size_t>(rank) * ld, 0, ld * sizeof(float), st));
+    FC_NCCL(ncclGroupStart());
+    for (int s2 = 0; s2 < 2; ++s2)
+      FC_NCCL(ncclReduceScatter(rs_part + s2 * bd, rs_shard + s2 * ld, ld, ncclFloat32, ncclSum, comm, st));
+    FC_NCCL(ncclGroupEnd());
+    const float c = static_cast<float>(1.0 / (static_cast<double>(Bl) * static_cast<double>(B - 1)));
+    fc::fc_axpy2_kernel<<<std::min<long long>(4096, (ld + 255) / 256), 256, 0, st>>>(out->de1, out->de2, rs_shard,
+                                                                                     rs_shard + ld, static_cast<long long>(ld), c);
+    FC_CUDA(cudaGetLastError());
+  }
+
+  // The reference fabric's collectives of one step (trainer.cpp:422-425, 464, 479, 530-533, 572)
+  // with its wire model (fabric.cpp:18-28), and this rank's actual peer bytes.
+  void book_step() {
+    if (K < 2) return;
+    const unsigned long long k = static_cast<unsigned long long>(K), bl = static_cast<unsigned long long>(Bl);
+    const unsigned long long ag = k * (k - 1), dd = static_cast<unsigned long long>(d);
+    const bool mbcl = cfg.variant == FC_OPENCLIP_MBCL;
+    const bool learn = cfg.variant == FC_FASTCLIP_V0 || cfg.variant == FC_FASTCLIP_V3 || mbcl;
+    // E1 / E2 slices, bf16, to K - 1 peers
+    book("feature-gather", 0, 2 * ag * bl * dd, 2 * (k - 1) * bl * dd * 2);
+    if (!rs && !mbcl) book("u-gather", 0, ag * 2 * bl, (k - 1) * 2 * bl * 8);
+    if (!rs && !mbcl && indiv) book("tau-gather", 0, ag * 2 * bl, (k - 1) * 2 * bl * 8);
+    if (learn) book("tau-reduce", 1, 2 * (k - 1), use_peer ? (k - 1) * 3 * static_cast<unsigned long long>(nblk) * 8 : 8);
+    if (rs) book("rs-grad", 2, 2 * ag * bl * dd, 2 * (k - 1) * bl * dd * 4);
+    // what only the per-GPU replicas need: ids, the remaining payload columns, pass-2 parameters
+    const unsigned long long payload = use_peer ? static_cast<unsigned long long>(pstride) * 8 + 8 * bl * 4 + 16
+                                                : static_cast<unsigned long long>(pstride) * 8;
+    unsigned long long used = 0;
+    if (!rs && !mbcl) used += 2 * bl * 8 * (indiv ? 2 : 1);
+    if (learn && use_peer) used += 3 * static_cast<unsigned long long>(nblk) * 8;
+    book("replica-sync", 0, 0, (k - 1) * (payload > used ? payload - used : 0));
   }
 
   int kernels_per_step() const {
     int n = 1 /*prep*/ + 1 /*pass1*/ + 1 /*reduce*/ + (indiv ? 1 : 0) + 1 /*pass2*/ + 1 /*gemm*/;
     n += 1;   // fc_anchor_kernel
     if (K > 1) n += use_peer ? 3 /*two peer gathers + u replica*/ : 1 /*weights*/;
+    if (rs) n += 3;   // weight mask, partial GEMM, axpy (+ NCCL's reduce-scatter kernel)
     return n;
   }
 
@@ -909,7 +1014,7 @@ struct LossStep {
                     (void*)s1, (void*)s2, (void*)tau_state, (void*)e1g, (void*)e2g, (void*)diag, (void*)rowstat,
                     (void*)partial, (void*)col_partial, (void*)clamps, (void*)bounds, (void*)f64, (void*)red, (void*)par, (void*)rcoef,
                     (void*)q, (void*)err, (void*)pflags, (void*)ptickets, (void*)idset,
-                    (void*)step_tag})
+                    (void*)step_tag, (void*)rs_part, (void*)rs_shard})
       if (p) cudaFree(p);
     if (recv && recv != send) cudaFree(recv);
     if (send) cudaFree(send);
@@ -1095,6 +1200,7 @@ int fc_config_defaults(int32_t variant, int64_t n_train, fc_config* out) {
   out->lr_decay_factor = 1.0 / 3.0;
   out->scale_by_tau = (variant == FC_FASTCLIP_V0 || variant == FC_OPENCLIP_MBCL) ? 0 : 1;
   out->world = 1;
+  out->reduction = variant == FC_OPENCLIP_MBCL ? 1 : 0;   // fabric.reduction = auto (trainer.cpp:86-88)
   return FC_OK;
 }
 
@@ -1661,6 +1767,29 @@ int fc_grad_allreduce_mean(void* ctx, double* grad, int64_t n, void* stream) {
     fc_scale_kernel<<<static_cast<int>(g), 256, 0, st>>>(grad, n, 1.0 / static_cast<double>(s->K));
     FC_CUDA(cudaGetLastError());
   });
+}
+
+int fc_comm_ledger(void* ctx, fc_ledger_entry* out, int32_t max) {
+  if (!ctx || (!out && max > 0)) return -FC_ERR_SHAPE;
+  auto* s = static_cast<LossStep*>(ctx);
+  int n = 0;
+  for (const auto& r : s->ledger) {
+    if (n >= max) break;
+    fc_ledger_entry& e = out[n++];
+    std::memset(&e, 0, sizeof(e));
+    std::strncpy(e.phase, r.phase.c_str(), sizeof(e.phase) - 1);
+    e.primitive = r.primitive;
+    e.world = s->K;
+    e.elements = r.elements;
+    e.bytes = r.bytes;
+  }
+  return n;
+}
+
+int fc_comm_ledger_reset(void* ctx) {
+  if (!ctx) return FC_ERR_SHAPE;
+  static_cast<LossStep*>(ctx)->ledger.clear();
+  return FC_OK;
 }
 
 int fc_table_write(void* ctx, const char* path) {

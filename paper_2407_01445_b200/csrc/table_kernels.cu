@@ -145,6 +145,26 @@ __global__ void fc_delay_kernel(long long ns) {
   } while (t - t0 < ns);
 }
 
+// openclip_rs (trainer.cpp:504-518): the anchors of other ranks carry no weights on this rank --
+// zero their pass-2 coefficients (the exponent parameters stay, only coef / fac enter Q').
+__global__ void fc_rs_mask_kernel(StepArgs a) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= a.B || (i >= a.row0 && i < a.row0 + a.Bl)) return;
+  a.coef1[i] = 0.f;
+  a.coef2[i] = 0.f;
+  a.fac1[i] = 0.f;
+  a.fac2[i] = 0.f;
+}
+
+// dE += c * reduce-scattered contrast cotangents (engine.cpp:146-149 with the mean's 1/K folded in)
+__global__ void fc_axpy2_kernel(float* y1, float* y2, const float* x1, const float* x2, long long n, float c) {
+  for (long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    y1[i] = fmaf(c, x1[i], y1[i]);
+    y2[i] = fmaf(c, x2[i], y2[i]);
+  }
+}
+
 // K > 1, after the payload all-gather: thread per anchor of the global batch -> pass-2
 // parameters of every anchor (the local ones were written by fc_anchor_kernel as well) and the
 // u replica update for the other ranks' ids.

@@ -91,6 +91,8 @@ constexpr int kErrShape = 2, kErrOwnership = 5, kErrNumeric = 9;
 __global__ void fc_weights_kernel(StepArgs a);
 __global__ void fc_anchor_kernel(StepArgs a);
 __global__ void fc_delay_kernel(long long ns);
+__global__ void fc_rs_mask_kernel(StepArgs a);
+__global__ void fc_axpy2_kernel(float* y1, float* y2, const float* x1, const float* x2, long long n, float c);
 __global__ void fc_reduce_kernel(StepArgs a);
 __global__ void fc_indiv_update_kernel(StepArgs a);
 __global__ void fc_rows_kernel(const __nv_bfloat16* __restrict__ e1, const __nv_bfloat16* __restrict__ e2, int B,

@@ -51,6 +51,7 @@ class FcConfig(C.Structure):
         ("adam_eps", C.c_double), ("lr_decay_enabled", C.c_int32),
         ("lr_decay_threshold", C.c_double), ("lr_decay_factor", C.c_double),
         ("scale_by_tau", C.c_int32), ("device", C.c_int32), ("nccl_id", C.c_uint8 * 128),
+        ("reduction", C.c_int32),
     ]
 
 
@@ -66,6 +67,11 @@ class FcStepOut(C.Structure):
 class FcStepScalars(C.Structure):
     _fields_ = [("loss", C.c_double), ("gtau", C.c_double), ("tau", C.c_double),
                 ("exp_clamps", C.c_uint64), ("latched", C.c_int32)]
+
+
+class FcLedgerEntry(C.Structure):
+    _fields_ = [("phase", C.c_char * 24), ("primitive", C.c_int32), ("world", C.c_int32),
+                ("elements", C.c_uint64), ("bytes", C.c_uint64)]
 
 
 class FcModelState(C.Structure):
@@ -132,6 +138,8 @@ def lib():
         L.fc_adamw_step.argtypes = [I64, P, P, P, LP, P, D, D, D, D, D, P, P]
         L.fc_lamb_step.argtypes = [I64, P, P, P, LP, P, D, D, D, D, D, I32, LP, LP, I32, P, P]
         L.fc_model_last_error.restype = C.c_char_p
+        L.fc_comm_ledger.argtypes = [P, C.POINTER(FcLedgerEntry), I32]
+        L.fc_comm_ledger_reset.argtypes = [P]
         _lib = L
     return _lib
 
@@ -146,7 +154,7 @@ EXPORTED = [
     "fc_batch_plan_create", "fc_batch_plan_destroy", "fc_batch_plan_iters_per_epoch", "fc_batch_plan_permutation",
     "fc_batch_plan_local", "fc_plan_last_error", "fc_synthetic_embeddings", "fc_synthetic_ids", "fc_synthetic_warm_u",
     "fc_tower_forward", "fc_tower_vjp", "fc_grad_allreduce_mean", "fc_adamw_step", "fc_lamb_step",
-    "fc_model_last_error",
+    "fc_model_last_error", "fc_comm_ledger", "fc_comm_ledger_reset",
 ]
 PHASES = ["allgather_e", "prep", "pass1_stats", "tables_tau", "pass2_q", "grad_gemm"]
 
@@ -325,6 +333,14 @@ class LossStep:
         _check(lib().fc_checkpoint_read(self._h, os.fsencode(path), C.byref(ms)))
         return dict(seed=ms.seed, next_epoch=ms.next_epoch, global_step=ms.global_step,
                     image_shape=list(ms.image_shape), text_shape=list(ms.text_shape), opt_step=ms.opt_step, **arrs)
+
+    def comm_ledger(self) -> dict:
+        """CommLedger of the steps so far: {phase: (primitive, reference wire elements, peer bytes)}."""
+        buf = (FcLedgerEntry * 16)()
+        n = lib().fc_comm_ledger(self._h, buf, 16)
+        if n < 0:
+            raise FastclipError(-n, "comm_ledger")
+        return {buf[i].phase.decode(): (buf[i].primitive, buf[i].elements, buf[i].bytes) for i in range(n)}
 
     def grad_allreduce_mean(self, grad, stream=None):
         """all_reduce_mean "grad-reduce" (trainer.cpp:540-546) of a CUDA fp64 gradient, in place."""

