@@ -113,64 +113,51 @@ def make_inputs(B, d, N, world, rank, n_sets, seed=0):
     return sets
 
 
-def cpu_reference_sample(B, d, N, variant, steps, warmup, log):
-    """The reference's own CPU path (oracle/_ref: engine.cpp, state.cpp, ... compiled from
-    the reference sources) on the box's host cores. The reference parallelises over
-    data-parallel workers (one std::thread each, fabric.cpp:237-258); we run W workers,
-    the largest divisor of B not above nproc. Each worker computes the three full S
-    products of its step (engine.cpp:159,:83,:185) plus its anchors' loops (~0.2-0.3 s per
-    anchor: the cotangent loops walk column-major rows). The per-anchor cost is calibrated
-    once from runs with every worker on 1 and on 65 anchors (the S products' run-to-run noise,
-    ~1 s, spread over 64 anchors); each timed step is a bounded sample (every worker on
-    2 anchors, the three full S products kept) extrapolated to the full slice with that cost.
-    A full B = 5120 step measured directly on 8 host threads took 202 s, ~1.5x the
-    extrapolation (the per-anchor cost grows with the slice: cache misses of the column-major
-    walks), so the reported CPU rate is an upper bound and the speed-up against it conservative."""
+def cpu_reference_step(B, d, N, variant, log, tau=None):
+    """ONE full step of the reference's own CPU path (oracle/_ref_fast: engine.cpp, state.cpp, ...
+    compiled from the reference sources, -O3) on the box's host cores, timed directly. The
+    reference parallelises over data-parallel workers (one std::thread each,
+    fabric.cpp:237-258); we run W workers, the largest divisor of B not above nproc, each with
+    its full anchor slice (every anchor's loops and the three full S products of its step,
+    engine.cpp:159, :83, :185). Nothing is extrapolated: value = 1 / (measured step time)."""
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import oracle as O
     from paper_2407_01445_b200 import synthetic as S
     nproc = os.cpu_count() or 1
     W = max(w for w in range(1, min(nproc, B) + 1) if B % w == 0)
-    Bl = B // W
     b1, b2 = S.embeddings(B, d, 0)
     E1 = S.bf16_to_f32(b1).astype(np.float64)
     E2 = S.bf16_to_f32(b2).astype(np.float64)
     ids = S.ids(B, N, 0)
-    cfg = O.default_config(variant, N)
+    cfg = O.default_config(variant, N, **({"tau_init": tau} if tau is not None else {}))
     st = O.new_state(cfg)
-
-    def run(La):
-        t = time.perf_counter()
-        O.step(cfg, st, W, E1, E2, ids, 0.6, 1e-14, backend="ref_fast", local_limit=La)
-        return time.perf_counter() - t
-
-    La = min(Bl, 65)
-    t1 = run(1)
-    t_big = run(La)
-    per_anchor = max(0.0, (t_big - t1) / max(1, La - 1))
-    fixed = max(0.0, t1 - per_anchor)
-    est = []
-    for i in range(warmup + steps):
-        ts = run(2)
-        if i >= warmup:
-            est.append(ts + (Bl - 2) * per_anchor)
-    t_step = float(np.mean(est)) if est else fixed + Bl * per_anchor
-    sample = (f"reference TUs (oracle/_ref) step at B={B}, d={d} as {W} fabric workers x {Bl} anchors; "
-              f"per-anchor cost {per_anchor * 1e3:.0f}ms from runs with every worker on 1 and {La} anchors; each "
-              f"timed step restricts every worker to 2 anchors (3 full S products kept), extrapolated to {Bl}")
-    log(f"[cpu] W={W} t(La=1)={t1:.2f}s t(La={La})={t_big:.2f}s -> est step {t_step:.1f}s")
+    t = time.perf_counter()
+    O.step(cfg, st, W, E1, E2, ids, 0.6, 1e-14, backend="ref_fast")
+    t_step = time.perf_counter() - t
+    cpu_model = ""
+    try:
+        with open("/proc/cpuinfo") as f:
+            cpu_model = next((ln.split(":", 1)[1].strip() for ln in f if ln.startswith("model name")), "")
+    except OSError:
+        pass
+    sample = (f"one full reference step (oracle/_ref TUs, -O3) at B={B}, d={d}, N={N} as {W} fabric workers x "
+              f"{B // W} anchors on {nproc} host threads ({cpu_model}); timed directly, not extrapolated")
+    log(f"[cpu] W={W} full step {t_step:.1f}s")
     return {"value": 1.0 / t_step, "unit": UNIT, "cores": W, "kind": "reference", "sample": sample,
-            "est_step_s": t_step, "fixed_s": fixed, "per_anchor_s": per_anchor}
+            "step_s": t_step}
 
 
 def reference_arm(args):
     world, rank, _ = dist_env()
     if rank != 0:
         return 0
-    cb = cpu_reference_sample(args.batch, args.dim, args.n_train, args.variant, args.steps, args.warmup,
-                              lambda m: print(m, file=sys.stderr))
+    cb = cpu_reference_step(args.batch, args.dim, args.n_train, args.variant, lambda m: print(m, file=sys.stderr),
+                            tau=args.tau)
+    # one full step is the unit of work and it takes tens of seconds on the host: the line reports
+    # the ONE step actually timed (steps_requested / warmup_requested are the driver's K / W)
     line = {"metric": METRIC, "value": cb["value"], "unit": UNIT, "impl": "reference", "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 / cb["value"],
+            "steps": 1, "warmup": 0, "steps_requested": args.steps, "warmup_requested": args.warmup,
+            "ms_per_step": 1e3 / cb["value"],
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "config": workload_config(args, world),
             "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
@@ -184,7 +171,8 @@ def ncu_traffic(phase):
     newest committed ncu --set full summary (profiles/<round>_traffic.json); None if absent."""
     import glob
     kern = {"pass1_stats": ("sim_tile_kernel<3>", "sim_tile_kernel<0>"), "pass2_q": ("sim_tile_kernel<1>",),
-            "grad_gemm": ("grad_gemm_kernel<1>", "grad_gemm_kernel<2>")}.get(phase, ())
+            "grad_gemm": ("grad_gemm_kernel", "grad_gemm_kernel<1>"),
+            "tables_tau": ("fc_anchor_kernel",)}.get(phase, ())
     files = sorted(glob.glob(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "*_traffic.json")))
     if not files:
         return None
@@ -205,7 +193,8 @@ def workload_config(args, world):
             "dim": args.dim, "n_train": args.n_train, "world": world,
             "parallelism": f"dp{world} (anchor slices; NVLink peer all-gathers of E and the scalar payload)" if world > 1
                            else "dp1",
-            "l2": "flushed between timed steps (256 MiB memset)", "tables": "warm u (log10 u ~ U[-8,0])"}
+            "l2": "flushed between timed steps (256 MiB memset)", "tables": "warm u (log10 u ~ U[-8,0])",
+            **({"tau_init": args.tau} if getattr(args, "tau", None) is not None else {})}
 
 
 def main():
@@ -220,6 +209,7 @@ def main():
     ap.add_argument("--n-train", type=int, default=2_700_000)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--tau", type=float, default=None, help="temperature.init (default: the variant's)")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
     if args.impl == "reference":
@@ -242,6 +232,8 @@ def main():
     Bl = B // world
 
     cfg = P.config_defaults(args.variant, N, dim=d, local_batch=Bl, world=world, rank=rank, device=local)
+    if args.tau is not None:
+        cfg.tau_init = args.tau
     if world > 1:
         obj = [P.nccl_unique_id() if rank == 0 else None]
         tdist.broadcast_object_list(obj, src=0)
@@ -336,21 +328,28 @@ def main():
         staging = [(torch.empty(Bl, d, device=dev, dtype=torch.bfloat16),
                     torch.empty(Bl, d, device=dev, dtype=torch.bfloat16),
                     torch.empty(Bl, device=dev, dtype=torch.int32)) for _ in range(2)]
+        outs = [(torch.empty(Bl, d, device=dev, dtype=torch.float32),
+                 torch.empty(Bl, d, device=dev, dtype=torch.float32)) for _ in range(2)]
+        host_out = [(torch.empty(Bl, d, dtype=torch.float32).pin_memory(),
+                     torch.empty(Bl, d, dtype=torch.float32).pin_memory()) for _ in range(2)]
         h2d = 2 * Bl * d * 2 + Bl * 4
-        d2h = 48
+        d2h = 2 * Bl * d * 4 + 48   # dE1, dE2 (fp32) + the step scalars
         # pipelined feed: a copy stream uploads step i+1's inputs (pinned -> double-buffered
-        # device staging) while step i computes; every step still pays its own H2D copy and a
-        # device -> host read of its result (loss / G_tau / tau, mapped pinned memory)
+        # device staging) and downloads step i-1's dE1 / dE2 (double-buffered outputs -> pinned
+        # host) while step i computes; every step pays its own H2D copy of E1 / E2 / ids and the
+        # D2H read of its gradients and scalars (loss / G_tau / tau, mapped pinned memory)
         cstream = torch.cuda.Stream(dev)
         copied = [torch.cuda.Event() for _ in range(2)]
         consumed = [torch.cuda.Event() for _ in range(2)]
-        for ev in consumed:
+        computed = [torch.cuda.Event() for _ in range(2)]
+        drained = [torch.cuda.Event() for _ in range(2)]
+        for ev in consumed + drained:
             ev.record(stream)
-        for i in range(3):   # warm the two staging graphs
+        for i in range(3):   # warm the staging / output graphs
             db = staging[i % 2]
             for dst, src in zip(db, pinned[i % n_sets]):
                 dst.copy_(src)
-            step.step(db[0], db[1], db[2], gamma, eps, de1, de2, stream)
+            step.step(db[0], db[1], db[2], gamma, eps, outs[i % 2][0], outs[i % 2][1], stream)
         barrier()
         torch.cuda.synchronize()
         e_start = torch.cuda.Event(enable_timing=True)
@@ -366,10 +365,16 @@ def main():
                     dst.copy_(src, non_blocking=True)
                 copied[b].record(cstream)
             stream.wait_event(copied[b])
-            # the step writes its 48-byte result (loss, G_tau, tau, clamps) into mapped pinned
-            # host memory (the per-step device -> host transfer); read back after the last step
-            step.step(db[0], db[1], db[2], gamma, eps, de1, de2, stream)
+            stream.wait_event(drained[b])                # step i-2's gradients are on the host
+            step.step(db[0], db[1], db[2], gamma, eps, outs[b][0], outs[b][1], stream)
             consumed[b].record(stream)
+            computed[b].record(stream)
+            with torch.cuda.stream(cstream):
+                cstream.wait_event(computed[b])
+                host_out[b][0].copy_(outs[b][0], non_blocking=True)
+                host_out[b][1].copy_(outs[b][1], non_blocking=True)
+                drained[b].record(cstream)
+        stream.wait_stream(cstream)
         e_end.record(stream)
         _ = step.scalars()
         torch.cuda.synchronize()
@@ -397,7 +402,10 @@ def main():
     # S (2 B^2 d at K=1, 4 Bl B d at K>1) is credited half to each similarity pass.
     s_share = (1.0 * B * B * d) if world == 1 else 2.0 * Bd
     per_kernel_flops = {"pass1_stats": s_share, "pass2_q": s_share, "grad_gemm": 4.0 * Bd}
-    exec_flops = {"pass1_stats": 4.0 * Bd, "pass2_q": (2.0 if world == 1 else 4.0) * Bd, "grad_gemm": 4.0 * Bd}
+    # executed: the K = 1 pass 1 multiplies S once (row and column statistics from one tile), K > 1
+    # runs both segments; pass 2 recomputes S (K = 1: once, Q^T shared) / both segments
+    exec_flops = {"pass1_stats": (2.0 if world == 1 else 4.0) * Bd, "pass2_q": (2.0 if world == 1 else 4.0) * Bd,
+                  "grad_gemm": 4.0 * Bd}
     tensor_phases = ["pass1_stats", "pass2_q", "grad_gemm"]
     dom = max(tensor_phases, key=lambda k: phases[k])
     t_dom = phases[dom] * 1e-3
@@ -407,6 +415,18 @@ def main():
                 "traffic_source": ncu_traffic(dom), "peak_kind": f"{peak_kind} bf16 burst",
                 "executed_tflops": exec_flops[dom] / t_dom / 1e12 if t_dom > 0 else 0.0,
                 "algorithmic_flops_per_launch": per_kernel_flops[dom]}
+    # the table kernel (K2: fc_anchor_kernel, the "tables_tau" phase): SURVEY.md §8(d) algorithmic
+    # bytes per id -- 4 B id + 16 B u read + 16 B u write, +128 B for the v2 tau / Adam state --
+    # over its measured duration, against the HBM peak; it is latency-bound (one dependent fp64
+    # chain per anchor), which the fraction makes explicit
+    indiv = args.variant in ("fastclip_v2", "isogclr")
+    k2_bytes = float(Bl) * (36.0 + (128.0 if indiv else 0.0))
+    t_k2 = phases.get("tables_tau", 0.0) * 1e-3
+    k2 = {"kernel": "fc_anchor_kernel", "bound": "hbm", "algorithmic_bytes": k2_bytes,
+          "achieved": k2_bytes / t_k2 / 1e9 if t_k2 > 0 else 0.0, "peak": hbm, "unit": "GB/s",
+          "frac": (k2_bytes / t_k2 / 1e9) / hbm if t_k2 > 0 else 0.0,
+          "traffic": (ncu_traffic("tables_tau") or {}).get("bytes"),
+          "note": "latency-bound: one fp64 dependent chain per anchor (partials -> g -> EMA -> weights -> logs)"}
     step_ach = step_flops / (ms_per_step * 1e-3) / 1e12
     step_roofline = {"achieved": step_ach, "peak": peak, "unit": "TFLOP/s", "frac": step_ach / peak,
                      "frac_of_sustained": step_ach / peak_sus, "algorithmic_flops_per_step": step_flops}
@@ -414,7 +434,7 @@ def main():
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
         try:
-            cb = cpu_reference_sample(B, d, N, args.variant, 1, 0, lambda m: print(m, file=sys.stderr))
+            cb = cpu_reference_step(B, d, N, args.variant, lambda m: print(m, file=sys.stderr))
             cpu = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
         except Exception as ex:  # the checker is absent on this box
             cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "reference", "sample": f"unavailable: {ex}"}
@@ -424,7 +444,7 @@ def main():
             "scaling": "strong", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
             "config": workload_config(args, world), "e2e": e2e,
             "gpu_launches": step.kernels_per_step * args.steps,
-            "roofline": roofline, "step_roofline": step_roofline,
+            "roofline": roofline, "step_roofline": step_roofline, "table_kernel": k2,
             "phases_ms": phases, "clocks": clk, "cpu_baseline": cpu,
             "last_step": {"loss": sc.loss, "gtau": sc.gtau, "tau": sc.tau, "exp_clamps": sc.exp_clamps}}
     print(json.dumps(line), flush=True)

@@ -237,6 +237,37 @@ __device__ __forceinline__ void fused_fast16(const uint32_t (&r)[16], float kap,
   transpose_reduce2_16(x, zx, lane, cx, czx);
 }
 
+// FUSED clamp-free two-exponential path (no clamp possible in the chunk, no diagonal / ragged
+// element, but outside the one-exponential form: a temperature per anchor (v2 / iSogCLR) or
+// kappa |s| > 63 (tau below ~0.023)): e_row = 2^(s kappa_i + beta_i) and e_col = 2^(s kappa_j +
+// beta_j) per element, the column anchors' {kappa_j, beta_j} broadcast from the lanes holding them
+// (one shuffle per column and warp, not per element). Row sums {sum e, sum y e} accumulate per
+// thread; the column sums go through the same register transposes as the one-exponential path.
+template <bool kOneKappa>
+__device__ __forceinline__ void fused_2e16(const uint32_t (&r)[16], float2 rs, float2 cs, int c0, uint32_t lane,
+                                           float2& re, float2& rye, float& ce, float& cye) {
+  const float2 rk2 = f2(rs.x, rs.x), rb2 = f2(rs.y, rs.y);
+  float x[16], zx[16];
+#pragma unroll
+  for (int k = 0; k < 16; k += 2) {
+    const float2 s = f2(__uint_as_float(r[k]), __uint_as_float(r[k + 1]));
+    const float2 yr = __ffma2_rn(s, rk2, rb2);
+    const float b0 = __shfl_sync(0xffffffffu, cs.y, c0 + k), b1 = __shfl_sync(0xffffffffu, cs.y, c0 + k + 1);
+    float2 kc = rk2;
+    if constexpr (!kOneKappa)
+      kc = f2(__shfl_sync(0xffffffffu, cs.x, c0 + k), __shfl_sync(0xffffffffu, cs.x, c0 + k + 1));
+    const float2 yc = __ffma2_rn(s, kc, f2(b0, b1));
+    const float2 er = f2(ex2_approx(yr.x), ex2_approx(yr.y));
+    const float2 ec = f2(ex2_approx(yc.x), ex2_approx(yc.y));
+    re = __fadd2_rn(re, er);
+    rye = __ffma2_rn(yr, er, rye);
+    const float2 ze = __fmul2_rn(yc, ec);
+    x[k] = ec.x; x[k + 1] = ec.y;
+    zx[k] = ze.x; zx[k + 1] = ze.y;
+  }
+  transpose_reduce2_16(x, zx, lane, ce, cye);
+}
+
 // FUSED exact path for one 8-column piece (rare: diagonal / ragged / clamp-capable chunks):
 // both exponentials with the safe_exp clamp, masks and clamp counts; the lanes of quarter q of
 // the warp get their column's exact {sum e, sum y e}.
@@ -748,19 +779,67 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(SimCfg<kMode>::kThre
             ce = lane < 16 ? c0x : c1x;
             cye = lane < 16 ? c0zx : c1zx;
           } else {
+            // per 16-column half: exact bounds from the tile values themselves (the norm bound
+            // smax is loose at small tau / for per-anchor temperatures): the row maxima and the
+            // half's maximum / maximum |s| decide whether any exponent can reach the clamp and
+            // whether the one-exponential form's range (kappa |s| <= 63, |beta| <= 63) holds
 #pragma unroll 1
             for (int hh = 0; hh < 2; ++hh) {
               uint32_t r16[16];
               tmem_ld_32x32b_x16(taddr + 32 * h + 16 * hh, r16);
               tmem_ld_wait();
               if (hh == 1 && h == chunks_w - 1) release_tmem();
+              int mode = 0;   // 0: masked exact path, 1: one exponential, 2: two exponentials
+              if (interior && warp_rows_ok) {
+                float mx = __uint_as_float(r16[0]), am = fabsf(mx);
 #pragma unroll
-              for (int q = 0; q < 2; ++q) {
-                uint32_t r8[8];
+                for (int k = 1; k < 16; ++k) {
+                  const float v = __uint_as_float(r16[k]);
+                  mx = fmaxf(mx, v);
+                  am = fmaxf(am, fabsf(v));
+                }
+                float M = mx, A = am;
 #pragma unroll
-                for (int k = 0; k < 8; ++k) r8[k] = r16[8 * q + k];
-                fused_masked(r8, rstat, sg.col_stat, col0 + 16 * hh + 8 * q, sg.cols, gi, row_ok, lane, 2 * hh + q, se,
-                             sye, ncl, ce, cye);
+                for (int o = 16; o > 0; o >>= 1) {
+                  M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
+                  A = fmaxf(A, __shfl_xor_sync(0xffffffffu, A, o));
+                }
+                const bool col_in = (lane >> 4) == static_cast<uint32_t>(hh);   // lanes of this half's columns
+                if (__all_sync(0xffffffffu, fmaf(mx, rstat.x, rstat.y) <= kClampLog2 &&
+                                                (!col_in || fmaf(M, cst.x, cst.y) <= kClampLog2))) {
+                  const bool one = p.fuse_fast && __all_sync(0xffffffffu, rstat.x * A <= kFactMaxLog2 &&
+                                                                            fabsf(rstat.y) <= kFactMaxLog2 &&
+                                                                            (!col_in || fabsf(cst.y) <= kFactMaxLog2));
+                  mode = one ? 1 : 2;
+                }
+              }
+              if (mode == 0) {
+#pragma unroll
+                for (int q = 0; q < 2; ++q) {
+                  uint32_t r8[8];
+#pragma unroll
+                  for (int k = 0; k < 8; ++k) r8[k] = r16[8 * q + k];
+                  fused_masked(r8, rstat, sg.col_stat, col0 + 16 * hh + 8 * q, sg.cols, gi, row_ok, lane, 2 * hh + q,
+                               se, sye, ncl, ce, cye);
+                }
+                continue;
+              }
+              float cx, cy;
+              if (mode == 1) {   // raw {sum x, sum z x} -> {sum e, sum y e} with 2^beta_j of the lane's column
+                fused_fast16(r16, rstat.x, se2, sye2, lane, cx, cy);
+                const float sc = ex2_approx(cst.y);
+                cy = sc * fmaf(cst.y, cx, cy);
+                cx = sc * cx;
+              } else {
+                float2 re = f2(0.f, 0.f), rye = f2(0.f, 0.f);
+                if (p.fuse_fast) fused_2e16<true>(r16, rstat, cst, 16 * hh, lane, re, rye, cx, cy);
+                else fused_2e16<false>(r16, rstat, cst, 16 * hh, lane, re, rye, cx, cy);
+                se += re.x + re.y;   // already {sum e, sum y e}
+                sye += rye.x + rye.y;
+              }
+              if ((lane >> 4) == static_cast<uint32_t>(hh)) {
+                ce = cx;
+                cye = cy;
               }
             }
           }
@@ -785,9 +864,33 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(SimCfg<kMode>::kThre
         } else {  // kSimQ
           uint32_t packed[16];
           const float* kc = par + 32 * h;
-          if (interior && row_safe && q_col_safe && q_fact)
+          bool safe = interior && row_safe && q_col_safe;
+          bool fact = safe && q_fact;
+          if (interior && !fact) {
+            // exact bounds from this chunk's values (the norm bounds are loose at small tau): no
+            // exponent reaches the clamp, and the one-exponential range holds (kappa |s| <= 63,
+            // |beta| <= 63 for the row and the 32 column anchors; column lane's parameters)
+            float mx = __uint_as_float(rr[0]), am = fabsf(mx);
+#pragma unroll
+            for (int k = 1; k < 32; ++k) {
+              const float v = __uint_as_float(rr[k]);
+              mx = fmaxf(mx, v);
+              am = fmaxf(am, fabsf(v));
+            }
+            float M = mx, A = am;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+              M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
+              A = fmaxf(A, __shfl_xor_sync(0xffffffffu, A, o));
+            }
+            const float kj = kc[lane], bj = kc[kPairN + lane];
+            safe = __all_sync(0xffffffffu, fmaf(mx, rk, rbeta) <= kClampLog2 && fmaf(M, kj, bj) <= kClampLog2);
+            fact = safe && p.q_factor &&
+                   __all_sync(0xffffffffu, rk * A <= kFactMaxLog2 && fabsf(rbeta) <= kFactMaxLog2 && fabsf(bj) <= kFactMaxLog2);
+          }
+          if (fact)
             q_chunk_fact(rr, rk, rf, kc + 3 * kPairN, packed);
-          else if (interior && row_safe && q_col_safe)
+          else if (safe)
             q_chunk<false>(rr, rk, rbeta, rc, kc, kc + kPairN, kc + 2 * kPairN, col0, sg.cols, gi, packed);
           else
             q_chunk<true>(rr, rk, rbeta, rc, kc, kc + kPairN, kc + 2 * kPairN, col0, sg.cols, gi, packed);
