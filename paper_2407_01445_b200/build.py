@@ -53,6 +53,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
         obj = os.path.join(LIBDIR, os.path.basename(src) + ".o")
         cmd = [nvcc, *ARCH, "-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-I", inc,
                "-c", src, "-o", obj]
+        if os.environ.get("FC_PROFILE") == "1":   # profiling build: globaltimer / cycle stamps compiled in
+            cmd.insert(1, "-DFC_PROFILE")
         if verbose:
             cmd.insert(1, "-Xptxas=-v")
         procs.append((subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT), src))

@@ -205,7 +205,7 @@ __device__ __forceinline__ void anchor_work(const StepArgs& a, int r, int sub, d
   const float s_ii = a.diag[a.row0 + rr];
   double s1, x1, s2, x2;
   reduce_partials(a, rr, valid, sub, s1, x1, s2, x2);
-  if (a.dbg && threadIdx.x == 0) {   // debug timeline: partials reduced
+  if (kProfStamps && a.dbg && threadIdx.x == 0) {   // debug timeline: partials reduced
     long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     a.dbg[blockIdx.x * 8 + 2] = t;

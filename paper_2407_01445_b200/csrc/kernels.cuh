@@ -8,6 +8,14 @@
 
 namespace fc {
 
+// globaltimer / cycle stamps of the profiling builds (FC_PROFILE=1 python -m paper_2407_01445_b200.build);
+// the shipped library compiles every stamp out
+#ifdef FC_PROFILE
+constexpr bool kProfStamps = true;
+#else
+constexpr bool kProfStamps = false;
+#endif
+
 // ---- tiling shared by the two tcgen05 kernels (CTA pair = cluster of 2, cta_group::2) ----
 constexpr int kPairM = 256;      // rows per pair tile (128 per CTA)
 constexpr int kCtaM = 128;       // TMEM lanes / rows per CTA
@@ -96,8 +104,7 @@ struct SimParams {
   int idset_mask;                      // slots - 1 (power of two >= 2 n_ids)
   const unsigned long long* step_tag;
   int* err;
-  int debug;                   // perf experiments: 1 = skip epilogue math, 2 = also skip B loads
-  long long* dbg_out;          // debug == 9: per-pair MMA-warp cycle counters [pair][8]
+  long long* dbg_out;          // FC_PROFILE builds: per-pair MMA-warp / epilogue counters, per-CTA stamps
 };
 
 // ---- weighted-gradient GEMM: out = scale * (Q' X - r o X_local) ----
@@ -144,7 +151,7 @@ struct PeerGather {
   unsigned long long* my_flag;        // local flag array [world]
   unsigned* ticket;                   // local grid-completion ticket
   int* err;
-  long long* dbg;                     // debug: globaltimer stamps {entry, stores done, flags out, peers in}
+  long long* dbg;                     // FC_PROFILE builds: globaltimer stamps {entry, stores done, flags out, peers in}
   int early_trigger;                  // release the next (programmatic) kernel at entry: it only
                                       // reads the gathered data after griddepcontrol.wait
   int wait_src;                       // programmatic launch: sources >= wait_src are written by the
@@ -164,8 +171,6 @@ enum SimMode { kSimStats = 0, kSimQ = 1, kSimRaw = 2, kSimFused = 3 };
 cudaError_t launch_sim(int mode, const SimParams& p, const CUtensorMap* mapA, const CUtensorMap* mapB,
                        const CUtensorMap* mapQout, int grid, cudaStream_t s, float* raw_out, bool pdl = false);
 cudaError_t sim_set_smem();
-cudaError_t launch_ring_probe(int n_pairs, int n_kb, int tile_kb, int epi, long long* cycles, cudaStream_t s);
-cudaError_t launch_mma_probe(int n_pairs, int n_mma, int commit_every, long long* cycles, cudaStream_t s);
 cudaError_t gemm_set_smem();
 cudaError_t launch_gemm(bool pdl, const GemmParams& p, const CUtensorMap* mapQ, const CUtensorMap* mapX,
                         const CUtensorMap* mapOut, int grid, cudaStream_t s);

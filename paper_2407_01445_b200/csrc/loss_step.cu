@@ -202,13 +202,13 @@ struct LossStep {
   double* scal = nullptr;        // device {gamma_t, eps_t}
   bool use_graph = true;
   bool shared_q = true;          // K == 1: one Q pass, Q^T read by the dE2 GEMM
-  int sim_debug = 0, gemm_debug = 0;
+  bool prof = false;               // FC_PROFILE builds with FC_PROF=1: stamps into dbg_buf (fc_debug_counters)
   bool q_factor = true;          // FC_Q_FACTOR=0 forces the two-exponential Q path (A/B checks)
   bool fused_p1 = false;         // K == 1: row + column statistics from one S pass (FC_FUSED_P1=0: two passes)
   bool pdl = true;               // programmatic dependent launch between the step's kernels (FC_PDL=0: off)
   bool split_tail = false;       // similarity kernels: leftover tiles as half tiles (FC_SPLIT_TAIL=1; measured neutral)
   int gemm_drain = 0;            // FC_GEMM_DRAIN: stream-K unit-boundary cost in k-blocks (0: KB / 10)
-  long long* dbg_buf = nullptr;   // FC_SIM_DEBUG=9 MMA-warp counters: [launch 0: pass 1, 1: pass 2][pair][8]             // FC_SIM_DEBUG perf experiments (results invalid when set)
+  long long* dbg_buf = nullptr;   // profiling stamps: [launch 0: pass 1, 1: pass 2][pair][8], GEMM, anchor, prep, gathers
   struct GraphEntry {
     const void* key[6];
     cudaGraphExec_t exec;
@@ -360,16 +360,17 @@ struct LossStep {
     if (const char* e = std::getenv("FC_GRAPH")) use_graph = atoi(e) != 0;
     shared_q = K == 1;
     if (const char* e = std::getenv("FC_DEBUG_SYNC")) debug_sync = atoi(e) != 0;
-    if (const char* e = std::getenv("FC_SIM_DEBUG")) sim_debug = atoi(e);
+#ifdef FC_PROFILE
+    if (const char* e = std::getenv("FC_PROF")) prof = atoi(e) != 0;
+#endif
     if (const char* e = std::getenv("FC_Q_FACTOR")) q_factor = atoi(e) != 0;
     fused_p1 = K == 1;
     if (const char* e = std::getenv("FC_PDL")) pdl = atoi(e) != 0;
     if (const char* e = std::getenv("FC_SPLIT_TAIL")) split_tail = atoi(e) != 0;
     if (const char* e = std::getenv("FC_GEMM_DRAIN")) gemm_drain = atoi(e);
     if (const char* e = std::getenv("FC_FUSED_P1")) fused_p1 = fused_p1 && atoi(e) != 0;
-    if (const char* e = std::getenv("FC_GEMM_DEBUG")) gemm_debug = atoi(e);
-    if (sim_debug == 9 || gemm_debug >= 9) dbg_buf = dalloc<long long>(2 * 2688 + 160 * 16 + 8192);
-    if (dbg_buf && use_peer) {   // FC_SIM_DEBUG=9: gather stamps after the anchor / prep stamps
+    if (prof) dbg_buf = dalloc<long long>(2 * 2688 + 160 * 16 + 8192);
+    if (dbg_buf && use_peer) {   // gather stamps after the anchor / prep stamps
       for (int q2 = 0; q2 < 2; ++q2) {
         pg_e[q2].dbg = dbg_buf + 2 * 2688 + 160 * 16 + 6000;
         pg_p[q2].dbg = pg_e[q2].dbg + 4;
@@ -701,7 +702,7 @@ struct LossStep {
     a.ids = in->ids;
     a.gscale = static_cast<float>(1.0 / (static_cast<double>(Bl) * static_cast<double>(B - 1)));
     a.scal = scal;
-    if (sim_debug == 9) a.dbg = dbg_buf + 2 * 2688 + 160 * 16;
+    if (prof) a.dbg = dbg_buf + 2 * 2688 + 160 * 16;
     // prep: with peer memory every rank preps only its own anchors, BEFORE the gather (the
     // diagonal and tau^t of non-local anchors are never needed: their pass-2 parameters arrive
     // ready-made); its norm maxima sit in this rank's bounds slot, which the gather copies
@@ -773,9 +774,8 @@ struct LossStep {
     sp.zero0 = reinterpret_cast<float4*>(out->de1);   // the GEMM's reduce-add targets
     sp.zero1 = reinterpret_cast<float4*>(out->de2);
     sp.zero_n4 = static_cast<long long>(Bl) * d / 4;
-    sp.debug = sim_debug;
     sp.split_tail = split_tail ? 1 : 0;
-    if (sim_debug == 9) sp.dbg_out = dbg_buf;
+    if (prof) sp.dbg_out = dbg_buf;
     CUtensorMap mA[2] = {mE1k, mE2k}, mB[2] = {mE2k, mE1k};
     mark(2, st);
     if (fused_p1) {
@@ -802,7 +802,7 @@ struct LossStep {
     mark(3, st);
     // table update + weights + local G_tau / loss terms + payload, one lane group per anchor
     a.n_blockpart = nblk;
-    if (sim_debug == 9) a.dbg = dbg_buf + 2 * 2688 + 160 * 16;
+    if (prof) a.dbg = dbg_buf + 2 * 2688 + 160 * 16;
     {
       cudaLaunchConfig_t cfg{};
       cudaLaunchAttribute attr[1];
@@ -877,7 +877,7 @@ struct LossStep {
       sp.n_rb[1] = 0;
       sp.n_items = sp.n_rb[0] * n_jt;
     }
-    if (sim_debug == 9) sp.dbg_out = dbg_buf + 2688;
+    if (prof) sp.dbg_out = dbg_buf + 2688;
     sp.q_factor = (!indiv && q_factor) ? 1 : 0;   // one shared temperature: single-exponential Q
     FC_CUDA(fc::launch_sim(fc::kSimQ, sp, mA, mB, mQo, pair_grid(sp.n_items), st, nullptr, pdl && !timing));
 
@@ -891,7 +891,7 @@ struct LossStep {
     gp.scale = static_cast<float>(1.0 / (static_cast<double>(Bl) * static_cast<double>(B - 1)));
     gp.reset_at_exit = bnd;   // this parity's slots: the next writer is step t+2 (see e1g)
     gp.n_reset = K;
-    if (gemm_debug >= 9) gp.dbg_out = dbg_buf + 2 * 2688;
+    if (prof) gp.dbg_out = dbg_buf + 2 * 2688;
     for (int s = 0; s < 2; ++s) {
       fc::GemmSeg& g = gp.seg[s];
       g.a_mn_major = (shared_q && s == 1) ? 1 : 0;
@@ -1162,19 +1162,6 @@ constexpr uint32_t kFck1Magic = 0x46434b31;   // "FCK1" (checkpoint.cpp:9)
 extern "C" {
 
 const char* fc_last_error(void) { return g_last_error.c_str(); }
-
-int fc_debug_ring_probe(int32_t n_pairs, int32_t n_kb, int32_t tile_kb, int32_t epi, long long* cycles_dev,
-                        void* stream) {
-  return guarded([&] {
-    FC_CUDA(fc::launch_ring_probe(n_pairs, n_kb, tile_kb, epi, cycles_dev, static_cast<cudaStream_t>(stream)));
-  });
-}
-
-int fc_debug_mma_probe(int32_t n_pairs, int32_t n_mma, int32_t commit_every, long long* cycles_dev, void* stream) {
-  return guarded([&] {
-    FC_CUDA(fc::launch_mma_probe(n_pairs, n_mma, commit_every, cycles_dev, static_cast<cudaStream_t>(stream)));
-  });
-}
 
 int fc_config_defaults(int32_t variant, int64_t n_train, fc_config* out) {
   if (!out) return FC_ERR_SHAPE;

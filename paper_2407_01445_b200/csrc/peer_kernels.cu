@@ -46,7 +46,7 @@ __device__ __forceinline__ long long gtimer() {
 constexpr int kErrCollectiveAborted = 8;   // FC_ERR_COLLECTIVE_ABORTED (CollectiveAborted, errors.hpp)
 
 __global__ void __launch_bounds__(256) peer_gather_kernel(PeerGather g) {
-  if (g.dbg && blockIdx.x == 0 && threadIdx.x == 0) g.dbg[0] = gtimer();
+  if (kProfStamps && g.dbg && blockIdx.x == 0 && threadIdx.x == 0) g.dbg[0] = gtimer();
   if (g.early_trigger) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   // ---- this rank's slices -> every rank's destination (row offset rank * bytes) ----
   const size_t stride = static_cast<size_t>(gridDim.x) * blockDim.x;
@@ -84,13 +84,13 @@ __global__ void __launch_bounds__(256) peer_gather_kernel(PeerGather g) {
   __syncthreads();
   if (!last || threadIdx.x != 0) return;
   *g.ticket = 0u;             // re-arm for the next gather (stream order)
-  if (g.dbg) g.dbg[1] = gtimer();
+  if (kProfStamps && g.dbg) g.dbg[1] = gtimer();
   // one release fence orders every CTA's stores (acquired through the ticket) before all the
   // flag stores, which then go out back to back (a release per store would serialise them
   // behind one NVLink round trip each)
   fence_acq_rel_sys();
   for (int k = 0; k < g.world; ++k) st_relaxed_sys(g.peer_flag[k] + g.rank, g.seq);
-  if (g.dbg) g.dbg[2] = gtimer();
+  if (kProfStamps && g.dbg) g.dbg[2] = gtimer();
   // wait for every rank's slice. A peer that stopped stepping is detected after timeout_ns: this
   // rank then poisons every rank (fabric.cpp:228-235); a poisoned rank stops waiting at once.
   const long long t0 = gtimer();
@@ -109,7 +109,7 @@ __global__ void __launch_bounds__(256) peer_gather_kernel(PeerGather g) {
     }
   }
   fence_acq_rel_sys();        // acquire: the peers' slices are read only after their flags
-  if (g.dbg) g.dbg[3] = gtimer();
+  if (kProfStamps && g.dbg) g.dbg[3] = gtimer();
 }
 
 cudaError_t launch_peer_gather(const PeerGather& g, int blocks, int threads, cudaStream_t s, bool pdl) {

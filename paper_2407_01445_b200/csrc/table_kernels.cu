@@ -35,7 +35,7 @@ __global__ void fc_prep_kernel(const __nv_bfloat16* __restrict__ e1, const __nv_
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const int w = (blockIdx.x * blockDim.x + threadIdx.x) / 32;
   const int lane = threadIdx.x & 31;
-  if (a.dbg && threadIdx.x == 0) {   // debug timeline: first entry / last exit of the grid
+  if (kProfStamps && a.dbg && threadIdx.x == 0) {   // debug timeline: first entry / last exit of the grid
     long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     atomicMin(reinterpret_cast<unsigned long long*>(a.dbg + 8 * 640), static_cast<unsigned long long>(t));
@@ -126,7 +126,7 @@ __global__ void fc_prep_kernel(const __nv_bfloat16* __restrict__ e1, const __nv_
   const float k1 = static_cast<float>(kLog2eD / t1), k2 = static_cast<float>(kLog2eD / t2);
   a.rowstat_R[r] = make_float2(k1, -acc * k1);   // y = s * kappa + beta (log2-domain exponent)
   a.rowstat_C[r] = make_float2(k2, -acc * k2);
-  if (a.dbg) {
+  if (kProfStamps && a.dbg) {
     long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     atomicMax(reinterpret_cast<unsigned long long*>(a.dbg + 8 * 640 + 1), static_cast<unsigned long long>(t));
@@ -213,18 +213,18 @@ __device__ __forceinline__ long long gtime() {
 }
 
 __global__ void __launch_bounds__(128) fc_anchor_kernel(StepArgs a) {
-  long long t_entry = a.dbg ? gtime() : 0;
+  long long t_entry = (kProfStamps && a.dbg) ? gtime() : 0;
   asm volatile("griddepcontrol.wait;" ::: "memory");   // pass-1 partials (programmatic launch)
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-  long long t_wait = a.dbg ? gtime() : 0;
+  long long t_wait = (kProfStamps && a.dbg) ? gtime() : 0;
   const int r = (blockIdx.x * blockDim.x + threadIdx.x) / kGroup;
   const int sub = threadIdx.x % kGroup;
   double ta = 0.0, tb = 0.0, tl = 0.0;
   float kmax = 0.f;
   anchor_work(a, r, sub, ta, tb, tl, kmax);
-  if (a.dbg && threadIdx.x == 0) a.dbg[blockIdx.x * 8 + 3] = gtime();
+  if (kProfStamps && a.dbg && threadIdx.x == 0) a.dbg[blockIdx.x * 8 + 3] = gtime();
   block_partials(a, ta, tb, tl, kmax);
-  if (a.dbg && threadIdx.x == 0) { a.dbg[blockIdx.x * 8 + 0] = t_entry; a.dbg[blockIdx.x * 8 + 1] = t_wait; a.dbg[blockIdx.x * 8 + 4] = gtime(); }
+  if (kProfStamps && a.dbg && threadIdx.x == 0) { a.dbg[blockIdx.x * 8 + 0] = t_entry; a.dbg[blockIdx.x * 8 + 1] = t_wait; a.dbg[blockIdx.x * 8 + 4] = gtime(); }
 }
 
 

@@ -5,6 +5,8 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include "kernels.cuh"
+
 namespace fc {
 
 // Replica scalar state of the global temperature (trainer.cpp:245-254), device resident.
@@ -78,7 +80,7 @@ struct StepArgs {
   int* err;
   StepResult* result;
   float gscale;                          // c = 1 / (Bl (B-1)), engine.cpp:84-85
-  long long* dbg;                        // FC_SIM_DEBUG=9: per-block globaltimer stamps of fc_anchor_kernel
+  long long* dbg;                        // FC_PROFILE builds: per-block globaltimer stamps of fc_anchor_kernel
   int prep_row0, prep_rows;              // rows of the prep kernel (all of G, or this rank's L before the gather)
   int weights_replica_only;              // fc_weights_kernel: only the u replica update (parameters arrived)
   unsigned long long* step_tag;          // the step's sequence number (prep writes it; pass 1's id set uses it)

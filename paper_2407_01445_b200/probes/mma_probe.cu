@@ -1,9 +1,17 @@
-// mma_probe.cu -- microbenchmark of the tcgen05 issue rate (diagnostics only, not on the
-// loss-step path): one CTA pair issues n back-to-back bf16 MMAs on resident shared-memory
+// mma_probe.cu -- microbenchmark of the tcgen05 issue rate (diagnostics only, NOT part of the
+// product library; build it on its own:
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -Xcompiler -fPIC -shared \
+//        -I paper_2407_01445_b200/csrc paper_2407_01445_b200/probes/mma_probe.cu -o /tmp/libmma_probe.so
+// and call probe_mma / probe_ring through ctypes; scripts/mma_probe2.py): one CTA pair issues n back-to-back bf16 MMAs on resident shared-memory
 // operands (M = 256 pair, N = 256, K = 16 each), optionally committing every `commit_every`
 // MMAs to an mbarrier; the leader reports elapsed SM cycles.
 #include "kernels.cuh"
 #include "sm100.cuh"
+
+namespace fc {
+cudaError_t launch_ring_probe(int n_pairs, int n_kb, int tile_kb, int epi, long long* cycles, cudaStream_t s);
+cudaError_t launch_mma_probe(int n_pairs, int n_mma, int commit_every, long long* cycles, cudaStream_t s);
+}  // namespace fc
 
 namespace fc {
 
@@ -184,3 +192,10 @@ cudaError_t launch_mma_probe(int n_pairs, int n_mma, int commit_every, long long
 }
 
 }  // namespace fc
+
+extern "C" int probe_mma(int n_pairs, int n_mma, int commit_every, long long* cycles, void* stream) {
+  return static_cast<int>(fc::launch_mma_probe(n_pairs, n_mma, commit_every, cycles, static_cast<cudaStream_t>(stream)));
+}
+extern "C" int probe_ring(int n_pairs, int n_kb, int tile_kb, int epi, long long* cycles, void* stream) {
+  return static_cast<int>(fc::launch_ring_probe(n_pairs, n_kb, tile_kb, epi, cycles, static_cast<cudaStream_t>(stream)));
+}

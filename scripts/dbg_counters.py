@@ -1,8 +1,8 @@
-"""FC_SIM_DEBUG=9 counters of the similarity kernels (diagnostics; results of the step are valid)."""
+"""Profiling counters of the step's kernels (diagnostics; results of the step are valid). Needs the
+profiling build: FC_PROFILE=1 python -m paper_2407_01445_b200.build --force, then FC_PROF=1."""
 import ctypes as C, os, sys, numpy as np, torch
 sys.path.insert(0, '.')
-os.environ['FC_SIM_DEBUG'] = '9'
-os.environ.setdefault('FC_GEMM_DEBUG', '9')
+os.environ['FC_PROF'] = '1'
 os.environ['FC_GRAPH'] = '1'
 import paper_2407_01445_b200 as P
 from paper_2407_01445_b200 import synthetic as S
@@ -34,17 +34,13 @@ for _ in range(5): st.step(e1, e2, ids, 0.6, 1e-14)
 torch.cuda.synchronize()
 print('phases (debug9 build)', {k: round(v * 1e3, 1) for k, v in st.phase_times(4).items()})
 g = out[2 * R:2 * R + 160 * 16].reshape(160, 16)[:148]
-if os.environ.get('FC_GEMM_DEBUG') in ('9', '10'):
+if True:
     ld = g[0::2]   # pair leaders (MMA counters)
     t0 = g[:, 11].min()
     us = lambda x: np.round(np.percentile((x - t0) / 1e3, [0, 50, 100]), 2)
     print(f'GEMM: MMA-warp cycles total {ld[:, 0].mean():.0f} (max {ld[:, 0].max()}) waits: tempty {ld[:, 1].mean():.0f} full {ld[:, 2].mean():.0f} first {ld[:, 3].mean():.0f}; units {ld[:, 4].min()}-{ld[:, 4].max()}')
     print(f'   epilogue warp0 cycles total {g[:, 8].mean():.0f} wait tfull {g[:, 9].mean():.0f}')
     print('   timeline us: entry', us(g[:, 11]), 'MMA end', us(ld[:, 5]), 'epi end', us(g[:, 10]))
-for pp in (1, 2):
-    n = C.c_int(0)
-    P.lib().fc_debug_gemm_clusters(pp, C.byref(n))
-    print(f'GEMM pairs/cluster {pp}: max active clusters {n.value}')
 # absolute step timeline from the per-CTA globaltimer stamps (ns): one graph replay
 for _ in range(2): st.step(e1, e2, ids, 0.6, 1e-14)
 st.disable_phase_timing()
@@ -62,7 +58,7 @@ f = lambda x: round((x - t0) / 1e3, 2)
 print('graph-step timeline (us from pass-1 first CTA entry):')
 print('  pass1: first entry', f(tls[0][:, 0].min()), 'last entry', f(tls[0][:, 0].max()), 'first exit', f(tls[0][:, 2].min()), 'last exit', f(tls[0][:, 2].max()))
 print('  pass2: first entry', f(tls[1][:, 0].min()), 'last entry', f(tls[1][:, 0].max()), 'first exit', f(tls[1][:, 2].min()), 'last exit', f(tls[1][:, 2].max()))
-if os.environ.get('FC_GEMM_DEBUG') in ('9', '10'):
+if True:
     print('  gemm : first entry', f(g[:, 11].min()), 'last entry', f(g[:, 11].max()), 'epi end min', f(g[:, 10].min()), 'epi end max', f(g[:, 10].max()))
 an = out[2 * R + 160 * 16:2 * R + 160 * 16 + 640 * 8].reshape(640, 8)
 an = an[an[:, 0] != 0]

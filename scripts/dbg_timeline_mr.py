@@ -1,9 +1,9 @@
-"""Per-rank step timeline of the K > 1 path (FC_SIM_DEBUG=9 globaltimer stamps, one graph
+"""Per-rank step timeline of the K > 1 path (profiling-build globaltimer stamps (FC_PROFILE=1 build, FC_PROF=1), one graph
 replay per rank). Launch: torchrun --nproc-per-node K scripts/dbg_timeline_mr.py"""
 import ctypes as C, os, sys, numpy as np, torch
 import torch.distributed as tdist
 sys.path.insert(0, '.')
-os.environ['FC_SIM_DEBUG'] = '9'
+os.environ['FC_PROF'] = '1'
 os.environ.setdefault('FC_GEMM_DEBUG', '9')
 import paper_2407_01445_b200 as P
 from paper_2407_01445_b200 import synthetic as S
