@@ -221,7 +221,11 @@ def main():
     from paper_2407_01445_b200 import synthetic as S
 
     world, rank, local = dist_env()
-    os.environ.setdefault("NCCL_DEBUG", "WARN")   # keep rank 0's stdout to the one JSON line
+    os.environ.setdefault("NCCL_DEBUG", "WARN")
+    # rank 0's stdout carries exactly one JSON line: libraries that print to fd 1 (NCCL's version
+    # banner, warnings) are redirected to stderr, the line goes to a duplicate of the real stdout
+    out = os.fdopen(os.dup(1), "w")
+    os.dup2(2, 1)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
@@ -447,7 +451,7 @@ def main():
             "roofline": roofline, "step_roofline": step_roofline, "table_kernel": k2,
             "phases_ms": phases, "clocks": clk, "cpu_baseline": cpu,
             "last_step": {"loss": sc.loss, "gtau": sc.gtau, "tau": sc.tau, "exp_clamps": sc.exp_clamps}}
-    print(json.dumps(line), flush=True)
+    print(json.dumps(line), file=out, flush=True)
     if world > 1:   # torch's process group first, then the loss step's own communicator
         tdist.barrier()
         tdist.destroy_process_group()

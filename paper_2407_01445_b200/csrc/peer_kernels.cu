@@ -95,12 +95,14 @@ __global__ void __launch_bounds__(256) peer_gather_kernel(PeerGather g) {
   // rank then poisons every rank (fabric.cpp:228-235); a poisoned rank stops waiting at once.
   const long long t0 = gtimer();
   for (int k = 0; k < g.world; ++k) {
+    unsigned spins = 0;
     while (ld_relaxed_sys(g.my_flag + k) < g.seq) {
+      __nanosleep(64);
+      if ((++spins & 255u) != 0u) continue;   // the abort word and the clock: every 256 polls
       if (ld_relaxed_sys(g.my_abort) != 0ull) {   // a peer gave up on this collective
         atomicCAS(g.err, 0, kErrCollectiveAborted);
         return;
       }
-      __nanosleep(128);
       if (gtimer() - t0 > g.timeout_ns) {
         for (int j = 0; j < g.world; ++j) st_relaxed_sys(g.peer_abort[j], g.seq);
         atomicCAS(g.err, 0, kErrCollectiveAborted);

@@ -121,6 +121,17 @@ def lib():
         L.fc_table_update.argtypes = [P, P, I64, P, P, P, I32, D, P, P, P, P]
         L.fc_grad_tau.argtypes = [I32, I32, I64, P, P, P, P, P, P, D, D, D, I64, P, P, P, P]
         L.fc_last_error.restype = C.c_char_p
+        try:
+            _bind_extended(L, D, I32, I64, P, LP)
+        except AttributeError:
+            if not os.environ.get("FC_LIB_PATH"):   # an older build loaded for an A/B lacks these
+                raise
+        _lib = L
+    return _lib
+
+
+def _bind_extended(L, D, I32, I64, P, LP):
+    if True:
         L.fc_table_write.argtypes = [P, C.c_char_p]
         L.fc_table_read.argtypes = [P, C.c_char_p]
         L.fc_checkpoint_write.argtypes = [P, C.c_char_p, C.POINTER(FcModelState)]
@@ -140,8 +151,6 @@ def lib():
         L.fc_model_last_error.restype = C.c_char_p
         L.fc_comm_ledger.argtypes = [P, C.POINTER(FcLedgerEntry), I32]
         L.fc_comm_ledger_reset.argtypes = [P]
-        _lib = L
-    return _lib
 
 
 EXPORTED = [

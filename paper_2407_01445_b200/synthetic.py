@@ -61,9 +61,17 @@ _I32P = C.POINTER(C.c_int32)
 _F64P = C.POINTER(C.c_double)
 
 
+_SYN = None
+
+
 def _lib():
-    from .fastclip import lib
-    L = lib()
+    # the in-tree build (not an FC_LIB_PATH override: an A/B against an older build still draws
+    # the same inputs)
+    global _SYN
+    if _SYN is None:
+        from . import build as _build
+        _SYN = C.CDLL(_build.build())
+    L = _SYN
     if not getattr(L, "_synthetic_typed", False):
         L.fc_synthetic_embeddings.argtypes = [C.c_uint64, C.c_int32, C.c_int32, C.c_double, _U16P, _U16P]
         L.fc_synthetic_ids.argtypes = [C.c_uint64, C.c_int32, C.c_int64, _I32P]
