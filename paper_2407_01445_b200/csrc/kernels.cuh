@@ -94,7 +94,7 @@ struct SimParams {
   float4* zero0;
   float4* zero1;
   long long zero_n4;
-  // duplicate-id check, run by the idle MMA warp of every non-leader CTA: an open-addressing set
+  // duplicate-id check, run by the epilogue threads before their first tile: an open-addressing set
   // of the rank's ids with slots tagged by the step's sequence number (*step_tag, written by
   // prep), so nothing is cleared between steps; a repeat sets *err = FC_ERR_OWNERSHIP before
   // the per-anchor kernel (which skips every table write then) starts

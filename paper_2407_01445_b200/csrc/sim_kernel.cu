@@ -522,19 +522,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(SimCfg<kMode>::kThre
         if constexpr (kMode == kSimQ) if (it == 0) load_params(0);
       }
     }
-  } else if (warp == kMmaWarp && rank != 0) {
-    // ===================== duplicate-id check (the non-leader CTA's idle MMA warp) =====================
-    if (p.idset) {
-      griddep_wait();   // prep wrote this step's tag
-      const unsigned long long seq = *p.step_tag;
-      bool dup = false;
-      for (int i = pair * 32 + static_cast<int>(lane); i < p.n_ids; i += n_pairs * 32) {
-        const int id = p.ids[i];
-        if (id >= 0 && !idset_insert(p.idset, p.idset_mask, seq, id)) dup = true;
-      }
-      // a repeated id: the reference's owner check (state.cpp:47-49) rejects the write
-      if (dup) atomicCAS(p.err, 0, 5 /* FC_ERR_OWNERSHIP */);
-    }
   } else if (warp == kMmaWarp) {
     // ===================== MMA issuer (leader CTA only, one thread) =====================
     // The issue loop is kept lean (precomputed descriptors, no per-MMA address math, no
@@ -628,6 +615,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(SimCfg<kMode>::kThre
       }
     }
     griddep_wait();   // row / column parameters and bounds come from the preceding kernel
+    if (p.idset) {
+      // duplicate-id check: every epilogue thread of the grid inserts at most a few of the rank's
+      // ids (one L2 round trip before its first accumulator wait, overlapping the first MMAs)
+      const unsigned long long seq = *p.step_tag;   // written by prep (this grid's predecessor)
+      bool dup = false;
+      for (int i = blockIdx.x * kEpi * 32 + static_cast<int>(threadIdx.x); i < p.n_ids; i += gridDim.x * kEpi * 32) {
+        const int id = p.ids[i];
+        if (id >= 0 && !idset_insert(p.idset, p.idset_mask, seq, id)) dup = true;
+      }
+      // a repeated id: the reference's owner check (state.cpp:47-49) rejects the write
+      if (__any_sync(0xffffffffu, dup) && lane == 0) atomicCAS(p.err, 0, 5 /* FC_ERR_OWNERSHIP */);
+    }
     const uint32_t q4 = warp & 3;               // TMEM lane quarter accessible to this warp
     long long e_wait = 0, e_ld = 0, e_math = 0, e_t0 = clock64(), e_g0 = 0;
     const bool eprof = kProf && warp == 5;

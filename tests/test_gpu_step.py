@@ -235,3 +235,31 @@ def test_step_matches_oracle_config1_shape(variant):
     res, _, _, _ = run_pair(variant, B=256, d=512, N=4096, steps=2, seed=3)
     for i, (got, ref) in enumerate(res):
         _check(got, ref, f"{variant} step {i}")
+
+
+@pytest.mark.parametrize("tau_init", [0.0299, 0.05])
+def test_tau_lr_latch_state_matches_oracle(tau_init):
+    # TauLrLatch (schedules.hpp:52-59, trainer.cpp:573-574): once the pre-step tau is below the
+    # threshold (0.03) the tau lr is scaled by the factor for good; the device latch, tau and its
+    # Adam state follow the oracle step by step
+    import torch
+    import paper_2407_01445_b200 as P
+    N, B, d = 2000, 128, 64
+    ocfg = O.default_config("fastclip_v3", N, tau_init=tau_init, tau_lr=1e-2)
+    st = O.new_state(ocfg)
+    step = P.LossStep(gpu_cfg(ocfg, d, B))
+    seen = []
+    for s in range(4):
+        b1, b2 = S.embeddings(B, d, 40 + s)
+        ids = S.ids(B, N, 40 + s)
+        ref = O.step(ocfg, st, 1, S.bf16_to_f32(b1).astype(np.float64), S.bf16_to_f32(b2).astype(np.float64), ids,
+                     0.6, 1e-14)
+        step.step(to_dev_bf16(b1), to_dev_bf16(b2), torch.from_numpy(ids).cuda(), 0.6, 1e-14)
+        sc = step.scalars()
+        ts = step.tau_state()
+        assert sc.latched == st.latched == ts["latched"], (s, sc.latched, st.latched)
+        assert abs(ts["tau"] - st.tau) <= 1e-3 * st.tau and ts["step"] == st.tau_step, (s, ts, st.tau)
+        assert abs(sc.tau - ref["tau_new"]) <= 1e-3 * ref["tau_new"]
+        seen.append(sc.latched)
+    if tau_init < 0.03:
+        assert seen == [1, 1, 1, 1]   # latched at the first step, for good
