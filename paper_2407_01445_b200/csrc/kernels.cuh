@@ -160,6 +160,7 @@ struct PeerGather {
   // for a peer's flag stores a non-zero abort word into every rank (its own included); every
   // waiting rank polls its local abort word and leaves with FC_ERR_COLLECTIVE_ABORTED
   long long timeout_ns;
+  int bulk;                           // 1: the slices go through the bulk-copy engine (thread 0 per CTA)
   unsigned long long* my_abort;
   unsigned long long* peer_abort[kMaxPeers];
 };

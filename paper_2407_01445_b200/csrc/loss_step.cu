@@ -194,6 +194,7 @@ struct LossStep {
   int idset_slots = 0;
   unsigned long long* step_tag = nullptr;
   bool dup_check = true;                 // FC_DUP_CHECK=0: skip the duplicate-id check (A/B only)
+  bool peer_bulk = false;                // FC_PEER_BULK=1: the embedding gather through the bulk-copy engine
   fc::StepResult* result_d = nullptr;   // device alias of result_h (mapped pinned memory)
   fc::StepResult* result_h = nullptr;   // written by the reduce kernel over PCIe: no D2H copy node
   cudaEvent_t done{}, fork{}, side_fork{}, side_join{};
@@ -379,6 +380,7 @@ struct LossStep {
     if (debug_sync) use_graph = false;
     if (const char* e = std::getenv("FC_SHARED_Q")) shared_q = shared_q && atoi(e) != 0;
     if (const char* e = std::getenv("FC_DUP_CHECK")) dup_check = atoi(e) != 0;
+    if (const char* e = std::getenv("FC_PEER_BULK")) peer_bulk = atoi(e) != 0;
     if (const char* e = std::getenv("FC_TEST_DELAY_US")) test_delay_ns = K > 1 ? atoll(e) * 1000LL : 0;
     FC_CUDA(fc::sim_set_smem());
     FC_CUDA(fc::gemm_set_smem());
@@ -730,6 +732,7 @@ struct LossStep {
         // bounds slot (source 2, prep's norm maxima) is sent after griddepcontrol.wait. Pass 1
         // waits for this grid, which completes only after prep did.
         g.wait_src = 2;
+        g.bulk = peer_bulk ? 1 : 0;
         FC_CUDA(fc::launch_peer_gather(g, n_sm, 256, st, pdl && !timing));
       } else {
         FC_NCCL(ncclGroupStart());

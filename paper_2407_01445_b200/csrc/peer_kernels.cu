@@ -45,12 +45,66 @@ __device__ __forceinline__ long long gtimer() {
 
 constexpr int kErrCollectiveAborted = 8;   // FC_ERR_COLLECTIVE_ABORTED (CollectiveAborted, errors.hpp)
 
+constexpr uint32_t kBulkChunk = 16384;   // bytes per bulk chunk (two chunks of shared staging per CTA)
+
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+// Bulk-copy engine path: thread 0 of each CTA streams its chunks of the slices through two
+// shared-memory buffers -- one bulk load from local memory, then one bulk store per rank into
+// the peer-mapped destination (the copy engine issues the NVLink writes instead of 16-byte LSU
+// stores from every thread) -- and waits for the stores' completion before the grid ticket.
+__device__ void gather_bulk(const PeerGather& g, uint8_t* stage, uint64_t* bar) {
+  if (threadIdx.x != 0) return;
+  for (int b = 0; b < 2; ++b)
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(bar + b)));
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  uint32_t it = 0;
+  for (int t = 0; t < g.n_src; ++t) {
+    if (t == g.wait_src) asm volatile("griddepcontrol.wait;" ::: "memory");   // the predecessor's outputs
+    const size_t bytes = g.bytes[t];
+    for (size_t off = static_cast<size_t>(blockIdx.x) * kBulkChunk; off < bytes;
+         off += static_cast<size_t>(gridDim.x) * kBulkChunk, ++it) {
+      const uint32_t sz = static_cast<uint32_t>(bytes - off < kBulkChunk ? bytes - off : kBulkChunk);
+      const uint32_t b = it & 1;
+      uint8_t* buf = stage + b * kBulkChunk;
+      // the stores that read this buffer two chunks ago are done reading it
+      asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar + b)), "r"(sz) : "memory");
+      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                       smem_addr(buf)),
+                   "l"(reinterpret_cast<uint64_t>(g.src[t] + off)), "r"(sz), "r"(smem_addr(bar + b))
+                   : "memory");
+      asm volatile(
+          "{\n\t.reg .pred P1;\n\t"
+          "WAIT_%=:\n\t"
+          "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+          "@P1 bra DONE_%=;\n\t"
+          "bra WAIT_%=;\n\t"
+          "DONE_%=:\n\t}" ::"r"(smem_addr(bar + b)),
+          "r"((it >> 1) & 1u)
+          : "memory");
+      for (int k = 0; k < g.world; ++k)
+        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(
+                         reinterpret_cast<uint64_t>(g.dst[t][k] + static_cast<size_t>(g.rank) * bytes + off)),
+                     "r"(smem_addr(buf)), "r"(sz)
+                     : "memory");
+      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    }
+  }
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");   // every store performed
+  asm volatile("fence.proxy.async.global;" ::: "memory");     // async-proxy writes -> generic observers
+}
+
 __global__ void __launch_bounds__(256) peer_gather_kernel(PeerGather g) {
   if (kProfStamps && g.dbg && blockIdx.x == 0 && threadIdx.x == 0) g.dbg[0] = gtimer();
   if (g.early_trigger) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   // ---- this rank's slices -> every rank's destination (row offset rank * bytes) ----
+  extern __shared__ __align__(128) uint8_t bulk_stage[];
+  if (g.bulk) gather_bulk(g, bulk_stage, reinterpret_cast<uint64_t*>(bulk_stage + 2 * kBulkChunk));
   const size_t stride = static_cast<size_t>(gridDim.x) * blockDim.x;
-  for (int t = 0; t < g.n_src; ++t) {
+  for (int t = 0; t < (g.bulk ? 0 : g.n_src); ++t) {
     if (t == g.wait_src) asm volatile("griddepcontrol.wait;" ::: "memory");   // the predecessor's outputs
     const size_t n16 = g.bytes[t] / 16;
     const uint4* src = reinterpret_cast<const uint4*>(g.src[t]);
@@ -121,7 +175,7 @@ cudaError_t launch_peer_gather(const PeerGather& g, int blocks, int threads, cud
   attr[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
   cfg.gridDim = dim3(blocks, 1, 1);
   cfg.blockDim = dim3(threads, 1, 1);
-  cfg.dynamicSmemBytes = 0;
+  cfg.dynamicSmemBytes = g.bulk ? 2 * kBulkChunk + 64 : 0;
   cfg.stream = s;
   cfg.attrs = attr;
   cfg.numAttrs = 1;

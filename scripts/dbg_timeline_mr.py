@@ -4,7 +4,6 @@ import ctypes as C, os, sys, numpy as np, torch
 import torch.distributed as tdist
 sys.path.insert(0, '.')
 os.environ['FC_PROF'] = '1'
-os.environ.setdefault('FC_GEMM_DEBUG', '9')
 import paper_2407_01445_b200 as P
 from paper_2407_01445_b200 import synthetic as S
 rank, K = int(os.environ['RANK']), int(os.environ['WORLD_SIZE'])
