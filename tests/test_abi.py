@@ -10,14 +10,14 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 def _declared():
     src = open(os.path.join(ROOT, "include", "fastclip_b200.h")).read()
-    return sorted(set(re.findall(r"^\s*(?:int|double|const char\*)\s+(fc_\w+)\s*\(", src, re.M)))
+    return sorted(set(re.findall(r"^\s*(?:int|int64_t|double|const char\*)\s+(fc_\w+)\s*\(", src, re.M)))
 
 
 def test_header_symbols_exported():
     import paper_2407_01445_b200 as P
     L = P.lib()
     names = _declared()
-    assert len(names) >= 18
+    assert len(names) >= 40
     for n in names:
         assert hasattr(L, n), n
 
@@ -34,6 +34,8 @@ def test_config_defaults_match_reference_resolution():
     assert v1.tau_lr == 0.0
     mb = P.config_defaults("openclip_mbcl", 100)
     assert (mb.scale_by_tau, mb.rho) == (0, 0.0)
+    # fabric.reduction = auto: the OpenCLIP baseline reduce-scatters, everything else gathers u
+    assert mb.reduction == 1 and v3.reduction == 0 and v2.reduction == 0   # trainer.cpp:86-88
     with pytest.raises(P.FastclipError):
         P.config_defaults(9, 100)
 
