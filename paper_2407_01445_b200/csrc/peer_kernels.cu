@@ -97,34 +97,58 @@ __device__ void gather_bulk(const PeerGather& g, uint8_t* stage, uint64_t* bar) 
   asm volatile("fence.proxy.async.global;" ::: "memory");     // async-proxy writes -> generic observers
 }
 
+// Sources [t0, t1) as one concatenated index space of 16-byte chunks, grid-strided, four
+// independent loads in flight per thread before the stores to every rank.
+__device__ void gather_lsu(const PeerGather& g, int t0, int t1) {
+  size_t total = 0;
+  for (int t = t0; t < t1; ++t) total += g.bytes[t] / 16;
+  const size_t stride = static_cast<size_t>(gridDim.x) * blockDim.x;
+  constexpr int kU = 4;
+  for (size_t i0 = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x; i0 < total; i0 += kU * stride) {
+    uint4 v[kU];
+    int ts[kU];
+    size_t js[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      size_t j = i0 + u * stride;
+      int t = t0;
+      ts[u] = -1;
+      if (j < total) {
+        while (j >= g.bytes[t] / 16) {
+          j -= g.bytes[t] / 16;
+          ++t;
+        }
+        ts[u] = t;
+        js[u] = j;
+        v[u] = reinterpret_cast<const uint4*>(g.src[t])[j];
+      }
+    }
+#pragma unroll 1
+    for (int k = 0; k < g.world; ++k) {
+#pragma unroll
+      for (int u = 0; u < kU; ++u)
+        if (ts[u] >= 0)
+          reinterpret_cast<uint4*>(g.dst[ts[u]][k] + static_cast<size_t>(g.rank) * g.bytes[ts[u]])[js[u]] = v[u];
+    }
+  }
+}
+
 __global__ void __launch_bounds__(256) peer_gather_kernel(PeerGather g) {
   if (kProfStamps && g.dbg && blockIdx.x == 0 && threadIdx.x == 0) g.dbg[0] = gtimer();
   if (g.early_trigger) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   // ---- this rank's slices -> every rank's destination (row offset rank * bytes) ----
   extern __shared__ __align__(128) uint8_t bulk_stage[];
   if (g.bulk) gather_bulk(g, bulk_stage, reinterpret_cast<uint64_t*>(bulk_stage + 2 * kBulkChunk));
-  const size_t stride = static_cast<size_t>(gridDim.x) * blockDim.x;
-  for (int t = 0; t < (g.bulk ? 0 : g.n_src); ++t) {
-    if (t == g.wait_src) asm volatile("griddepcontrol.wait;" ::: "memory");   // the predecessor's outputs
-    const size_t n16 = g.bytes[t] / 16;
-    const uint4* src = reinterpret_cast<const uint4*>(g.src[t]);
-    // four independent 16-byte loads in flight per thread before the stores: the copy is
-    // load-latency bound otherwise (one L2/HBM round trip per grid-stride step)
-    constexpr int kU = 4;
-    for (size_t i0 = blockIdx.x * blockDim.x + threadIdx.x; i0 < n16; i0 += kU * stride) {
-      uint4 v[kU];
-#pragma unroll
-      for (int u = 0; u < kU; ++u) {
-        const size_t i = i0 + u * stride;
-        v[u] = i < n16 ? src[i] : make_uint4(0u, 0u, 0u, 0u);
-      }
-#pragma unroll 1
-      for (int k = 0; k < g.world; ++k) {
-        uint4* dst = reinterpret_cast<uint4*>(g.dst[t][k] + static_cast<size_t>(g.rank) * g.bytes[t]);
-#pragma unroll
-        for (int u = 0; u < kU; ++u)
-          if (i0 + u * stride < n16) dst[i0 + u * stride] = v[u];
-      }
+  if (!g.bulk) {
+    // the sources written before this kernel started, then (after griddepcontrol.wait) the ones
+    // its predecessor writes: each range is one flattened index space of 16-byte chunks, so a
+    // thread keeps four loads in flight across small sources too (one round trip per batch,
+    // not one per source)
+    const int w = (g.wait_src >= 0 && g.wait_src < g.n_src) ? g.wait_src : g.n_src;
+    gather_lsu(g, 0, w);
+    if (w < g.n_src) {
+      asm volatile("griddepcontrol.wait;" ::: "memory");   // the predecessor's outputs
+      gather_lsu(g, w, g.n_src);
     }
   }
   // ---- grid completion: the last CTA publishes and waits ----
