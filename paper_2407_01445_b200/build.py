@@ -33,8 +33,15 @@ def sources():
     return sorted(glob.glob(os.path.join(CSRC, "*.cu")))
 
 
+def flavor() -> str:
+    return "profile" if os.environ.get("FC_PROFILE") == "1" else "release"
+
+
 def up_to_date() -> bool:
     if not os.path.exists(LIB):
+        return False
+    stamp = LIB + ".flavor"   # a profiling build never passes for the release one (or back)
+    if not os.path.exists(stamp) or open(stamp).read().strip() != flavor():
         return False
     t = os.path.getmtime(LIB)
     deps = sources() + glob.glob(os.path.join(CSRC, "*.cuh")) + [
@@ -72,6 +79,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
     os.replace(tmp, LIB)
+    with open(LIB + ".flavor", "w") as fh:
+        fh.write(flavor() + "\n")
     for o in objs:
         os.remove(o)
     return LIB

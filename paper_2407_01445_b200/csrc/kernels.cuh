@@ -104,6 +104,18 @@ struct SimParams {
   int idset_mask;                      // slots - 1 (power of two >= 2 n_ids)
   const unsigned long long* step_tag;
   int* err;
+  // K > 1, STATS: pass 1 overlapped with the embedding gather. A and the column tiles wholly
+  // inside this rank's slice (tiles [jt_lo, jt_lo + n_loc), rows from col_lo) are read from the
+  // caller's buffers (mapA*, mapQo0 / mapQo1 slots); every other tile from the gathered buffers
+  // once the producer saw the flag of each rank whose rows it holds (src_flag[k] >= *step_tag).
+  // Each pair runs its share of the own tiles first, then its share of the remote ones.
+  int local_first;
+  int jt_lo, n_loc;
+  int col_lo;                  // first global row of the caller's slice (also subtracted from A rows)
+  int rows_per_src;            // rows of G per rank
+  const unsigned long long* src_flag;
+  const unsigned long long* abort_flag;
+  int exact_bounds;            // STATS: per-chunk clamp check from the tile values (no norm bounds)
   long long* dbg_out;          // FC_PROFILE builds: per-pair MMA-warp / epilogue counters, per-CTA stamps
 };
 
@@ -164,14 +176,16 @@ struct PeerGather {
   unsigned long long* my_abort;
   unsigned long long* peer_abort[kMaxPeers];
 };
-cudaError_t launch_peer_gather(const PeerGather& g, int blocks, int threads, cudaStream_t s, bool pdl = false);
-void* peer_gather_kernel_fn();
+cudaError_t launch_peer_gather(const PeerGather& g, int blocks, int threads, cudaStream_t s, bool pdl = false,
+                               bool lean = false);
+void* peer_gather_kernel_fn(bool lean = false);
 
 enum SimMode { kSimStats = 0, kSimQ = 1, kSimRaw = 2, kSimFused = 3 };
 
 cudaError_t launch_sim(int mode, const SimParams& p, const CUtensorMap* mapA, const CUtensorMap* mapB,
                        const CUtensorMap* mapQout, int grid, cudaStream_t s, float* raw_out, bool pdl = false);
 cudaError_t sim_set_smem();
+cudaError_t sim_stats_attributes(cudaFuncAttributes* a);
 cudaError_t gemm_set_smem();
 cudaError_t launch_gemm(bool pdl, const GemmParams& p, const CUtensorMap* mapQ, const CUtensorMap* mapX,
                         const CUtensorMap* mapOut, int grid, cudaStream_t s);

@@ -195,6 +195,14 @@ struct LossStep {
   unsigned long long* step_tag = nullptr;
   bool dup_check = true;                 // FC_DUP_CHECK=0: skip the duplicate-id check (A/B only)
   bool peer_bulk = false;                // FC_PEER_BULK=1: the embedding gather through the bulk-copy engine
+  // K > 1 with peer memory: the embedding gather runs on its own stream beside pass 1, which
+  // starts on this rank's own column tiles (FC_GATHER_OVERLAP=0: gather, then pass 1)
+  bool overlap_e = false;
+  cudaStream_t ws3 = nullptr;
+  cudaEvent_t e_fork{}, e_join{};
+  CUtensorMap mE1l{}, mE2l{};             // the caller's slices (A rows and own column tiles)
+  const void* map_l1 = nullptr;
+  const void* map_l2 = nullptr;
   fc::StepResult* result_d = nullptr;   // device alias of result_h (mapped pinned memory)
   fc::StepResult* result_h = nullptr;   // written by the reduce kernel over PCIe: no D2H copy node
   cudaEvent_t done{}, fork{}, side_fork{}, side_join{};
@@ -381,6 +389,20 @@ struct LossStep {
     if (const char* e = std::getenv("FC_SHARED_Q")) shared_q = shared_q && atoi(e) != 0;
     if (const char* e = std::getenv("FC_DUP_CHECK")) dup_check = atoi(e) != 0;
     if (const char* e = std::getenv("FC_PEER_BULK")) peer_bulk = atoi(e) != 0;
+    if (use_peer) {
+      overlap_e = !peer_bulk;
+      if (const char* e = std::getenv("FC_GATHER_OVERLAP")) overlap_e = overlap_e && atoi(e) != 0;
+      // pass 1 waits inside its grid for the gather's flags: a gather CTA must fit beside a pass-1
+      // CTA on the same SM (registers, shared memory, threads), else the overlap could deadlock
+      if (overlap_e) overlap_e = gather_fits_beside_pass1();
+      if (overlap_e) {
+        int lo = 0, hi = 0;
+        FC_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+        FC_CUDA(cudaStreamCreateWithPriority(&ws3, cudaStreamNonBlocking, hi));
+        FC_CUDA(cudaEventCreateWithFlags(&e_fork, cudaEventDisableTiming));
+        FC_CUDA(cudaEventCreateWithFlags(&e_join, cudaEventDisableTiming));
+      }
+    }
     if (const char* e = std::getenv("FC_TEST_DELAY_US")) test_delay_ns = K > 1 ? atoll(e) * 1000LL : 0;
     FC_CUDA(fc::sim_set_smem());
     FC_CUDA(fc::gemm_set_smem());
@@ -394,8 +416,9 @@ struct LossStep {
                                  cudaSharedmemCarveoutMaxShared));
     FC_CUDA(cudaFuncSetAttribute(fc::fc_anchor_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
                                  cudaSharedmemCarveoutMaxShared));
-    FC_CUDA(cudaFuncSetAttribute(fc::peer_gather_kernel_fn(), cudaFuncAttributePreferredSharedMemoryCarveout,
-                                 cudaSharedmemCarveoutMaxShared));
+    for (bool lean : {false, true})
+      FC_CUDA(cudaFuncSetAttribute(fc::peer_gather_kernel_fn(lean), cudaFuncAttributePreferredSharedMemoryCarveout,
+                                   cudaSharedmemCarveoutMaxShared));
     FC_CUDA(cudaFuncSetAttribute(fc::fc_indiv_update_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
                                  cudaSharedmemCarveoutMaxShared));
     mQ[0] = make_map(q, ldq, Bl, static_cast<uint64_t>(ldq) * 2, 64, 128);
@@ -576,6 +599,37 @@ struct LossStep {
     use_peer = true;
   }
 
+  // One (lean) gather CTA of kGatherThreads beside one pass-1 CTA on an SM: shared memory (+ the
+  // per-CTA reservation), threads, and registers per SM sub-partition -- warps are dealt
+  // round-robin over the four sub-partitions, each with a quarter of the register file, so the
+  // pass-1 CTA's 18 warps leave its two fuller sub-partitions the least room; every alignment of
+  // the gather CTA's warps against them must fit.
+  static constexpr int kGatherThreads = 128;
+  bool gather_fits_beside_pass1() const {
+    cudaFuncAttributes fs{}, fg{};
+    if (fc::sim_stats_attributes(&fs) != cudaSuccess ||
+        cudaFuncGetAttributes(&fg, fc::peer_gather_kernel_fn(true)) != cudaSuccess) {
+      cudaGetLastError();
+      return false;
+    }
+    int smem_sm = 0, regs_sm = 0, thr_sm = 0, resv = 0;
+    cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, my_dev);
+    cudaDeviceGetAttribute(&regs_sm, cudaDevAttrMaxRegistersPerMultiprocessor, my_dev);
+    cudaDeviceGetAttribute(&thr_sm, cudaDevAttrMaxThreadsPerMultiProcessor, my_dev);
+    cudaDeviceGetAttribute(&resv, cudaDevAttrReservedSharedMemoryPerBlock, my_dev);
+    auto warp_regs = [](int per_thread) { return (per_thread * 32 + 255) / 256 * 256; };
+    const int sim_warps = fc::kSimThreads / 32, g_warps = kGatherThreads / 32;
+    bool regs_ok = true;
+    for (int rot = 0; rot < 4; ++rot)
+      for (int sp = 0; sp < 4; ++sp) {
+        const int ws_ = (sim_warps - sp + 3) / 4;                    // pass-1 warps on sub-partition sp
+        const int wg = (g_warps - ((sp - rot + 4) % 4) + 3) / 4;     // gather warps there (rotated start)
+        regs_ok = regs_ok && ws_ * warp_regs(fs.numRegs) + wg * warp_regs(fg.numRegs) <= regs_sm / 4;
+      }
+    const long smem = static_cast<long>(fc::kSimSmemBytes) + fs.sharedSizeBytes + resv + fg.sharedSizeBytes + resv;
+    return regs_ok && smem <= smem_sm && fc::kSimThreads + kGatherThreads <= thr_sm;
+  }
+
   void ensure_maps(const void* e1, const void* e2) {
     if (e1 == map_e1 && e2 == map_e2) return;
     const uint64_t rb = static_cast<uint64_t>(d) * 2;
@@ -644,7 +698,7 @@ struct LossStep {
             g.prep_node = nd;
             g.prep_params = kp;
           }
-          if (kp.func == fc::peer_gather_kernel_fn()) {
+          if (kp.func == fc::peer_gather_kernel_fn(false) || kp.func == fc::peer_gather_kernel_fn(true)) {
             GraphEntry::PeerNode pn{nd, kp, *static_cast<fc::PeerGather*>(kp.kernelParams[0])};
             g.peer_nodes.push_back(pn);
           }
@@ -721,9 +775,35 @@ struct LossStep {
       last_prep_e2 = p2;
       last_prep_args = a;
     };
+    const __nv_bfloat16* E1l = E1;   // the caller's slices
+    const __nv_bfloat16* E2l = E2;
+    const bool overlap = K > 1 && overlap_e;
+    if (overlap) {
+      // the embedding gather on its own stream from the step's start: pass 1 reads own column
+      // tiles from the caller's slices and each rank's gathered rows after that rank's flag
+      FC_CUDA(cudaEventRecord(e_fork, st));
+      FC_CUDA(cudaStreamWaitEvent(ws3, e_fork, 0));
+      fc::PeerGather g = pg_e[par];
+      g.src[0] = reinterpret_cast<const uint8_t*>(E1);
+      g.src[1] = reinterpret_cast<const uint8_t*>(E2);
+      g.n_src = 2;   // no bounds slot: pass 1 checks the clamp per chunk, pass 2 gets the slots with the payload
+      g.seq = seq;
+      g.wait_src = -1;
+      FC_CUDA(fc::launch_peer_gather(g, n_sm, kGatherThreads, ws3, false, true));
+      FC_CUDA(cudaEventRecord(e_join, ws3));
+      if (E1 != map_l1 || E2 != map_l2) {
+        const uint64_t rbytes = static_cast<uint64_t>(d) * 2;
+        mE1l = make_map(E1, d, Bl, rbytes, 64, 128);
+        mE2l = make_map(E2, d, Bl, rbytes, 64, 128);
+        map_l1 = E1;
+        map_l2 = E2;
+      }
+    }
     if (local_prep) launch_prep(E1, E2, rank * Bl, Bl);
     if (K > 1) {
-      if (use_peer) {   // NVLink stores into every rank's e1g / e2g, flag handshake
+      if (overlap) {
+        // launched above
+      } else if (use_peer) {   // NVLink stores into every rank's e1g / e2g, flag handshake
         fc::PeerGather g = pg_e[par];
         g.src[0] = reinterpret_cast<const uint8_t*>(E1);
         g.src[1] = reinterpret_cast<const uint8_t*>(E2);
@@ -781,6 +861,26 @@ struct LossStep {
     if (prof) sp.dbg_out = dbg_buf;
     CUtensorMap mA[2] = {mE1k, mE2k}, mB[2] = {mE2k, mE1k};
     mark(2, st);
+    if (overlap) {
+      sp.local_first = 1;
+      sp.col_lo = rank * Bl;
+      sp.jt_lo = (rank * Bl + fc::kPairN - 1) / fc::kPairN;
+      sp.n_loc = std::max(0, std::min((rank + 1) * Bl / fc::kPairN, n_jt) - sp.jt_lo);
+      sp.rows_per_src = Bl;
+      sp.src_flag = pg_e[par].my_flag;
+      sp.abort_flag = pg_e[par].my_abort;
+      sp.exact_bounds = 1;
+      sp.n_bounds = 0;
+      sp.split_tail = 0;
+
+      CUtensorMap mAl[2] = {mE1l, mE2l}, mOwn[2] = {mE2l, mE1l};
+      // at least two tiles per pair: the local-first split keeps every pair's remote share >= 0
+      FC_CUDA(fc::launch_sim(fc::kSimStats, sp, mAl, mB, mOwn, pair_grid(sp.n_items / 2), st, nullptr, pdl && !timing));
+      sp.local_first = 0;
+      sp.exact_bounds = 0;
+      sp.n_bounds = K;
+      sp.split_tail = split_tail ? 1 : 0;
+    } else
     if (fused_p1) {
       // K = 1: segment C is S^T -- its row statistics are the column statistics of the
       // segment-R tiles, collected in the same epilogue (S is multiplied once)
@@ -925,6 +1025,7 @@ struct LossStep {
     mark(6, st);
 
     FC_CUDA(cudaStreamWaitEvent(st, side_join, 0));
+    if (overlap) FC_CUDA(cudaStreamWaitEvent(st, e_join, 0));
   }
 
   // openclip_rs: this rank's anchors' contrast cotangents for every row of G (for_e1 = Q'_C^T E2[L],
@@ -1025,6 +1126,9 @@ struct LossStep {
     if (scal) cudaFree(scal);
     if (ws) cudaStreamDestroy(ws);
     if (ws2) cudaStreamDestroy(ws2);
+    if (ws3) cudaStreamDestroy(ws3);
+    if (e_fork) cudaEventDestroy(e_fork);
+    if (e_join) cudaEventDestroy(e_join);
     cudaEventDestroy(side_fork);
     cudaEventDestroy(side_join);
     cudaEventDestroy(done);

@@ -97,13 +97,13 @@ __device__ void gather_bulk(const PeerGather& g, uint8_t* stage, uint64_t* bar) 
   asm volatile("fence.proxy.async.global;" ::: "memory");     // async-proxy writes -> generic observers
 }
 
-// Sources [t0, t1) as one concatenated index space of 16-byte chunks, grid-strided, four
+// Sources [t0, t1) as one concatenated index space of 16-byte chunks, grid-strided, kU
 // independent loads in flight per thread before the stores to every rank.
+template <int kU>
 __device__ void gather_lsu(const PeerGather& g, int t0, int t1) {
   size_t total = 0;
   for (int t = t0; t < t1; ++t) total += g.bytes[t] / 16;
   const size_t stride = static_cast<size_t>(gridDim.x) * blockDim.x;
-  constexpr int kU = 4;
   for (size_t i0 = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x; i0 < total; i0 += kU * stride) {
     uint4 v[kU];
     int ts[kU];
@@ -133,22 +133,53 @@ __device__ void gather_lsu(const PeerGather& g, int t0, int t1) {
   }
 }
 
-__global__ void __launch_bounds__(256) peer_gather_kernel(PeerGather g) {
+// kLean: the embedding gather that runs beside pass 1 (whose producer waits for its flags), so
+// one of its CTAs must fit next to a pass-1 CTA: 128 threads at <= 32 registers (1024 per warp --
+// what the pass-1 CTA's 96-register warps leave free on its two fuller SM sub-partitions),
+// two loads in flight. Otherwise up to 256 threads, four loads in flight.
+// Two equal-size sources (the embedding slices), lean CTAs: chunk i of both and chunk i + stride
+// of both -- four 16-byte loads in flight per thread within the 32-register budget.
+__device__ void gather_pair_lean(const PeerGather& g) {
+  const size_t n = g.bytes[0] / 16;
+  const size_t stride = static_cast<size_t>(gridDim.x) * blockDim.x;
+  const uint4* a = reinterpret_cast<const uint4*>(g.src[0]);
+  const uint4* b = reinterpret_cast<const uint4*>(g.src[1]);
+  const size_t off = static_cast<size_t>(g.rank) * g.bytes[0];
+  for (size_t i = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += 2 * stride) {
+    const size_t j = i + stride < n ? i + stride : i;   // past the end: chunk i twice (same bytes)
+    const uint4 a0 = a[i], b0 = b[i], a1 = a[j], b1 = b[j];
+#pragma unroll 1
+    for (int k = 0; k < g.world; ++k) {
+      uint4* da = reinterpret_cast<uint4*>(g.dst[0][k] + off);
+      uint4* db = reinterpret_cast<uint4*>(g.dst[1][k] + off);
+      da[i] = a0;
+      db[i] = b0;
+      da[j] = a1;
+      db[j] = b1;
+    }
+  }
+}
+
+template <bool kLean>
+__global__ void __launch_bounds__(kLean ? 128 : 256, kLean ? 16 : 1) peer_gather_kernel(PeerGather g) {
+  constexpr int kU = kLean ? 2 : 4;
   if (kProfStamps && g.dbg && blockIdx.x == 0 && threadIdx.x == 0) g.dbg[0] = gtimer();
   if (g.early_trigger) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   // ---- this rank's slices -> every rank's destination (row offset rank * bytes) ----
   extern __shared__ __align__(128) uint8_t bulk_stage[];
-  if (g.bulk) gather_bulk(g, bulk_stage, reinterpret_cast<uint64_t*>(bulk_stage + 2 * kBulkChunk));
-  if (!g.bulk) {
+  if (!kLean && g.bulk) gather_bulk(g, bulk_stage, reinterpret_cast<uint64_t*>(bulk_stage + 2 * kBulkChunk));
+  if constexpr (kLean) {
+    gather_pair_lean(g);   // the host launches the lean kernel only for two equal-size sources
+  } else if (!g.bulk) {
     // the sources written before this kernel started, then (after griddepcontrol.wait) the ones
     // its predecessor writes: each range is one flattened index space of 16-byte chunks, so a
     // thread keeps four loads in flight across small sources too (one round trip per batch,
     // not one per source)
     const int w = (g.wait_src >= 0 && g.wait_src < g.n_src) ? g.wait_src : g.n_src;
-    gather_lsu(g, 0, w);
+    gather_lsu<kU>(g, 0, w);
     if (w < g.n_src) {
       asm volatile("griddepcontrol.wait;" ::: "memory");   // the predecessor's outputs
-      gather_lsu(g, w, g.n_src);
+      gather_lsu<kU>(g, w, g.n_src);
     }
   }
   // ---- grid completion: the last CTA publishes and waits ----
@@ -192,7 +223,7 @@ __global__ void __launch_bounds__(256) peer_gather_kernel(PeerGather g) {
   if (kProfStamps && g.dbg) g.dbg[3] = gtimer();
 }
 
-cudaError_t launch_peer_gather(const PeerGather& g, int blocks, int threads, cudaStream_t s, bool pdl) {
+cudaError_t launch_peer_gather(const PeerGather& g, int blocks, int threads, cudaStream_t s, bool pdl, bool lean) {
   cudaLaunchConfig_t cfg{};
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -203,9 +234,15 @@ cudaError_t launch_peer_gather(const PeerGather& g, int blocks, int threads, cud
   cfg.stream = s;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, peer_gather_kernel, g);
+  if (lean) {
+    cfg.dynamicSmemBytes = 0;
+    return cudaLaunchKernelEx(&cfg, peer_gather_kernel<true>, g);
+  }
+  return cudaLaunchKernelEx(&cfg, peer_gather_kernel<false>, g);
 }
 
-void* peer_gather_kernel_fn() { return reinterpret_cast<void*>(peer_gather_kernel); }
+void* peer_gather_kernel_fn(bool lean) {
+  return lean ? reinterpret_cast<void*>(peer_gather_kernel<true>) : reinterpret_cast<void*>(peer_gather_kernel<false>);
+}
 
 }  // namespace fc

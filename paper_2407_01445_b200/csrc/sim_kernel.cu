@@ -75,11 +75,30 @@ __device__ __forceinline__ SmemLayout carve(uint8_t* base) {
 // instead of q + 1.
 struct PairItems {
   int q, tail_lo, n_pairs, pair, count;
+  int n_own, rem_lo;   // local-first order: own-tile items, first remote item
 };
-__device__ __forceinline__ PairItems pair_items(int n_tiles, int pair, int n_pairs, bool split) {
+__device__ __forceinline__ PairItems pair_items(const SimParams& p, int n_tiles, int pair, int n_pairs, bool split) {
   PairItems pi;
   pi.n_pairs = n_pairs;
   pi.pair = pair;
+  if (p.local_first) {
+    // two lists in group order -- every (segment, row block) group's own tiles, then every
+    // group's remote tiles. The pair takes a contiguous share of each: the same fraction of the
+    // own list, and of the remote list what makes its total the balanced share of all tiles
+    // (floor(T (p+1) / P) - floor(T p / P); the host launches at most T / 2 pairs, which keeps
+    // the remote shares non-negative). Both shares cover about the same groups, so A mostly
+    // stays resident; the remote share runs in reverse, starting in the group the own share ended in.
+    const long long n_grp = n_tiles / p.n_jt;
+    const long long own = n_grp * p.n_loc;
+    const int c_lo = static_cast<int>(static_cast<long long>(n_tiles) * pair / n_pairs);
+    const int c_hi = static_cast<int>(static_cast<long long>(n_tiles) * (pair + 1) / n_pairs);
+    pi.q = -2;
+    pi.tail_lo = static_cast<int>(own * pair / n_pairs);
+    pi.n_own = static_cast<int>(own * (pair + 1) / n_pairs) - pi.tail_lo;
+    pi.rem_lo = c_lo - pi.tail_lo;
+    pi.count = max(c_hi - c_lo, pi.n_own);
+    return pi;
+  }
   if (!split) {   // contiguous ranges of whole tiles
     pi.q = -1;
     pi.tail_lo = static_cast<int>((static_cast<long long>(n_tiles) * pair) / n_pairs);
@@ -96,6 +115,24 @@ __device__ __forceinline__ PairItems pair_items(int n_tiles, int pair, int n_pai
 __device__ __forceinline__ void decode_item(const SimParams& p, const PairItems& pi, int item, int& s, int& rb,
                                             int& jt, int& half) {
   int t;
+  if (pi.q == -2) {   // local-first order
+    int grp;
+    if (item < pi.n_own) {
+      const int u = pi.tail_lo + item;
+      grp = u / p.n_loc;
+      jt = p.jt_lo + u % p.n_loc;
+    } else {
+      const int n_rem = p.n_jt - p.n_loc;
+      const int v = pi.rem_lo + (pi.count - 1 - item);   // reverse order
+      grp = v / n_rem;
+      const int r = v % n_rem;
+      jt = r < p.jt_lo ? r : r + p.n_loc;
+    }
+    half = -1;
+    s = grp < p.n_rb[0] ? 0 : 1;
+    rb = grp - (s ? p.n_rb[0] : 0);
+    return;
+  }
   if (pi.q < 0) {
     t = pi.tail_lo + item;
     half = -1;
@@ -437,10 +474,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(SimCfg<kMode>::kThre
   cluster_sync();
   tc_fence_after();
   const uint32_t tmem_base = *L.tmem_ptr;
-  griddep_launch_dependents();   // the next kernel may take SMs as this grid's CTAs retire
+  // the next kernel may take SMs as this grid's CTAs retire. Local-first: only once the producer
+  // saw every gather flag -- the dependent grid's early CTAs would otherwise fill the room a
+  // gather CTA needs beside this one (pass 1 waits for that gather)
+  if (!p.local_first) griddep_launch_dependents();
 
   const int n_chunks = (nkb + kSimASlots - 1) / kSimASlots;
-  const PairItems pi = pair_items(p.n_items, pair, n_pairs, p.split_tail != 0);
+  const PairItems pi = pair_items(p, p.n_items, pair, n_pairs, p.split_tail != 0);
   const int it_lo = 0, it_hi = pi.count;
 
   if (warp == kProdWarp) {
@@ -476,16 +516,50 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(SimCfg<kMode>::kThre
         }
         __syncwarp();
       };
+      // local-first (K > 1): rank k's rows of the gathered buffers are read only after its flag
+      // carries this step's sequence number (set by the gather kernel running beside this grid)
+      uint32_t seen = 0;
+      unsigned long long seq = 0;
+      auto wait_rank = [&](int k) {
+        if ((seen >> k) & 1u) return;
+        if (seen == 0) {
+          griddep_wait();   // the step tag is written by the preceding kernel
+          seq = *p.step_tag;
+        }
+        if (issuer) {
+          unsigned spins = 0;
+          while (ld_relaxed_sys(p.src_flag + k) < seq) {
+            __nanosleep(32);
+            // a poisoned collective (the gather kernel's timeout): stop waiting, report it
+            if ((++spins & 255u) == 0u && ld_relaxed_sys(p.abort_flag) != 0ull) {
+              atomicCAS(p.err, 0, 8 /* FC_ERR_COLLECTIVE_ABORTED */);
+              break;
+            }
+          }
+          // acquire through the flag (an acquire load, not a fence.sys: that would drain this SM's
+          // outstanding traffic), then order the peer's rows for the TMA (async-proxy) reads
+          (void)ld_acquire_sys(p.src_flag + k);
+          fence_proxy_async_global();
+        }
+        __syncwarp();
+        seen |= 1u << k;
+      };
       for (int item = it_lo; item < it_hi; ++item, ++it) {
         int s, rb, jt, half;
         decode_item(p, pi, item, s, rb, jt, half);
+        const bool own = p.local_first && jt >= p.jt_lo && jt < p.jt_lo + p.n_loc;
         const CUtensorMap* ma = s ? &mapA1 : &mapA0;
-        const CUtensorMap* mb = s ? &mapB1 : &mapB0;
-        const int a_row = p.seg[s].a_row0 + rb * kPairM + static_cast<int>(rank) * kCtaM;
+        const CUtensorMap* mb = own ? (s ? &mapQo1 : &mapQo0) : (s ? &mapB1 : &mapB0);
+        const int a_row = p.seg[s].a_row0 - (p.local_first ? p.col_lo : 0) + rb * kPairM + static_cast<int>(rank) * kCtaM;
         // each CTA supplies half of the tile's columns: 128 of a whole tile, 64 of a half tile
         // (the 128-row box then also brings 64 rows the UMMA does not read)
-        const int b_row = half < 0 ? jt * kPairN + static_cast<int>(rank) * (kPairN / 2)
-                                   : jt * kPairN + half * (kPairN / 2) + static_cast<int>(rank) * (kPairN / 4);
+        const int b_row = (half < 0 ? jt * kPairN + static_cast<int>(rank) * (kPairN / 2)
+                                    : jt * kPairN + half * (kPairN / 2) + static_cast<int>(rank) * (kPairN / 4)) -
+                          (own ? p.col_lo : 0);
+        if (p.local_first && !own) {
+          const int c_hi = min(jt * kPairN + kPairN, p.seg[s].cols) - 1;
+          for (int k = (jt * kPairN) / p.rows_per_src; k <= c_hi / p.rows_per_src; ++k) wait_rank(k);
+        }
         // params ahead of the tile's operands, except for the pair's first tile: its operands
         // go out first, so its MMAs run while the per-anchor kernel is still producing the
         // parameters (the first param load is the grid-dependency wait)
@@ -520,6 +594,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(SimCfg<kMode>::kThre
           }
         }
         if constexpr (kMode == kSimQ) if (it == 0) load_params(0);
+      }
+      // the later kernels of the step read the whole gathered buffers: every rank's flag (this
+      // rank's own gather included) is observed before this grid completes
+      if (p.local_first) {
+        for (int k = 0; k * p.rows_per_src < p.seg[0].cols; ++k) wait_rank(k);
+        griddep_launch_dependents();
       }
     }
   } else if (warp == kMmaWarp) {
@@ -744,7 +824,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(SimCfg<kMode>::kThre
               if (col0 + k < sg.cols) dst[col0 + k] = __uint_as_float(rr[k]);
           }
         } else if constexpr (kMode == kSimStats) {
-          if (interior && warp_rows_ok && row_safe) stats_fast(rr, rstat.x, rstat.y, se2, sye2);
+          bool fast = interior && warp_rows_ok;
+          if (p.exact_bounds) {   // the chunk's row maxima decide whether safe_exp can clamp
+            if (fast) {
+              float mx = __uint_as_float(rr[0]);
+#pragma unroll
+              for (int k = 1; k < 32; ++k) mx = fmaxf(mx, __uint_as_float(rr[k]));
+              fast = __all_sync(0xffffffffu, fmaf(mx, rstat.x, rstat.y) <= kClampLog2);
+            }
+          } else {
+            fast = fast && row_safe;
+          }
+          if (fast) stats_fast(rr, rstat.x, rstat.y, se2, sye2);
           else stats_masked(rr, rstat.x, rstat.y, col0, sg.cols, gi, row_ok, se, sye, ncl);
         } else if constexpr (kMode == kSimFused) {
           // column anchor of this lane (the statistics it collects) and its parameters
@@ -989,6 +1080,8 @@ cudaError_t sim_set_smem() {
   if (e == cudaSuccess) e = cudaFuncSetAttribute(sim_tile_kernel<kSimFused>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSimSmemBytes);
   return e;
 }
+
+cudaError_t sim_stats_attributes(cudaFuncAttributes* a) { return cudaFuncGetAttributes(a, sim_tile_kernel<kSimStats>); }
 
 cudaError_t launch_sim(int mode, const SimParams& p, const CUtensorMap* mapA, const CUtensorMap* mapB,
                        const CUtensorMap* mapQout, int grid, cudaStream_t s, float* raw_out, bool pdl) {

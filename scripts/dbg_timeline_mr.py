@@ -45,6 +45,13 @@ for rep in range(3):
     lines.append(f'rank {rank} rep {rep} (us from prep entry): prep exit {f(prep[1])} | pass1 {f(tls[0][:, 0].min())}..{f(tls[0][:, 2].max())} '
                  f'| gatherE {[f(x) for x in pe[:4]]} | anchor {f(an[:, 0].min())} wait {f(an[:, 1].min())} exit {f(an[:, 4].max())} '
                  f'| gatherP {[f(x) for x in pe[4:]]} | pass2 {f(tls[1][:, 0].min())}..{f(tls[1][:, 2].max())} | gemm {f(ge.min())}..{f(g[:, 10].max())}')
+    if rep == 2:   # pass-1 MMA-warp counters per pair (cycles -> us at 1.9 GHz)
+        m = out[:74 * 8].reshape(74, 8).astype(np.float64)
+        c = lambda x: np.round(x / 1900.0, 1)
+        lines.append(f'rank {rank} pass1 pairs: items min/max {int(m[:, 6].min())}/{int(m[:, 6].max())} | loop us mean/max {c(m[:, 0].mean())}/{c(m[:, 0].max())} '
+                     f'| wait B mean/max {c(m[:, 3].mean())}/{c(m[:, 3].max())} | wait A {c(m[:, 2].mean())}/{c(m[:, 2].max())} '
+                     f'| wait tmem {c(m[:, 1].mean())}/{c(m[:, 1].max())} | first mma {c(m[:, 4].mean())}/{c(m[:, 4].max())} '
+                     f'| cta entry {f(tls[0][:, 0].min())}..{f(tls[0][:, 0].max())} work end {f(tls[0][:, 1].min())}..{f(tls[0][:, 1].max())}')
 print('\n'.join(lines), flush=True)
 tdist.barrier()
 st.close()

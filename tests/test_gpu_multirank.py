@@ -99,6 +99,17 @@ def _norm_rel(a, b):
                                        (4, "fastclip_v3"), (4, "fastclip_v2"), (4, "fastclip_v0")])
 def test_ranks_match_oracle(K, variant):
     B, d, N, steps = 1024 if K == 4 else 512, 128, 8192, 2
+    _check_ranks(K, variant, B, d, N, steps)
+
+
+@pytest.mark.parametrize("K,variant,B,d", [(2, "fastclip_v3", 2560, 128), (4, "fastclip_v2", 4096, 64)])
+def test_ranks_match_oracle_many_pairs(K, variant, B, d):
+    # enough tiles for every CTA pair of pass 1 to run own-column tiles (from the caller's slice)
+    # before gathered ones (after the peers' flags): the embedding gather overlapped with pass 1
+    _check_ranks(K, variant, B, d, 65536, 2)
+
+
+def _check_ranks(K, variant, B, d, N, steps):
     res, refs, st = _run(K, variant, B, d, N, steps)
     Bl = B // K
     for s in range(steps):
@@ -118,7 +129,10 @@ def test_ranks_match_oracle(K, variant):
         names = ["u1", "u2"] + (["tau1", "tau2"] if "tau1" in tabs else [])
         for name in names:
             got, ref_tab = tabs[name], getattr(st, name)
-            assert np.max(np.abs(got - ref_tab) / np.maximum(np.abs(ref_tab), 1e-300)) < 1e-3, (variant, r, name)
+            # per-index temperatures: each is one sparse-Adam step from an fp32-accumulated
+            # gradient (m / sqrt(v) keeps the gradient's relative error), 3e-3 over 4096 entries
+            tol = 3e-3 if name.startswith("tau") else 1e-3
+            assert np.max(np.abs(got - ref_tab) / np.maximum(np.abs(ref_tab), 1e-300)) < tol, (variant, r, name)
 
 
 def test_nccl_fallback_matches_oracle(monkeypatch):
