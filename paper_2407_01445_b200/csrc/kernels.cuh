@@ -104,17 +104,20 @@ struct SimParams {
   int idset_mask;                      // slots - 1 (power of two >= 2 n_ids)
   const unsigned long long* step_tag;
   int* err;
-  // K > 1, STATS: pass 1 overlapped with the embedding gather. A and the column tiles wholly
-  // inside this rank's slice (tiles [jt_lo, jt_lo + n_loc), rows from col_lo) are read from the
-  // caller's buffers (mapA*, mapQo0 / mapQo1 slots); every other tile from the gathered buffers
-  // once the producer saw the flag of each rank whose rows it holds (src_flag[k] >= *step_tag).
-  // Each pair runs its share of the own tiles first, then its share of the remote ones.
+  // K > 1: a pass overlapped with a gather; each pair runs its share of the own column tiles
+  // (tiles [jt_lo, jt_lo + n_loc), wholly inside this rank's slice) first, then its share of
+  // the remote ones. local_first 1 (pass 1 beside the embedding gather): A and the own tiles are
+  // read from the caller's buffers (mapA*, mapQo0 / mapQo1 slots, rows from col_lo), a remote
+  // tile from the gathered buffers once the producer saw the flag of each rank whose rows it
+  // holds (src_flag[k] >= *step_tag). local_first 2 (pass 2 beside the payload gather): the
+  // operands are all gathered already; a remote tile's column parameters wait for the flags.
   int local_first;
   int jt_lo, n_loc;
   int col_lo;                  // first global row of the caller's slice (also subtracted from A rows)
   int rows_per_src;            // rows of G per rank
   const unsigned long long* src_flag;
   const unsigned long long* abort_flag;
+  long long timeout_ns;        // no flag within this long: FC_ERR_COLLECTIVE_ABORTED, stop waiting
   int exact_bounds;            // STATS: per-chunk clamp check from the tile values (no norm bounds)
   long long* dbg_out;          // FC_PROFILE builds: per-pair MMA-warp / epilogue counters, per-CTA stamps
 };
@@ -185,7 +188,7 @@ enum SimMode { kSimStats = 0, kSimQ = 1, kSimRaw = 2, kSimFused = 3 };
 cudaError_t launch_sim(int mode, const SimParams& p, const CUtensorMap* mapA, const CUtensorMap* mapB,
                        const CUtensorMap* mapQout, int grid, cudaStream_t s, float* raw_out, bool pdl = false);
 cudaError_t sim_set_smem();
-cudaError_t sim_stats_attributes(cudaFuncAttributes* a);
+cudaError_t sim_attributes(int mode, cudaFuncAttributes* a);   // kSimStats / kSimQ
 cudaError_t gemm_set_smem();
 cudaError_t launch_gemm(bool pdl, const GemmParams& p, const CUtensorMap* mapQ, const CUtensorMap* mapX,
                         const CUtensorMap* mapOut, int grid, cudaStream_t s);

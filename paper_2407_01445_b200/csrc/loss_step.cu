@@ -394,7 +394,7 @@ struct LossStep {
       if (const char* e = std::getenv("FC_GATHER_OVERLAP")) overlap_e = overlap_e && atoi(e) != 0;
       // pass 1 waits inside its grid for the gather's flags: a gather CTA must fit beside a pass-1
       // CTA on the same SM (registers, shared memory, threads), else the overlap could deadlock
-      if (overlap_e) overlap_e = gather_fits_beside_pass1();
+      if (overlap_e) overlap_e = gather_fits_beside_passes();
       if (overlap_e) {
         int lo = 0, hi = 0;
         FC_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
@@ -599,15 +599,20 @@ struct LossStep {
     use_peer = true;
   }
 
-  // One (lean) gather CTA of kGatherThreads beside one pass-1 CTA on an SM: shared memory (+ the
+  // One (lean) gather CTA of kGatherThreads beside one pass-1 / pass-2 CTA on an SM: shared memory (+ the
   // per-CTA reservation), threads, and registers per SM sub-partition -- warps are dealt
   // round-robin over the four sub-partitions, each with a quarter of the register file, so the
   // pass-1 CTA's 18 warps leave its two fuller sub-partitions the least room; every alignment of
   // the gather CTA's warps against them must fit.
   static constexpr int kGatherThreads = 128;
-  bool gather_fits_beside_pass1() const {
+  bool gather_fits_beside_passes() const {
+    for (int mode : {fc::kSimStats, fc::kSimQ})
+      if (!gather_fits_beside(mode)) return false;
+    return true;
+  }
+  bool gather_fits_beside(int mode) const {
     cudaFuncAttributes fs{}, fg{};
-    if (fc::sim_stats_attributes(&fs) != cudaSuccess ||
+    if (fc::sim_attributes(mode, &fs) != cudaSuccess ||
         cudaFuncGetAttributes(&fg, fc::peer_gather_kernel_fn(true)) != cudaSuccess) {
       cudaGetLastError();
       return false;
@@ -778,6 +783,9 @@ struct LossStep {
     const __nv_bfloat16* E1l = E1;   // the caller's slices
     const __nv_bfloat16* E2l = E2;
     const bool overlap = K > 1 && overlap_e;
+    // pass 2 beside the payload gather as well, except for the reduce-scatter strategy (its mask
+    // kernel zeroes the gathered parameters of the other ranks' anchors before pass 2)
+    const bool overlap2 = overlap && !rs;
     if (overlap) {
       // the embedding gather on its own stream from the step's start: pass 1 reads own column
       // tiles from the caller's slices and each rank's gathered rows after that rank's flag
@@ -869,6 +877,7 @@ struct LossStep {
       sp.rows_per_src = Bl;
       sp.src_flag = pg_e[par].my_flag;
       sp.abort_flag = pg_e[par].my_abort;
+      sp.timeout_ns = pg_e[par].timeout_ns;
       sp.exact_bounds = 1;
       sp.n_bounds = 0;
       sp.split_tail = 0;
@@ -922,7 +931,18 @@ struct LossStep {
     if (K > 1) {
       // ONE all-gather carries u/tau/id, the v2 per-index tau gradients and the G_tau / loss
       // block partials of every rank (no scalar all-reduce, no second gather)
-      if (use_peer) {
+      if (use_peer && overlap2) {
+        // payload + this rank's pass-2 parameters into every rank, on the gather stream beside
+        // pass 2: pass 2 runs its own column tiles first (their parameters are this rank's, from
+        // the per-anchor kernel) and waits for each rank's flag before that rank's columns
+        fc::PeerGather g = pg_p[par];
+        g.seq = seq;
+        g.early_trigger = 0;
+        g.wait_src = -1;
+        FC_CUDA(cudaEventRecord(e_fork, st));
+        FC_CUDA(cudaStreamWaitEvent(ws3, e_fork, 0));
+        FC_CUDA(fc::launch_peer_gather(g, n_sm, kGatherThreads, ws3, false, true));
+      } else if (use_peer) {
         // payload + this rank's pass-2 parameters into every rank (the u replica update of the
         // other ranks' ids follows on the side branch)
         fc::PeerGather g = pg_p[par];
@@ -941,8 +961,8 @@ struct LossStep {
       }
     }
     // the G_tau reduction, temperature step and IndividualTemp update only feed the next step
-    // and the step scalars: they run on the side branch
-    FC_CUDA(cudaEventRecord(side_fork, st));
+    // and the step scalars: they run on the side branch (after the payload gather)
+    FC_CUDA(cudaEventRecord(side_fork, overlap2 ? ws3 : st));
     FC_CUDA(cudaStreamWaitEvent(ws2, side_fork, 0));
     fc::fc_reduce_kernel<<<1, 32, 0, ws2>>>(a);
     if (K > 1 && use_peer) {
@@ -982,7 +1002,22 @@ struct LossStep {
     }
     if (prof) sp.dbg_out = dbg_buf + 2688;
     sp.q_factor = (!indiv && q_factor) ? 1 : 0;   // one shared temperature: single-exponential Q
-    FC_CUDA(fc::launch_sim(fc::kSimQ, sp, mA, mB, mQo, pair_grid(sp.n_items), st, nullptr, pdl && !timing));
+    int p2_grid = pair_grid(sp.n_items);
+    if (overlap2) {   // own column tiles first; a remote tile's parameters after its ranks' payload flags
+      sp.local_first = 2;
+      sp.col_lo = rank * Bl;
+      sp.jt_lo = (rank * Bl + fc::kPairN - 1) / fc::kPairN;
+      sp.n_loc = std::max(0, std::min((rank + 1) * Bl / fc::kPairN, n_jt) - sp.jt_lo);
+      sp.rows_per_src = Bl;
+      sp.src_flag = pg_p[par].my_flag;
+      sp.abort_flag = pg_p[par].my_abort;
+      sp.timeout_ns = pg_p[par].timeout_ns;
+      sp.split_tail = 0;
+      p2_grid = pair_grid(sp.n_items / 2);
+      // the bounds: an own tile's columns are this rank's anchors (own slot final); the other
+      // slots hold 0 or a peer's final values until its flag, so their max stays a valid bound
+    }
+    FC_CUDA(fc::launch_sim(fc::kSimQ, sp, mA, mB, mQo, p2_grid, st, nullptr, pdl && !timing));
 
     // ---- pass 2b: dE = c (Q' E - r o E_local) ----
     mark(5, st);

@@ -162,14 +162,16 @@ __device__ void gather_pair_lean(const PeerGather& g) {
 
 template <bool kLean>
 __global__ void __launch_bounds__(kLean ? 128 : 256, kLean ? 16 : 1) peer_gather_kernel(PeerGather g) {
-  constexpr int kU = kLean ? 2 : 4;
+  constexpr int kU = 4;
   if (kProfStamps && g.dbg && blockIdx.x == 0 && threadIdx.x == 0) g.dbg[0] = gtimer();
   if (g.early_trigger) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   // ---- this rank's slices -> every rank's destination (row offset rank * bytes) ----
   extern __shared__ __align__(128) uint8_t bulk_stage[];
   if (!kLean && g.bulk) gather_bulk(g, bulk_stage, reinterpret_cast<uint64_t*>(bulk_stage + 2 * kBulkChunk));
-  if constexpr (kLean) {
-    gather_pair_lean(g);   // the host launches the lean kernel only for two equal-size sources
+  if (kLean && g.n_src == 2 && g.bytes[0] == g.bytes[1] && g.wait_src < 0) {
+    gather_pair_lean(g);   // the embedding slices
+  } else if (kLean) {
+    gather_lsu<1>(g, 0, g.n_src);   // the payload (no programmatic predecessor on the lean path)
   } else if (!g.bulk) {
     // the sources written before this kernel started, then (after griddepcontrol.wait) the ones
     // its predecessor writes: each range is one flattened index space of 16-byte chunks, so a

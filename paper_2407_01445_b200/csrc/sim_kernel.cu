@@ -77,11 +77,12 @@ struct PairItems {
   int q, tail_lo, n_pairs, pair, count;
   int n_own, rem_lo;   // local-first order: own-tile items, first remote item
 };
+template <bool kLF>
 __device__ __forceinline__ PairItems pair_items(const SimParams& p, int n_tiles, int pair, int n_pairs, bool split) {
   PairItems pi;
   pi.n_pairs = n_pairs;
   pi.pair = pair;
-  if (p.local_first) {
+  if (kLF && p.local_first) {
     // two lists in group order -- every (segment, row block) group's own tiles, then every
     // group's remote tiles. The pair takes a contiguous share of each: the same fraction of the
     // own list, and of the remote list what makes its total the balanced share of all tiles
@@ -112,10 +113,11 @@ __device__ __forceinline__ PairItems pair_items(const SimParams& p, int n_tiles,
   return pi;
 }
 // item -> (segment, row block, column tile, half: -1 whole tile, 0 / 1 the column half)
+template <bool kLF>
 __device__ __forceinline__ void decode_item(const SimParams& p, const PairItems& pi, int item, int& s, int& rb,
                                             int& jt, int& half) {
   int t;
-  if (pi.q == -2) {   // local-first order
+  if (kLF && pi.q == -2) {   // local-first order
     int grp;
     if (item < pi.n_own) {
       const int u = pi.tail_lo + item;
@@ -151,9 +153,10 @@ __device__ __forceinline__ void decode_item(const SimParams& p, const PairItems&
   jt = local % p.n_jt;
 }
 // Identity of the A block an (item, chunk) needs: segment, row block, 512-wide K chunk.
+template <bool kLF>
 __device__ __forceinline__ int a_key(const SimParams& p, const PairItems& pi, int item, int chunk, int n_chunks) {
   int s, rb, jt, half;
-  decode_item(p, pi, item, s, rb, jt, half);
+  decode_item<kLF>(p, pi, item, s, rb, jt, half);
   return ((s * 65536) + rb) * n_chunks + chunk;
 }
 
@@ -422,6 +425,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(SimCfg<kMode>::kThre
                     const __grid_constant__ CUtensorMap mapB1, const __grid_constant__ CUtensorMap mapQo0,
                     const __grid_constant__ CUtensorMap mapQo1, float* __restrict__ raw_out) {
   constexpr int kStagesB = kMode == kSimQ ? kSimStagesQ : kSimStagesStats;
+  constexpr bool kLF = kMode == kSimStats || kMode == kSimQ;   // the passes that run beside a gather (K > 1)
   constexpr bool kStatsLike = kMode == kSimStats || kMode == kSimFused;
   extern __shared__ uint8_t smem_raw[];
   long long g_entry = 0;
@@ -475,12 +479,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(SimCfg<kMode>::kThre
   tc_fence_after();
   const uint32_t tmem_base = *L.tmem_ptr;
   // the next kernel may take SMs as this grid's CTAs retire. Local-first: only once the producer
-  // saw every gather flag -- the dependent grid's early CTAs would otherwise fill the room a
-  // gather CTA needs beside this one (pass 1 waits for that gather)
+  // saw every gather flag -- the dependent grid's early CTAs would otherwise take the room a
+  // gather CTA needs beside this one (this grid waits for that gather)
   if (!p.local_first) griddep_launch_dependents();
 
   const int n_chunks = (nkb + kSimASlots - 1) / kSimASlots;
-  const PairItems pi = pair_items(p, p.n_items, pair, n_pairs, p.split_tail != 0);
+  const PairItems pi = pair_items<kLF>(p, p.n_items, pair, n_pairs, p.split_tail != 0);
   const int it_lo = 0, it_hi = pi.count;
 
   if (warp == kProdWarp) {
@@ -496,13 +500,54 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(SimCfg<kMode>::kThre
       uint32_t spar = 0;   // bit per A slot: parity of its load generation (afull/aempty phase), kept in a register
       int cur_key = -1;
       int it = 0;
+      // local-first (K > 1): what rank k's gather writes (pass 1: its rows of the gathered
+      // embeddings; pass 2: its anchors' column parameters) is read only after rank k's flag
+      // carries this step's sequence number (set by the gather kernel running beside this grid)
+      uint32_t seen = 0;
+      unsigned long long seq = 0;
+      auto wait_rank = [&](int k) {
+        if ((seen >> k) & 1u) return;
+        if (seen == 0) {
+          griddep_wait();   // the step tag is written by the preceding kernel
+          seq = *p.step_tag;
+        }
+        if (issuer) {
+          unsigned spins = 0;
+          long long t0 = 0;
+          asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+          while (ld_relaxed_sys(p.src_flag + k) < seq) {
+            __nanosleep(32);
+            if ((++spins & 255u) != 0u) continue;
+            // a poisoned collective (the gather kernel's timeout), or no flag within the peer
+            // timeout (e.g. the gather never got an SM): stop waiting, report it
+            long long t1;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+            if (ld_relaxed_sys(p.abort_flag) != 0ull || t1 - t0 > p.timeout_ns) {
+              atomicCAS(p.err, 0, 8 /* FC_ERR_COLLECTIVE_ABORTED */);
+              break;
+            }
+          }
+          // acquire through the flag (an acquire load, not a fence.sys: that would drain this SM's
+          // outstanding traffic), then order the peer's rows for the TMA (async-proxy) reads
+          (void)ld_acquire_sys(p.src_flag + k);
+          fence_proxy_async_global();
+        }
+        __syncwarp();
+        seen |= 1u << k;
+      };
       // column parameters of the pair's j-th tile (each CTA keeps its own copy), written by the
       // preceding per-anchor kernel: the first load waits for that grid (programmatic launch;
       // the A / B operand loads do not depend on it)
+      // columns [jt * 256, +256) of a tile: wait for every rank that holds some of them
+      auto wait_tile = [&](int s, int jt) {
+        const int c_hi = min(jt * kPairN + kPairN, p.seg[s].cols) - 1;
+        for (int k = (jt * kPairN) / p.rows_per_src; k <= c_hi / p.rows_per_src; ++k) wait_rank(k);
+      };
       auto load_params = [&](int j) {
         int s, rb, jt, half;
-        decode_item(p, pi, it_lo + j, s, rb, jt, half);
+        decode_item<kLF>(p, pi, it_lo + j, s, rb, jt, half);
         if (j == 0) griddep_wait();
+        if (p.local_first == 2 && !(jt >= p.jt_lo && jt < p.jt_lo + p.n_loc)) wait_tile(s, jt);
         const int ps = j % kSimPSlots;
         mbar_wait(&L.pempty[ps], ((j / kSimPSlots) & 1) ^ 1);
         if (issuer) {
@@ -516,50 +561,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(SimCfg<kMode>::kThre
         }
         __syncwarp();
       };
-      // local-first (K > 1): rank k's rows of the gathered buffers are read only after its flag
-      // carries this step's sequence number (set by the gather kernel running beside this grid)
-      uint32_t seen = 0;
-      unsigned long long seq = 0;
-      auto wait_rank = [&](int k) {
-        if ((seen >> k) & 1u) return;
-        if (seen == 0) {
-          griddep_wait();   // the step tag is written by the preceding kernel
-          seq = *p.step_tag;
-        }
-        if (issuer) {
-          unsigned spins = 0;
-          while (ld_relaxed_sys(p.src_flag + k) < seq) {
-            __nanosleep(32);
-            // a poisoned collective (the gather kernel's timeout): stop waiting, report it
-            if ((++spins & 255u) == 0u && ld_relaxed_sys(p.abort_flag) != 0ull) {
-              atomicCAS(p.err, 0, 8 /* FC_ERR_COLLECTIVE_ABORTED */);
-              break;
-            }
-          }
-          // acquire through the flag (an acquire load, not a fence.sys: that would drain this SM's
-          // outstanding traffic), then order the peer's rows for the TMA (async-proxy) reads
-          (void)ld_acquire_sys(p.src_flag + k);
-          fence_proxy_async_global();
-        }
-        __syncwarp();
-        seen |= 1u << k;
-      };
       for (int item = it_lo; item < it_hi; ++item, ++it) {
         int s, rb, jt, half;
-        decode_item(p, pi, item, s, rb, jt, half);
-        const bool own = p.local_first && jt >= p.jt_lo && jt < p.jt_lo + p.n_loc;
+        decode_item<kLF>(p, pi, item, s, rb, jt, half);
+        // pass 1 (local_first 1): own tiles and A from the caller's slices
+        const bool own = p.local_first == 1 && jt >= p.jt_lo && jt < p.jt_lo + p.n_loc;
         const CUtensorMap* ma = s ? &mapA1 : &mapA0;
         const CUtensorMap* mb = own ? (s ? &mapQo1 : &mapQo0) : (s ? &mapB1 : &mapB0);
-        const int a_row = p.seg[s].a_row0 - (p.local_first ? p.col_lo : 0) + rb * kPairM + static_cast<int>(rank) * kCtaM;
+        const int a_row = p.seg[s].a_row0 - (p.local_first == 1 ? p.col_lo : 0) + rb * kPairM + static_cast<int>(rank) * kCtaM;
         // each CTA supplies half of the tile's columns: 128 of a whole tile, 64 of a half tile
         // (the 128-row box then also brings 64 rows the UMMA does not read)
         const int b_row = (half < 0 ? jt * kPairN + static_cast<int>(rank) * (kPairN / 2)
                                     : jt * kPairN + half * (kPairN / 2) + static_cast<int>(rank) * (kPairN / 4)) -
                           (own ? p.col_lo : 0);
-        if (p.local_first && !own) {
-          const int c_hi = min(jt * kPairN + kPairN, p.seg[s].cols) - 1;
-          for (int k = (jt * kPairN) / p.rows_per_src; k <= c_hi / p.rows_per_src; ++k) wait_rank(k);
-        }
+        if (p.local_first == 1 && !own) wait_tile(s, jt);
         // params ahead of the tile's operands, except for the pair's first tile: its operands
         // go out first, so its MMAs run while the per-anchor kernel is still producing the
         // parameters (the first param load is the grid-dependency wait)
@@ -567,9 +582,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(SimCfg<kMode>::kThre
         for (int c = 0; c < n_chunks; ++c) {
           const int kb_lo = c * kSimASlots;
           const int kb_hi = min(nkb, kb_lo + kSimASlots);
-          const int key = a_key(p, pi, item, c, n_chunks);
-          if (key != cur_key) {
-            for (int kb = kb_lo; kb < kb_hi; ++kb) {
+          const int key = a_key<kLF>(p, pi, item, c, n_chunks);
+          const bool new_a = key != cur_key;
+          cur_key = key;
+          // a new A block goes out k block by k block, each A slot right before the B stage of
+          // the same k block (the first MMA needs 32 KB per CTA, not the whole 128 KB of A)
+          for (int kb = kb_lo; kb < kb_hi; ++kb) {
+            if (new_a) {
               const int slot = kb - kb_lo;
               mbar_wait(&L.aempty[slot], ((spar >> slot) & 1) ^ 1);
               spar ^= 1u << slot;
@@ -580,9 +599,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(SimCfg<kMode>::kThre
               }
               __syncwarp();
             }
-            cur_key = key;
-          }
-          for (int kb = kb_lo; kb < kb_hi; ++kb) {
             mbar_wait(&L.empty[stage], phase ^ 1);
             if (issuer) {
               if (rank == 0) mbar_arrive_expect_tx(&L.full[stage], 2 * kStageBytesB);
@@ -596,7 +612,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(SimCfg<kMode>::kThre
         if constexpr (kMode == kSimQ) if (it == 0) load_params(0);
       }
       // the later kernels of the step read the whole gathered buffers: every rank's flag (this
-      // rank's own gather included) is observed before this grid completes
+      // rank's own gather included) is observed before this grid completes (pass 1). For
+      // pass 2: this rank's own gather included, so the step's later bounds reset cannot
+      // precede any of the payload gather's stores
       if (p.local_first) {
         for (int k = 0; k * p.rows_per_src < p.seg[0].cols; ++k) wait_rank(k);
         griddep_launch_dependents();
@@ -628,12 +646,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(SimCfg<kMode>::kThre
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * kPairN;
         int s_, rb_, jt_, half_;
-        decode_item(p, pi, item, s_, rb_, jt_, half_);
+        decode_item<kLF>(p, pi, item, s_, rb_, jt_, half_);
         const uint32_t idesc = half_ < 0 ? idesc_full : idesc_half;
         for (int c = 0; c < n_chunks; ++c) {
           const int kb_lo = c * kSimASlots;
           const int kb_hi = min(nkb, kb_lo + kSimASlots);
-          const int key = a_key(p, pi, item, c, n_chunks);
+          const int key = a_key<kLF>(p, pi, item, c, n_chunks);
           if (key != cur_key) {
             cur_key = key;
             ready = 0;
@@ -641,8 +659,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(SimCfg<kMode>::kThre
           }
           // last use of this A generation: release each slot right after its MMAs
           int nxt_key = -2;
-          if (c + 1 < n_chunks) nxt_key = a_key(p, pi, item, c + 1, n_chunks);
-          else if (item + 1 < it_hi) nxt_key = a_key(p, pi, item + 1, 0, n_chunks);
+          if (c + 1 < n_chunks) nxt_key = a_key<kLF>(p, pi, item, c + 1, n_chunks);
+          else if (item + 1 < it_hi) nxt_key = a_key<kLF>(p, pi, item + 1, 0, n_chunks);
           const bool last_use = nxt_key != key;
           const bool last_chunk = c == n_chunks - 1;
           for (int kb = kb_lo; kb < kb_hi; ++kb) {
@@ -715,7 +733,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(SimCfg<kMode>::kThre
     int it = 0;
     for (int item = it_lo; item < it_hi; ++item, ++it) {
       int s, rb, jt, half;
-      decode_item(p, pi, item, s, rb, jt, half);
+      decode_item<kLF>(p, pi, item, s, rb, jt, half);
       const SimSeg& sg = p.seg[s];
       // a half tile holds its 128 columns in TMEM columns 0..127. FUSED / Q / RAW spread them
       // over all column groups (half the chunks per warp); STATS keeps its 64-column row
@@ -1081,7 +1099,9 @@ cudaError_t sim_set_smem() {
   return e;
 }
 
-cudaError_t sim_stats_attributes(cudaFuncAttributes* a) { return cudaFuncGetAttributes(a, sim_tile_kernel<kSimStats>); }
+cudaError_t sim_attributes(int mode, cudaFuncAttributes* a) {
+  return mode == kSimQ ? cudaFuncGetAttributes(a, sim_tile_kernel<kSimQ>) : cudaFuncGetAttributes(a, sim_tile_kernel<kSimStats>);
+}
 
 cudaError_t launch_sim(int mode, const SimParams& p, const CUtensorMap* mapA, const CUtensorMap* mapB,
                        const CUtensorMap* mapQout, int grid, cudaStream_t s, float* raw_out, bool pdl) {

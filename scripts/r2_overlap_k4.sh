@@ -1,0 +1,10 @@
+# 4 GPUs: multi-rank parity (K = 2 and 4), then step distributions and bench lines vs _ab/lib_prev.so
+export FC_PEER_TIMEOUT_MS=3000
+timeout -s KILL 600 python -m pytest tests/test_gpu_multirank.py -m gpu -q -x 2>&1 | grep -E "passed|failed|Error|assert" | head -8
+for v in new prev; do
+  unset FC_LIB_PATH; [ $v = prev ] && export FC_LIB_PATH=$PWD/_ab/lib_prev.so
+  timeout -s KILL 120 python -m torch.distributed.run --nnodes=1 --nproc-per-node 4 --master-addr 127.0.0.1 --master-port 29516 \
+    scripts/dbg_steps_mr.py 2>&1 | grep "^rank 0" | sed "s/^/$v /"
+  timeout -s KILL 180 python -m torch.distributed.run --nnodes=1 --nproc-per-node 4 --master-addr 127.0.0.1 --master-port 29515 \
+    bench.py --gpus 4 --steps 50 --warmup 5 --no-e2e 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read().strip().splitlines()[-1]); print('bench N=4 $v', round(d['ms_per_step']*1e3,1), 'us')"
+done
