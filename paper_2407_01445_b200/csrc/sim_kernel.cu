@@ -408,8 +408,8 @@ __device__ __forceinline__ void q_chunk(const uint32_t (&r)[32], float rk, float
 
 }  // namespace
 
-// Epilogue width per mode: FUSED runs 8 epilogue warps (128 columns each) so that its wider
-// per-chunk working set (two 32-column transposes) fits the register file; the others run 16.
+// Epilogue shape (every mode): 16 epilogue warps, 4 per TMEM lane quarter, 64 columns each; the
+// FUSED path works in 16-column halves so its transposes fit the 96-register budget.
 template <int kMode>
 struct SimCfg {
   static constexpr int kEpi = kSimEpiWarps;
