@@ -135,10 +135,13 @@ def _check_ranks(K, variant, B, d, N, steps):
             assert np.max(np.abs(got - ref_tab) / np.maximum(np.abs(ref_tab), 1e-300)) < tol, (variant, r, name)
 
 
-def test_nccl_fallback_matches_oracle(monkeypatch):
+@pytest.mark.parametrize("env", [{"FC_PEER": "0"}, {"FC_GATHER_OVERLAP": "0"}], ids=["nccl", "serial_gathers"])
+def test_nccl_fallback_matches_oracle(monkeypatch, env):
     # FC_PEER=0: the NCCL all-gather / all-reduce path (used when GPUs cannot map each other's
-    # memory) gives the same results
-    monkeypatch.setenv("FC_PEER", "0")
+    # memory); FC_GATHER_OVERLAP=0: the peer gathers before the passes instead of beside them --
+    # both give the same results
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
     B, d, N, steps = 512, 128, 8192, 2
     res, refs, st = _run(2, "fastclip_v3", B, d, N, steps)
     Bl = B // 2
