@@ -191,16 +191,24 @@ __device__ __forceinline__ void store_payload(const StepArgs& a, int r, int id, 
 // partial reduction, g and the u EMA (engine.cpp:151-176, state.cpp:45-71), PairWeights and the
 // pass-2 parameters (engine.cpp:37-75), r_i, the local tau-gradient / loss terms (returned for
 // the caller's block reduction) and the packed payload. Every lane of the warp must call it.
-__device__ __forceinline__ void anchor_work(const StepArgs& a, int r, int sub, double& ta, double& tb, double& tl,
-                                            float& kmax) {
+// u^{t-1} of anchor r's id (uo1 / uo2): loaded by the caller before its grid-dependency wait --
+// the tables were last written by the previous step, the ids are the step's input.
+__device__ __forceinline__ void anchor_u_old(const StepArgs& a, int r, int& id, double& uo1, double& uo2) {
+  const int rr = r < a.Bl ? r : 0;
+  id = a.ids[rr];
+  const bool ok = id >= 0 && id < a.n_train;   // out of range: prep reports ShapeError, no table access
+  uo1 = (a.track_u && ok) ? a.u1_tab[id] : 0.0;
+  uo2 = (a.track_u && ok) ? a.u2_tab[id] : 0.0;
+}
+
+__device__ __forceinline__ void anchor_work(const StepArgs& a, int r, int sub, int id, double uo1, double uo2,
+                                            double& ta, double& tb, double& tl, float& kmax) {
   const bool valid = r < a.Bl;
   const int rr = valid ? r : 0;
   // every load of the anchor first (independent, overlapping the partial loads)
   const double gamma = a.scal[0], eps = a.scal[1];
   const double tau = a.tau_state->tau;
-  const int id = a.ids[rr];
   const float kr = a.rowstat_R[rr].x, kc = a.rowstat_C[rr].x;
-  const double uo1 = a.track_u ? a.uold1[rr] : 0.0, uo2 = a.track_u ? a.uold2[rr] : 0.0;
   const double t1 = a.t_loc1[rr], t2 = a.t_loc2[rr];
   const float s_ii = a.diag[a.row0 + rr];
   double s1, x1, s2, x2;

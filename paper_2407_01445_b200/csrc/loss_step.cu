@@ -320,7 +320,7 @@ struct LossStep {
     clamps = dalloc<unsigned long long>(1);
     bounds = dalloc<float>(2 * 4 * fc::kMaxPeers);   // one {norm1, norm2, kappa, -} slot per rank and parity
     FC_CUDA(cudaMemset(bounds, 0, 2 * 4 * fc::kMaxPeers * sizeof(float)));
-    f64 = dalloc<double>(static_cast<size_t>(Bl) * 18);
+    f64 = dalloc<double>(static_cast<size_t>(Bl) * 13);   // F(0) .. F(12) below
     nblk = (Bl * fc::kAnchorLanes + kAnchorBlock - 1) / kAnchorBlock;
     pstride = (7 * Bl + 3 * nblk + 1) & ~1;   // even: 16-byte slices for the peer gather
     send = dalloc<double>(static_cast<size_t>(pstride));
@@ -451,7 +451,6 @@ struct LossStep {
     a.g1 = F(6); a.g2 = F(7); a.u1 = F(8); a.u2 = F(9);
     a.term_a = F(10); a.term_b = F(11); a.term_loss = F(12);
     a.gt1 = send + 5 * static_cast<size_t>(Bl); a.gt2 = send + 6 * static_cast<size_t>(Bl);   // payload columns
-    a.uold1 = F(15); a.uold2 = F(16);
     a.send = send; a.recv = recv;
     a.pstride = pstride; a.nblk = nblk;
     const size_t np = static_cast<size_t>(n_jt) * fc::kPairN;

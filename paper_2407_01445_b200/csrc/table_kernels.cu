@@ -3,8 +3,9 @@
 // These are latency-bound gather/scatter and scalar kernels (no tensor-core shape):
 //   fc_prep_kernel        S_ii = <E1_i, E2_i> and the row-norm bounds for the global batch;
 //                         tau^t snapshot (global tau or IndividualTemp by id, state.cpp:112-122)
-//                         and u^{t-1} gather for the local anchors -> pass-1 row parameters
-//   fc_anchor_kernel      per local anchor: fixed-order reduction of the pass-1 partials -> g
+//                         for the local anchors -> pass-1 row parameters
+//   fc_anchor_kernel      per local anchor: u^{t-1} gather by id (before its grid wait), then
+//                         the fixed-order reduction of the pass-1 partials -> g
 //                         (engine.cpp:151-176), UTable EMA + snapshot (state.cpp:45-71),
 //                         PairWeights (engine.cpp:37-75), pass-2 parameters, r_i, the local
 //                         tau-gradient / loss terms and the packed payload (+ block partials)
@@ -87,9 +88,9 @@ __global__ void fc_prep_kernel(const __nv_bfloat16* __restrict__ e1, const __nv_
     }
   };
   // u^{t-1} / tau^t of the anchor's id: gathered here, off the table kernel's dependent chain
-  double uo1 = 0.0, uo2 = 0.0, t1 = 0.0, t2 = 0.0;
+  // tau^t of the anchor's id (pass 1 needs kappa_i); u^{t-1} is gathered by the per-anchor kernel
+  double t1 = 0.0, t2 = 0.0;
   if (lead) {
-    if (a.track_u) { uo1 = a.u1_tab[id]; uo2 = a.u2_tab[id]; }
     if (a.individual) { t1 = a.tau1_tab[id]; t2 = a.tau2_tab[id]; }
     else { t1 = t2 = a.tau_state->tau; }
   }
@@ -116,10 +117,6 @@ __global__ void fc_prep_kernel(const __nv_bfloat16* __restrict__ e1, const __nv_
   if (lane != 0 || !valid) return;
   a.diag[wg] = acc;
   if (!lead) return;
-  if (a.track_u) {
-    a.uold1[r] = uo1;
-    a.uold2[r] = uo2;
-  }
   a.t_loc1[r] = t1;
   a.t_loc2[r] = t2;
 
@@ -214,14 +211,18 @@ __device__ __forceinline__ long long gtime() {
 
 __global__ void __launch_bounds__(128) fc_anchor_kernel(StepArgs a) {
   long long t_entry = (kProfStamps && a.dbg) ? gtime() : 0;
+  const int r = (blockIdx.x * blockDim.x + threadIdx.x) / kGroup;
+  const int sub = threadIdx.x % kGroup;
+  // the u^{t-1} gather by id (two dependent DRAM round trips) while pass 1 drains
+  int id;
+  double uo1, uo2;
+  anchor_u_old(a, r, id, uo1, uo2);
   asm volatile("griddepcontrol.wait;" ::: "memory");   // pass-1 partials (programmatic launch)
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   long long t_wait = (kProfStamps && a.dbg) ? gtime() : 0;
-  const int r = (blockIdx.x * blockDim.x + threadIdx.x) / kGroup;
-  const int sub = threadIdx.x % kGroup;
   double ta = 0.0, tb = 0.0, tl = 0.0;
   float kmax = 0.f;
-  anchor_work(a, r, sub, ta, tb, tl, kmax);
+  anchor_work(a, r, sub, id, uo1, uo2, ta, tb, tl, kmax);
   if (kProfStamps && a.dbg && threadIdx.x == 0) a.dbg[blockIdx.x * 8 + 3] = gtime();
   block_partials(a, ta, tb, tl, kmax);
   if (kProfStamps && a.dbg && threadIdx.x == 0) { a.dbg[blockIdx.x * 8 + 0] = t_entry; a.dbg[blockIdx.x * 8 + 1] = t_wait; a.dbg[blockIdx.x * 8 + 4] = gtime(); }

@@ -60,7 +60,6 @@ struct StepArgs {
   double* g1; double* g2; double* u1; double* u2;
   double* term_a; double* term_b; double* term_loss;
   double* gt1; double* gt2;              // v2 tau gradients, contiguous [gt1 | gt2] (send)
-  double* uold1; double* uold2;          // u^{t-1} of the local ids, gathered by the prep kernel
   // packed per-rank payload (all-gathered at K > 1; recv == send at K == 1):
   //   [u1 | u2 | t1 | t2 | id | gt1 | gt2] x Bl, then nblk x {G_tau term a, term b, loss}
   // so one all-gather carries the per-sample scalars, the v2 per-index tau gradients and the
