@@ -18,6 +18,7 @@
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
 #include <nccl.h>
+#include <nvtx3/nvtx3.hpp>   // header-only ranges: no-ops unless a tool injects a collector
 
 #include <cmath>
 #include <cstdio>
@@ -655,6 +656,7 @@ struct LossStep {
   // Validates, stages the step scalars and runs the step on the context stream: replayed
   // from a CUDA graph captured per (input, output) pointer set, or enqueued directly.
   void step(const fc_step_in* in, fc_step_out* out, cudaStream_t caller) {
+    nvtx3::scoped_range nvtx_step{"fc_loss_step"};
     if (!in || !out || !in->e1 || !in->e2 || !in->ids || !out->de1 || !out->de2)
       throw FcError{FC_ERR_SHAPE, "fc_loss_step: null input/output pointer"};
     if (in->eps < 0.0) throw FcError{FC_ERR_DOMAIN, "epsilon must be non-negative"};
@@ -674,6 +676,7 @@ struct LossStep {
           graphs.erase(graphs.begin());
         }
         GraphEntry g{};
+        nvtx3::scoped_range nvtx_cap{"fc_loss_step: capture + instantiate the step graph"};
         FC_CUDA(cudaStreamBeginCapture(ws, cudaStreamCaptureModeThreadLocal));
         try {
           enqueue(in, out, ws);
