@@ -10,7 +10,10 @@
 // (relaxed polling, then a system-scope acquire fence). The kernel therefore
 // completes only when the whole gathered buffer is in local HBM -- a stream-ordered all-gather
 // with no NCCL launch and no proxy thread (~20-30 us per NCCL gather on this system vs a few
-// microseconds of NVLink traffic for the payload and ~2.6 MB embedding slices).
+// microseconds of NVLink traffic for the payload and ~2.6 MB embedding slices). With the
+// overlapped step (loss_step.cu) the gathers run on their own stream and the passes that read
+// their data poll the same flags inside their grids; those launches use the lean variant below,
+// whose CTAs fit beside a similarity-pass CTA.
 #include <cstdint>
 
 #include <cuda_runtime.h>
@@ -133,7 +136,7 @@ __device__ void gather_lsu(const PeerGather& g, int t0, int t1) {
   }
 }
 
-// kLean: the embedding gather that runs beside pass 1 (whose producer waits for its flags), so
+// kLean: a gather that runs beside pass 1 / pass 2 (whose producers wait for its flags), so
 // one of its CTAs must fit next to a pass-1 CTA: 128 threads at <= 32 registers (1024 per warp --
 // what the pass-1 CTA's 96-register warps leave free on its two fuller SM sub-partitions),
 // two loads in flight. Otherwise up to 256 threads, four loads in flight.
