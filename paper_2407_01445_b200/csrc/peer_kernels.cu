@@ -136,10 +136,6 @@ __device__ void gather_lsu(const PeerGather& g, int t0, int t1) {
   }
 }
 
-// kLean: a gather that runs beside pass 1 / pass 2 (whose producers wait for its flags), so
-// one of its CTAs must fit next to a pass-1 CTA: 128 threads at <= 32 registers (1024 per warp --
-// what the pass-1 CTA's 96-register warps leave free on its two fuller SM sub-partitions),
-// two loads in flight. Otherwise up to 256 threads, four loads in flight.
 // Two equal-size sources (the embedding slices), lean CTAs: chunk i of both and chunk i + stride
 // of both -- four 16-byte loads in flight per thread within the 32-register budget.
 __device__ void gather_pair_lean(const PeerGather& g) {
@@ -163,6 +159,11 @@ __device__ void gather_pair_lean(const PeerGather& g) {
   }
 }
 
+// kLean: a gather that runs beside pass 1 / pass 2 (whose producers wait for its flags), so one
+// of its CTAs must fit next to a similarity-pass CTA: 128 threads at <= 32 registers (1024 per
+// warp -- what the pass CTA's 96-register warps leave free on its two fuller SM sub-partitions);
+// the embedding slices with four loads in flight per thread, the payload's small sources with
+// one. Otherwise up to 256 threads, four loads in flight.
 template <bool kLean>
 __global__ void __launch_bounds__(kLean ? 128 : 256, kLean ? 16 : 1) peer_gather_kernel(PeerGather g) {
   constexpr int kU = 4;
